@@ -1,0 +1,367 @@
+#!/usr/bin/env python
+"""Benchmark: spin flips/ns of the multi-spin checkerboard Metropolis sweep on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c3|c4|c5]
+
+A step is one full sweep (black + white half-sweep) of the whole lattice.  N = 1 runs
+BASELINE.json configs[2] (C3: 32768 x 32768, beta = 0.4406868, random start, seed 1).
+N > 1 (launched by torch.distributed.run, one process per GPU) weak-scales C3: each
+rank owns a 32768 x 32768 slab of an (N*32768) x 32768 lattice and exchanges halo rows
+with ncclSend/ncclRecv ("scaling": "weak").  --config c4 strong-scales 131072^2,
+--config c5 weak-scales 131072 x 1048576 per GPU.
+
+value: flips/ns over the K timed sweeps, device-timed with CUDA events on the launching
+stream inside the library, max over ranks.  e2e: the same workload through the C ABI with
+host buffers — write_lattice from pinned host memory, K sweeps, observables each sweep,
+read_lattice back — all inside the timed region.  --impl reference times the CPU oracle
+(oracle/, the "reference arm" of this tier) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BETA = 0.4406868
+SEED = 1
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+BYTES_PER_FLIP = 1.5  # 4-bit spins: read target + read source + write target
+
+
+def config_for(name: str, n: int):
+    if name == "c3":
+        return 32768 * n, 32768, "weak", f"C3 32768x32768 per GPU (BASELINE configs[2]); lattice {32768 * n}x32768"
+    if name == "c4":
+        return 131072, 131072, "strong", "C4 131072x131072 strong-scaled (BASELINE configs[3])"
+    if name == "c5":
+        return 131072 * n, 1048576, "weak", f"C5 131072x1048576 per GPU (BASELINE configs[4]); lattice {131072 * n}x1048576"
+    if name == "c2":
+        return 2048 * n, 2048, "weak", f"C2 2048x2048 per GPU (BASELINE configs[1] shape); lattice {2048 * n}x2048"
+    raise SystemExit(f"unknown config {name}")
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.idx = device_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.th.join(timeout=2)
+        sm, smax, pw, reasons = [], None, [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+                pw.append(float(f[3]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {
+            "sm_mhz": statistics.median(sm) if sm else None,
+            "sm_max_mhz": smax,
+            "power_w_median": statistics.median(pw) if pw else None,
+            "samples": len(sm),
+            "reasons": sorted(reasons),
+        }
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def measured_peaks():
+    try:
+        with open(PEAKS_FILE) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+# --------------------------------------------------------------------- oracle
+def oracle_rate(rows: int, cols: int, sweeps: int, threads: int | None = None):
+    """Oracle (oracle/ising_oracle.c, as it stands) flips/ns on a rows x cols torus."""
+    import oracle
+
+    if threads:
+        oracle.set_threads(threads)
+    lat = oracle.Lattice(rows, cols, SEED).init_random().set_beta(BETA)
+    lat.sweep(1)  # warm caches / page in
+    t0 = time.perf_counter()
+    lat.sweep(sweeps)
+    dt = time.perf_counter() - t0
+    return rows * cols * sweeps / (dt * 1e9), oracle.get_threads(), dt
+
+
+def cpu_baseline(cols: int) -> dict:
+    # bounded sample of the workload: 2048 full-width rows of the C3 lattice (a
+    # 2048 x cols torus), sweeps sized for ~10-20 s of CPU work on the box's cores
+    rows = 2048
+    rate, cores, dt = oracle_rate(rows, cols, 1)
+    sweeps = max(1, min(16, int(12.0 / max(dt, 1e-3))))
+    rate, cores, dt = oracle_rate(rows, cols, sweeps)
+    return {"value": rate, "unit": "flips/ns", "cores": cores, "kind": "oracle",
+            "sample": f"{rows}x{cols} torus (C3 row width), beta={BETA}, random start seed {SEED}, "
+                      f"{sweeps} sweeps, {dt:.1f} s, OpenMP over rows of a colour phase"}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    N, M, scaling, workload = config_for(args.config, world)
+    import oracle
+
+    rows = 2048  # bounded sample: 2048 full-width rows per step
+    lat = oracle.Lattice(rows, M, SEED).init_random().set_beta(BETA)
+    for _ in range(args.warmup):
+        lat.sweep(1)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        lat.sweep(1)
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    value = rows * M * args.steps / (total * 1e9)
+    cores = oracle.get_threads()
+    line = {
+        "impl": "reference", "metric": "spin flips/ns (attempted updates, host-timed)", "value": value,
+        "unit": "flips/ns", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": scaling,
+        "vs_baseline": None, "dtype": "i8", "data": "synthetic",
+        "config": {"workload": workload, "sample": f"{rows}x{M} torus per step (bounded sample)",
+                   "beta": BETA, "seed": SEED},
+        "cpu_baseline": {"value": value, "unit": "flips/ns", "cores": cores, "kind": "oracle",
+                         "sample": f"{rows}x{M} torus, {args.steps} sweeps"},
+        "e2e": {"value": value, "unit": "flips/ns", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------ ours
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    from paper_1906_06297_b200.ising import IsingLattice, ising_probe_philox
+
+    rank, world, local = dist_env()
+    assert world == args.gpus or world == 1, "launch N>1 with torch.distributed.run"
+    n = world
+    torch.cuda.set_device(local)
+    dist = None
+    if n > 1:
+        import torch.distributed as dist_mod
+
+        dist = dist_mod
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    N, M, scaling, workload = config_for(args.config, n)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def allmax(x: float) -> float:
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    if n > 1:
+        lat = IsingLattice.distributed(N, M, SEED, device=local)
+    else:
+        lat = IsingLattice(N, M, SEED, n_gpus=1)
+    row0, rows = lat.slab_info()
+    lat.set_beta(BETA).init_random()
+    lat.sweep(args.warmup)
+
+    # ---- device-timed region: K sweeps, events inside the library ----
+    clk = ClockSampler(local)
+    barrier()
+    clk.start()
+    time.sleep(0.3)
+    l0 = lat.launch_count()
+    lat.sweep(args.steps)
+    launches = lat.launch_count() - l0
+    ms = lat.last_sweep_ms()
+    barrier()
+    clocks = clk.stop()
+    ms = allmax(ms)
+    value = N * M * args.steps / (ms * 1e6)
+
+    # ---- per-launch kernel timing (profiling on: one event pair per launch) ----
+    lat.set_profiling(True)
+    kprof_sweeps = max(2, min(args.steps, 16))
+    lat.sweep(kprof_sweeps)
+    kms, klaunches = lat.kernel_stats()
+    sweep_ms_prof = lat.last_sweep_ms()
+    lat.set_profiling(False)
+    # dominant kernel = k_halfsweep; flips per launch = slab rows * M / 2 for n == 1
+    flips_per_launch = rows * M * 2 * kprof_sweeps / max(klaunches, 1)
+    avg_launch_ms = kms / max(klaunches, 1)
+    peaks, peak_src = measured_peaks()
+    hbm_gbs = BYTES_PER_FLIP * flips_per_launch / (avg_launch_ms * 1e6)
+
+    # ---- ALU roofline denominator: Philox-only draws/ns on this device, now ----
+    philox_peak = ising_probe_philox(local)
+    flips_per_ns_kernel = flips_per_launch / (avg_launch_ms * 1e6)
+
+    # ---- end to end through the C ABI with host buffers ----
+    e2e = None
+    if N * M <= (1 << 34):  # host copy of the full int8 lattice (C5 would need 1 TiB)
+        full = torch.empty((N, M), dtype=torch.int8, pin_memory=True)
+        lat.read_lattice(full.numpy())  # current state as the e2e input (rank rows only)
+        if n > 1:
+            # every rank needs the whole input lattice: rank mode writes its own rows and halos
+            g = torch.empty((N, M), dtype=torch.int8, device="cuda")
+            g[row0:row0 + rows].copy_(full[row0:row0 + rows])
+            # gather slabs (each rank's rows) into every rank's buffer
+            parts = [torch.empty((rows, M), dtype=torch.int8, device="cuda") for _ in range(n)]
+            dist.all_gather(parts, g[row0:row0 + rows].contiguous())
+            full.copy_(torch.cat(parts).cpu())
+            del g, parts
+        out = torch.empty((N, M), dtype=torch.int8, pin_memory=True)
+        barrier()
+        t0 = time.perf_counter()
+        lat.write_lattice(full.numpy(), t=0)
+        obs = []
+        for _ in range(args.steps):
+            lat.sweep(1)
+            obs.append(lat.observables())
+        lat.read_lattice(out.numpy())
+        barrier()
+        e2e_s = allmax(time.perf_counter() - t0)
+        e2e = {
+            "value": N * M * args.steps / (e2e_s * 1e9),
+            "unit": "flips/ns",
+            "h2d_bytes_per_step": rows * M // args.steps if n > 1 else N * M // args.steps,
+            "d2h_bytes_per_step": (rows * M if n > 1 else N * M) // args.steps + 16,
+            "how": "write_lattice(pinned int8) + per sweep: ising_sweep(1) + ising_observables; "
+                   "read_lattice(pinned int8); wall clock, max over ranks",
+        }
+        del full, out
+
+    cpu = None
+    if rank == 0 and n == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(M)
+
+    if rank == 0:
+        line = {
+            "metric": "spin flips/ns (device-timed)",
+            "value": value,
+            "unit": "flips/ns",
+            "n_gpus": n,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms / args.steps,
+            "higher_is_better": True,
+            "scaling": scaling,
+            "vs_baseline": None,
+            "dtype": "u32",
+            "data": "synthetic",
+            "config": {
+                "workload": workload,
+                "lattice": [N, M],
+                "beta": BETA,
+                "seed": SEED,
+                "start": "random",
+                "parallelism": f"slab{n}",
+                "l2": f"inputs larger than L2: packed planes {N * M // 2 / 2**20:.0f} MiB per "
+                      f"{'GPU' if n == 1 else 'lattice'} vs 126 MB L2; no flush",
+            },
+            "roofline": {
+                "bound": "alu",
+                "achieved": flips_per_ns_kernel,
+                "peak": philox_peak,
+                "unit": "flips/ns",
+                "frac": flips_per_ns_kernel / philox_peak,
+                "traffic": None,
+                "kernel": "k_halfsweep<0>",
+                "avg_launch_ms": avg_launch_ms,
+                "launches": klaunches,
+                "kernel_share_of_step": kms / max(sweep_ms_prof, 1e-9),
+                "peak_source": "Philox4x32-10-only draws/ns measured in this run (ising_probe_philox); "
+                               "1 draw per attempted flip",
+                "hbm": {"achieved_gbs": hbm_gbs, "peak_gbs": peaks.get("hbm_gbs"),
+                        "frac": hbm_gbs / peaks.get("hbm_gbs", 6650.0), "peak_source": peak_src,
+                        "bytes_per_flip": BYTES_PER_FLIP},
+            },
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    lat.close()
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=64)
+    ap.add_argument("--warmup", type=int, default=8)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="c3", choices=["c2", "c3", "c4", "c5"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        raise SystemExit("--warmup must be >= 3")
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

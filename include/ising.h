@@ -1,0 +1,173 @@
+/*
+ * include/ising.h — C ABI of the B200 checkerboard-Metropolis library (libising.so).
+ *
+ * The library runs the hot path of arXiv 1906.06297: the checkerboard
+ * (red/black) Metropolis sweep of the 2D ferromagnetic Ising model on an
+ * L_rows x L_cols periodic lattice, "update all the spins of one color in parallel,
+ * keeping the other color constant, and then repeat the process with the opposite
+ * color" (§2), with the multi-spin coding of §3.3:
+ * the two colours live in separate arrays, four bits per spin, sixteen spins per
+ * 64-bit word, and each half-sweep is one sm_100a kernel that forms the four
+ * neighbour sums of a whole word with word-wide adds, draws an inline counter-based
+ * Philox4x32-10 number per spin and accepts with an integer threshold.
+ *
+ * Conventions:
+ *   - J = 1; beta = 1/T.  Site (i, J) is black iff i + J is even (R1).
+ *   - Draw for plane site (i, j = J/2) of colour c (0 black, 1 white) in sweep t:
+ *       r = Philox4x32-10(ctr = {j/4, i, t, c}, key = {lo32(seed), hi32(seed)})[j % 4] (R6).
+ *   - Metropolis: with e = s*h (h = sum of the 4 neighbours),
+ *     flip iff e <= 0 or r < T[e], T[e] = min(2^32, ceil(2^32 exp(-2 beta e))) (R5),
+ *     computed on the host in IEEE double.  Heat bath:
+ *     flip iff r < ceil(2^32 p/(1+p)), p = exp(-2 beta e), for every e.
+ *   - One sweep = black half-sweep then white half-sweep; sweeps are numbered
+ *     t = 1, 2, ...; t = 0 is the random initialisation (R7, R8).
+ *
+ * Status: every call returns ISING_OK (0) or a negative ising_status.  No C++
+ * exception crosses the ABI.  A handle is not thread-safe.  The library owns the
+ * handle and all device memory; the caller owns every host buffer it passes.
+ * Calls that return data synchronise.  ising_sweep returns after the sweeps have
+ * completed on every device of the handle.
+ */
+#ifndef ISING_H
+#define ISING_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ising_ctx* ising_t;
+
+enum ising_status {
+  ISING_OK = 0,
+  ISING_ERR_ARG = -1,    /* invalid argument (shape, beta, pointer, length) */
+  ISING_ERR_STATE = -2,  /* call order: sweep before set_beta + init, etc.   */
+  ISING_ERR_DEVICE = -3, /* no / too few sm_100 devices, bad device index    */
+  ISING_ERR_OOM = -4,    /* device or pinned host allocation failed          */
+  ISING_ERR_CUDA = -5,   /* CUDA runtime error (message via ising_last_error)*/
+  ISING_ERR_NCCL = -6,   /* NCCL error                                       */
+  ISING_ERR_RANGE = -7   /* sweep counter would exceed 2^32 - 1; short buffer*/
+};
+
+enum ising_rule {
+  ISING_RULE_METROPOLIS = 0, /* PAPER.md:36-42 (the path)                    */
+  ISING_RULE_HEATBATH = 1
+};
+
+/* ---------------------------------------------------------------- lifetime */
+
+/* Create a lattice of L_rows x L_cols spins split into n_gpus row slabs on CUDA
+ * devices 0..n_gpus-1 of this process (§4: "partitioned into
+ * horizontal slabs and each GPU stores one slab").  Requirements: L_rows even,
+ * L_rows % n_gpus == 0, L_rows / n_gpus >= 2, L_cols % 64 == 0, L_cols >= 64.
+ * Neighbouring slabs exchange boundary rows by direct peer stores from the
+ * half-sweep kernel (NVLink P2P).  *out receives the handle.
+ * Errors: ARG (shape, NULL out), DEVICE (fewer than n_gpus sm_100 devices or no
+ * P2P between neighbours), OOM, CUDA. */
+int ising_create(ising_t* out, int64_t L_rows, int64_t L_cols, uint64_t seed, int n_gpus);
+
+/* As ising_create, with an explicit device for each of n_slabs slabs
+ * (devices[k] for global rows [k R, (k+1) R), R = L_rows / n_slabs).  Devices may
+ * repeat: slabs on the same device exchange halos through that device's memory.
+ * This is how slab decomposition is exercised on a single GPU. */
+int ising_create_slabs(ising_t* out, int64_t L_rows, int64_t L_cols, uint64_t seed, int n_slabs,
+                       const int* devices);
+
+/* One process per GPU (torchrun): this process owns slab `rank` of `world` on CUDA
+ * device `device`; halo rows move by ncclSend/ncclRecv (NCCL over NVLink) overlapped
+ * with the interior update.  nccl_id points to id_len (= 128) bytes produced by
+ * ising_nccl_unique_id on rank 0 and broadcast by the caller (e.g. torch.distributed).
+ * With world == 1 nccl_id may be NULL.  Collective: all ranks must call it. */
+int ising_create_rank(ising_t* out, int64_t L_rows, int64_t L_cols, uint64_t seed, int rank,
+                      int world, int device, const void* nccl_id, size_t id_len);
+
+/* Writes an NCCL unique id (id_len >= 128 bytes) into id. */
+int ising_nccl_unique_id(void* id, size_t id_len);
+
+/* Releases all device memory, streams and communicators.  NULL is a no-op. */
+int ising_destroy(ising_t h);
+
+/* --------------------------------------------------------------- parameters */
+
+/* beta = J/T in [0, +inf]; NaN or negative -> ARG.  Computes the integer
+ * thresholds on the host (R5). */
+int ising_set_beta(ising_t h, double beta);
+
+/* ISING_RULE_METROPOLIS (default) or ISING_RULE_HEATBATH; takes effect at the
+ * next set_beta.  Other values -> ARG. */
+int ising_set_rule(ising_t h, int rule);
+
+/* ------------------------------------------------------------------- state */
+
+/* Random start: spin = +1 iff r(seed, t=0, c, i, j) < 2^31 (R8).  Sets t := 0. */
+int ising_init_random(ising_t h);
+
+/* Cold start: all spins +1.  Sets t := 0. */
+int ising_init_cold(ising_t h);
+
+/* Load a full lattice from host memory: in[i*L_cols + J] in {-1, +1}, row-major,
+ * in_len >= L_rows*L_cols (else RANGE); any other value -> ARG.  Sets the sweep
+ * counter to t (the next sweep is t+1) — with the counter-based draws this is an
+ * exact resume (checkpoint/restart).  In rank mode every rank
+ * passes the full lattice and keeps its own rows. */
+int ising_write_lattice(ising_t h, const int8_t* in, int64_t in_len, uint64_t t);
+
+/* Run n >= 0 full sweeps (black then white), t += n.  STATE if set_beta or an
+ * init/write has not happened; RANGE if t + n > 2^32 - 1.  Returns after
+ * completion.  Collective in rank mode. */
+int ising_sweep(ising_t h, int64_t n);
+
+/* Unpack to host: out[i*L_cols + J] = spin (i, J) in {-1, +1}, row-major;
+ * out_len >= L_rows*L_cols (else RANGE).  In rank mode only this rank's rows
+ * are written. */
+int ising_read_lattice(ising_t h, int8_t* out, int64_t out_len);
+
+/* Integer observables of the whole lattice (Eq. 1):
+ * *up_count = number of +1 spins; *bond_energy = -sum over the 2 N M torus bonds
+ * of s s' (each bond once, R11), in [-2NM, 2NM].  STATE before an init.
+ * Collective in rank mode (int64 all-reduce over NCCL). */
+int ising_observables(ising_t h, int64_t* up_count, int64_t* bond_energy);
+
+/* ------------------------------------------------------------ introspection */
+
+/* CUDA-event time of the last ising_sweep on this process's devices (max over
+ * devices), milliseconds. */
+int ising_last_sweep_ms(ising_t h, double* device_ms);
+
+/* Per-launch timing of the half-sweep kernels of the last ising_sweep when
+ * profiling is enabled (ising_set_profiling(h, 1)): *kernel_ms = summed CUDA-event
+ * duration of the half-sweep launches on the first device's stream, *launches = how
+ * many.  Profiling adds one event pair per launch. */
+int ising_set_profiling(ising_t h, int enable);
+int ising_kernel_stats(ising_t h, double* kernel_ms, int64_t* launches);
+
+/* Current sweep counter t. */
+int ising_get_sweep(ising_t h, uint64_t* t);
+
+/* This process's slab: first global row and number of rows (all rows for
+ * ising_create / ising_create_slabs handles). */
+int ising_slab_info(ising_t h, int64_t* row0, int64_t* rows);
+
+/* Thresholds the kernels use for the current beta and rule: T[k] for e = 2k - 4,
+ * k = 0..4 (2^32 means "always").  Host-side; for tests and reports. */
+int ising_thresholds(ising_t h, uint64_t T[5]);
+
+/* Number of kernel launches issued by this handle since creation. */
+int ising_launch_count(ising_t h, int64_t* launches);
+
+/* Diagnostic: Philox4x32-10-only draw throughput of CUDA device `device` (the same
+ * device function the half-sweep uses, outputs XOR-folded), in draws per ns — the
+ * measured ALU roofline of the path (every attempted flip consumes one draw). */
+int ising_probe_philox(int device, double* draws_per_ns);
+
+const char* ising_strerror(int status);
+
+/* Message of the last CUDA/NCCL error seen by this thread ("" if none). */
+const char* ising_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ISING_H */

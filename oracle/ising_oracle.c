@@ -187,6 +187,7 @@ void oracle_sweep(int8_t* black, int8_t* white, int64_t nx, int64_t ny, uint64_t
 void oracle_init_random(int8_t* black, int8_t* white, int64_t nx, int64_t ny, uint64_t seed) {
   for (int c = 0; c < 2; ++c) {
     int8_t* plane = c == 0 ? black : white;
+#pragma omp parallel for schedule(static) if (nx * ny >= 65536)
     for (int64_t i = 0; i < nx; ++i)
       for (int64_t j = 0; j < ny; ++j)
         plane[i * ny + j] = oracle_rand(seed, 0, (uint32_t)c, (uint32_t)i, (uint64_t)j) < 0x80000000u
@@ -207,6 +208,7 @@ void oracle_init_cold(int8_t* black, int8_t* white, int64_t nx, int64_t ny) {
 void oracle_full_lattice(const int8_t* black, const int8_t* white, int64_t nx, int64_t ny,
                          int8_t* out) {
   int64_t M = 2 * ny;
+#pragma omp parallel for schedule(static) if (nx * ny >= 65536)
   for (int64_t i = 0; i < nx; ++i)
     for (int64_t J = 0; J < M; ++J)
       out[i * M + J] = ((i + J) % 2 == 0) ? black[i * ny + J / 2] : white[i * ny + J / 2];
@@ -230,6 +232,7 @@ void oracle_observables(const int8_t* black, const int8_t* white, int64_t nx, in
                         int64_t* up, int64_t* energy) {
   int64_t M = 2 * ny;
   int64_t u = 0, E = 0;
+#pragma omp parallel for schedule(static) reduction(+ : u, E) if (nx * ny >= 65536)
   for (int64_t i = 0; i < nx; ++i) {
     for (int64_t J = 0; J < M; ++J) {
       int64_t ir = i, Jr = (J + 1) % M, id = (i + 1) % nx, Jd = J;

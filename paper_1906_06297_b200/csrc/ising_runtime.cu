@@ -1,0 +1,863 @@
+// ising_runtime.cu — host runtime behind include/ising.h.
+//
+// Owns the per-device slabs (two padded colour planes each), streams, events,
+// the NCCL communicator of rank mode, the host-side threshold table and the sweep
+// counter.  Every step of the path runs in the kernels of ising_kernels.cu; this
+// file only allocates, launches, synchronises and exchanges halo rows.
+//
+// Multi-GPU (§4): the lattice is split into row
+// slabs.  Handle modes:
+//   LOCAL (ising_create / ising_create_slabs): one process drives every slab; the
+//     half-sweep kernel stores its boundary rows straight into the neighbouring
+//     slab's halo row (same device, or a peer device over NVLink P2P), and each
+//     phase waits on the neighbours' previous phase (RAW on the halo it reads, WAR
+//     on the halo it writes).
+//   RANK (ising_create_rank): one process per GPU; per phase the two boundary
+//     rows are updated first, then ncclSend/ncclRecv move them on a comm stream
+//     while the interior rows update (the classic halo/bulk overlap the paper cites,
+//     PAPER.md:224).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/ising.h"
+#include "ising_kernels.cuh"
+
+namespace ising {
+__global__ void k_init(const InitParams p);
+__global__ void k_observables(const ObsParams p);
+__global__ void k_pack(const PackParams p);
+__global__ void k_unpack(const UnpackParams p);
+}  // namespace ising
+
+using namespace ising;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail_cuda(cudaError_t e, const char* what, int line) {
+  char buf[512];
+  snprintf(buf, sizeof buf, "%s: %s (ising_runtime.cu:%d)", what, cudaGetErrorString(e), line);
+  g_last_error = buf;
+  return e == cudaErrorMemoryAllocation ? ISING_ERR_OOM : ISING_ERR_CUDA;
+}
+
+int fail_nccl(ncclResult_t r, const char* what, int line) {
+  char buf[512];
+  snprintf(buf, sizeof buf, "%s: %s (ising_runtime.cu:%d)", what, ncclGetErrorString(r), line);
+  g_last_error = buf;
+  return ISING_ERR_NCCL;
+}
+
+#define CU(x)                                                  \
+  do {                                                         \
+    cudaError_t e_ = (x);                                      \
+    if (e_ != cudaSuccess) return fail_cuda(e_, #x, __LINE__); \
+  } while (0)
+
+#define NC(x)                                                   \
+  do {                                                          \
+    ncclResult_t r_ = (x);                                      \
+    if (r_ != ncclSuccess) return fail_nccl(r_, #x, __LINE__);  \
+  } while (0)
+
+#define TRY(x)                 \
+  do {                         \
+    int s_ = (x);              \
+    if (s_ != ISING_OK) return s_; \
+  } while (0)
+
+constexpr size_t kStagingBytes = size_t(64) << 20;  // pack/unpack staging chunk
+
+struct Device {
+  int dev = -1;
+  int sms = 0;
+  int hs_blocks_per_sm = 0;  // occupancy of k_halfsweep<0>
+  cudaStream_t stream = nullptr;
+  cudaStream_t comm = nullptr;
+  cudaEvent_t ev_phase = nullptr;  // end of the latest phase on this device
+  cudaEvent_t ev_bnd = nullptr;    // rank mode: boundary rows done
+  cudaEvent_t ev_comm = nullptr;   // rank mode: halo exchange done
+  cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;
+  int8_t* staging = nullptr;
+  unsigned long long* red = nullptr;  // [0] up, [1] antiparallel, [2] bad-value flag
+};
+
+struct Slab {
+  int devi = 0;      // index into ctx->devs
+  int64_t row0 = 0;  // global row of local row 0
+  int64_t R = 0;
+  uint64_t* plane[2] = {nullptr, nullptr};  // (R + 2) x W words each
+};
+
+}  // namespace
+
+struct ising_ctx {
+  int64_t N = 0, M = 0, W = 0;
+  uint64_t seed = 0;
+  bool rank_mode = false;
+  int rank = 0, world = 1;
+  ncclComm_t comm = nullptr;
+  std::vector<Device> devs;
+  std::vector<Slab> slabs;
+  std::vector<int> slab_of_rank;  // unused in local mode
+  int rule = ISING_RULE_METROPOLIS;
+  double beta = 0;
+  bool beta_set = false, state_set = false;
+  uint64_t T[5] = {0, 0, 0, 0, 0};
+  Accept acc{};
+  PhiloxKeys keys{};
+  uint64_t t = 0;
+  double last_ms = 0;
+  bool profiling = false;
+  double kernel_ms = 0;
+  int64_t kernel_launches = 0;
+  int64_t launch_count = 0;
+  std::vector<cudaEvent_t> prof_events;
+  int rows_per_item_override = 0;
+};
+
+namespace {
+
+// ------------------------------------------------------------ thresholds
+// Reading R5: u = r 2^-32 < P  <=>  r < ceil(2^32 P) (ldexp is exact; the only
+// rounding is the host libm exp).  2^32 encodes "always".
+uint64_t ceil_2p32(double P) {
+  if (!(P > 0.0)) return 0;
+  if (P >= 1.0) return uint64_t(1) << 32;
+  const double x = std::ceil(std::ldexp(P, 32));
+  if (x >= 4294967296.0) return uint64_t(1) << 32;
+  return (uint64_t)x;
+}
+
+void compute_thresholds(double beta, int rule, uint64_t T[5]) {
+  for (int a = 0; a < 5; ++a) {
+    const int e = 2 * a - 4;  // e = s * h, dE = 2 e (J = 1)
+    double P;
+    if (rule == ISING_RULE_METROPOLIS) {
+      // accept if dE <= 0, else with exp(-beta dE)
+      P = (e <= 0) ? 1.0 : (std::isinf(beta) ? 0.0 : std::exp(-2.0 * beta * (double)e));
+    } else {
+      // heat bath: exp(-beta dE) / (exp(-beta dE) + 1)
+      if (std::isinf(beta)) {
+        P = e < 0 ? 1.0 : (e == 0 ? 0.5 : 0.0);
+      } else {
+        const double p = std::exp(-2.0 * beta * (double)e);
+        P = std::isinf(p) ? 1.0 : p / (p + 1.0);
+      }
+    }
+    T[a] = ceil_2p32(P);
+  }
+}
+
+void make_keys(uint64_t seed, PhiloxKeys* K) {
+  uint32_t k0 = (uint32_t)(seed & 0xffffffffu), k1 = (uint32_t)(seed >> 32);
+  for (int r = 0; r < 10; ++r) {
+    K->k0[r] = k0;
+    K->k1[r] = k1;
+    k0 += kPhiloxW0;
+    k1 += kPhiloxW1;
+  }
+}
+
+int check_shape(int64_t N, int64_t M, int n_slabs) {
+  if (N < 2 || (N & 1) || M < 64 || (M % 64) != 0 || n_slabs < 1 || N % n_slabs != 0 ||
+      N / n_slabs < 2 || N > (int64_t(1) << 32) || M > (int64_t(1) << 36)) {
+    g_last_error = "shape: need L_rows even, L_rows % n == 0, L_rows/n >= 2, L_cols % 64 == 0";
+    return ISING_ERR_ARG;
+  }
+  return ISING_OK;
+}
+
+int setup_device(Device& d, int dev) {
+  int ndev = 0;
+  CU(cudaGetDeviceCount(&ndev));
+  if (dev < 0 || dev >= ndev) {
+    g_last_error = "device index out of range";
+    return ISING_ERR_DEVICE;
+  }
+  cudaDeviceProp pr;
+  CU(cudaGetDeviceProperties(&pr, dev));
+  if (pr.major != 10) {
+    g_last_error = std::string("device is not sm_100 (Blackwell B200): ") + pr.name;
+    return ISING_ERR_DEVICE;
+  }
+  d.dev = dev;
+  d.sms = pr.multiProcessorCount;
+  CU(cudaSetDevice(dev));
+  CU(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
+  CU(cudaStreamCreateWithFlags(&d.comm, cudaStreamNonBlocking));
+  CU(cudaEventCreateWithFlags(&d.ev_phase, cudaEventDisableTiming));
+  CU(cudaEventCreateWithFlags(&d.ev_bnd, cudaEventDisableTiming));
+  CU(cudaEventCreateWithFlags(&d.ev_comm, cudaEventDisableTiming));
+  CU(cudaEventCreate(&d.ev_t0));
+  CU(cudaEventCreate(&d.ev_t1));
+  CU(cudaMalloc(&d.red, 4 * sizeof(unsigned long long)));
+  CU(halfsweep_occupancy(&d.hs_blocks_per_sm));
+  if (d.hs_blocks_per_sm < 1) d.hs_blocks_per_sm = 1;
+  return ISING_OK;
+}
+
+int alloc_slabs(ising_ctx* h) {
+  for (auto& s : h->slabs) {
+    CU(cudaSetDevice(h->devs[s.devi].dev));
+    const size_t bytes = (size_t)(s.R + 2) * (size_t)h->W * sizeof(uint64_t);
+    for (int c = 0; c < 2; ++c) {
+      CU(cudaMalloc(&s.plane[c], bytes));
+      CU(cudaMemsetAsync(s.plane[c], 0, bytes, h->devs[s.devi].stream));
+    }
+  }
+  for (auto& d : h->devs) {
+    CU(cudaSetDevice(d.dev));
+    CU(cudaStreamSynchronize(d.stream));
+  }
+  return ISING_OK;
+}
+
+int ensure_staging(Device& d) {
+  if (!d.staging) {
+    CU(cudaSetDevice(d.dev));
+    CU(cudaMalloc(&d.staging, kStagingBytes));
+  }
+  return ISING_OK;
+}
+
+void destroy_ctx(ising_ctx* h) {
+  if (!h) return;
+  for (auto& s : h->slabs) {
+    if (s.devi < (int)h->devs.size()) cudaSetDevice(h->devs[s.devi].dev);
+    for (int c = 0; c < 2; ++c)
+      if (s.plane[c]) cudaFree(s.plane[c]);
+  }
+  if (h->comm) ncclCommDestroy(h->comm);
+  for (auto& d : h->devs) {
+    if (d.dev < 0) continue;
+    cudaSetDevice(d.dev);
+    if (d.staging) cudaFree(d.staging);
+    if (d.red) cudaFree(d.red);
+    for (cudaEvent_t e : {d.ev_phase, d.ev_bnd, d.ev_comm, d.ev_t0, d.ev_t1})
+      if (e) cudaEventDestroy(e);
+    if (d.stream) cudaStreamDestroy(d.stream);
+    if (d.comm) cudaStreamDestroy(d.comm);
+  }
+  for (cudaEvent_t e : h->prof_events) cudaEventDestroy(e);
+  delete h;
+}
+
+// Launch geometry for rows [ra, rb) of a slab: H rows per work item, one item per
+// thread, blocks of 128; H chosen so the grid is >= ~4 waves of resident blocks.
+void halfsweep_geometry(const ising_ctx* h, const Device& d, int64_t rows, int* H,
+                        int64_t* items, int* grid) {
+  const int64_t chunks = h->W / 2;
+  int hh = h->rows_per_item_override;
+  if (hh <= 0) {
+    const int64_t resident = (int64_t)d.sms * d.hs_blocks_per_sm * 128;
+    int64_t want = (chunks * rows) / (resident * 4);
+    hh = 1;
+    while (hh * 2 <= want && hh < 32) hh *= 2;
+  }
+  *H = hh;
+  *items = chunks * ((rows + hh - 1) / hh);
+  *grid = (int)std::min<int64_t>((*items + 127) / 128, int64_t(1) << 30);
+}
+
+int run_halfsweep(ising_ctx* h, Slab& s, int c, int r_begin, int r_end, uint64_t* halo_up,
+                     uint64_t* halo_dn, uint32_t t) {
+  if (r_end <= r_begin) return ISING_OK;
+  Device& d = h->devs[s.devi];
+  HalfSweepParams p;
+  p.tgt = s.plane[c];
+  p.src = s.plane[1 - c];
+  p.halo_up = halo_up;
+  p.halo_dn = halo_dn;
+  p.W = h->W;
+  p.row0 = s.row0;
+  p.R = (int32_t)s.R;
+  p.r_begin = r_begin;
+  p.r_end = r_end;
+  int grid;
+  halfsweep_geometry(h, d, r_end - r_begin, &p.H, &p.items, &grid);
+  p.t = t;
+  p.colour = (uint32_t)c;
+  p.keys = h->keys;
+  p.acc = h->acc;
+  const bool prof = h->profiling && s.devi == 0;
+  if (prof) CU(cudaEventRecord(h->prof_events[2 * h->kernel_launches], d.stream));
+  CU(launch_halfsweep(h->rule, grid, d.stream, p));
+  if (prof) {
+    CU(cudaEventRecord(h->prof_events[2 * h->kernel_launches + 1], d.stream));
+    ++h->kernel_launches;
+  }
+  ++h->launch_count;
+  return ISING_OK;
+}
+
+int sync_all(ising_ctx* h) {
+  for (auto& d : h->devs) {
+    CU(cudaSetDevice(d.dev));
+    CU(cudaStreamSynchronize(d.stream));
+    CU(cudaStreamSynchronize(d.comm));
+  }
+  return ISING_OK;
+}
+
+// One colour phase, LOCAL mode.
+int phase_local(ising_ctx* h, int c, uint32_t t) {
+  const int n = (int)h->slabs.size();
+  const bool multi_dev = h->devs.size() > 1;
+  if (multi_dev) {
+    // phase p on device d waits for phase p-1 on the devices of its slabs' neighbours
+    for (int di = 0; di < (int)h->devs.size(); ++di) {
+      std::vector<int> waits;
+      for (int k = 0; k < n; ++k) {
+        if (h->slabs[k].devi != di) continue;
+        for (int nb : {(k + n - 1) % n, (k + 1) % n}) {
+          const int nd = h->slabs[nb].devi;
+          if (nd != di && std::find(waits.begin(), waits.end(), nd) == waits.end()) waits.push_back(nd);
+        }
+      }
+      CU(cudaSetDevice(h->devs[di].dev));
+      for (int nd : waits) CU(cudaStreamWaitEvent(h->devs[di].stream, h->devs[nd].ev_phase, 0));
+    }
+  }
+  for (int k = 0; k < n; ++k) {
+    Slab& s = h->slabs[k];
+    Slab& up = h->slabs[(k + n - 1) % n];
+    Slab& dn = h->slabs[(k + 1) % n];
+    CU(cudaSetDevice(h->devs[s.devi].dev));
+    // local row 0 -> upper slab's bottom halo (padded row R+1); local row R-1 -> lower
+    // slab's top halo (padded row 0).
+    TRY(run_halfsweep(h, s, c, 0, (int)s.R, up.plane[c] + (up.R + 1) * h->W, dn.plane[c], t));
+  }
+  if (multi_dev) {
+    for (auto& d : h->devs) {
+      CU(cudaSetDevice(d.dev));
+      CU(cudaEventRecord(d.ev_phase, d.stream));
+    }
+  }
+  return ISING_OK;
+}
+
+// One colour phase, RANK mode (world >= 2): boundary rows, then NCCL halo exchange
+// overlapped with the interior rows.
+int phase_rank(ising_ctx* h, int c, uint32_t t) {
+  Slab& s = h->slabs[0];
+  Device& d = h->devs[0];
+  const int R = (int)s.R;
+  const size_t W = (size_t)h->W;
+  TRY(run_halfsweep(h, s, c, 0, 1, nullptr, nullptr, t));
+  if (R > 1) TRY(run_halfsweep(h, s, c, R - 1, R, nullptr, nullptr, t));
+  CU(cudaEventRecord(d.ev_bnd, d.stream));
+  CU(cudaStreamWaitEvent(d.comm, d.ev_bnd, 0));
+  const int up = (h->rank + h->world - 1) % h->world, dn = (h->rank + 1) % h->world;
+  uint64_t* pl = s.plane[c];
+  NC(ncclGroupStart());
+  NC(ncclSend(pl + 1 * W, W, ncclUint64, up, h->comm, d.comm));        // row 0 -> up's bottom halo
+  NC(ncclRecv(pl + (size_t)(R + 1) * W, W, ncclUint64, dn, h->comm, d.comm));
+  NC(ncclSend(pl + (size_t)R * W, W, ncclUint64, dn, h->comm, d.comm)); // row R-1 -> dn's top halo
+  NC(ncclRecv(pl, W, ncclUint64, up, h->comm, d.comm));
+  NC(ncclGroupEnd());
+  CU(cudaEventRecord(d.ev_comm, d.comm));
+  TRY(run_halfsweep(h, s, c, 1, R - 1, nullptr, nullptr, t));
+  CU(cudaStreamWaitEvent(d.stream, d.ev_comm, 0));
+  return ISING_OK;
+}
+
+int enable_peers(ising_ctx* h) {
+  const int n = (int)h->slabs.size();
+  for (int k = 0; k < n; ++k) {
+    const int a = h->devs[h->slabs[k].devi].dev;
+    for (int nb : {(k + n - 1) % n, (k + 1) % n}) {
+      const int b = h->devs[h->slabs[nb].devi].dev;
+      if (a == b) continue;
+      int can = 0;
+      CU(cudaDeviceCanAccessPeer(&can, a, b));
+      if (!can) {
+        g_last_error = "no P2P access between neighbouring slab devices";
+        return ISING_ERR_DEVICE;
+      }
+      CU(cudaSetDevice(a));
+      cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+      } else if (e != cudaSuccess) {
+        return fail_cuda(e, "cudaDeviceEnablePeerAccess", __LINE__);
+      }
+    }
+  }
+  return ISING_OK;
+}
+
+int create_local(ising_t* out, int64_t N, int64_t M, uint64_t seed, int n_slabs, const int* devices) {
+  if (!out) return ISING_ERR_ARG;
+  *out = nullptr;
+  TRY(check_shape(N, M, n_slabs));
+  ising_ctx* h = new (std::nothrow) ising_ctx;
+  if (!h) return ISING_ERR_OOM;
+  h->N = N;
+  h->M = M;
+  h->W = M / 32;
+  h->seed = seed;
+  make_keys(seed, &h->keys);
+  const int64_t R = N / n_slabs;
+  for (int k = 0; k < n_slabs; ++k) {
+    int di = -1;
+    for (int j = 0; j < (int)h->devs.size(); ++j)
+      if (h->devs[j].dev == devices[k]) di = j;
+    if (di < 0) {
+      h->devs.emplace_back();
+      int st = setup_device(h->devs.back(), devices[k]);
+      if (st != ISING_OK) {
+        destroy_ctx(h);
+        return st;
+      }
+      di = (int)h->devs.size() - 1;
+    }
+    Slab s;
+    s.devi = di;
+    s.row0 = k * R;
+    s.R = R;
+    h->slabs.push_back(s);
+  }
+  int st = enable_peers(h);
+  if (st == ISING_OK) st = alloc_slabs(h);
+  if (st != ISING_OK) {
+    destroy_ctx(h);
+    return st;
+  }
+  const char* env = getenv("ISING_ROWS_PER_ITEM");
+  if (env) h->rows_per_item_override = atoi(env);
+  *out = h;
+  return ISING_OK;
+}
+
+int run_init(ising_ctx* h, int cold) {
+  for (auto& s : h->slabs) {
+    Device& d = h->devs[s.devi];
+    CU(cudaSetDevice(d.dev));
+    InitParams p;
+    p.plane[0] = s.plane[0];
+    p.plane[1] = s.plane[1];
+    p.W = h->W;
+    p.row0 = s.row0;
+    p.N = h->N;
+    p.R = (int32_t)s.R;
+    p.cold = cold;
+    p.keys = h->keys;
+    const int64_t total = 2 * (s.R + 2) * h->W;
+    const int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)d.sms * 64);
+    k_init<<<grid, 256, 0, d.stream>>>(p);
+    CU(cudaGetLastError());
+    ++h->launch_count;
+  }
+  TRY(sync_all(h));
+  h->t = 0;
+  h->state_set = true;
+  return ISING_OK;
+}
+
+// Copy global rows [g, g + n) (wrapping mod N) of the host lattice to dst.
+int h2d_rows(ising_ctx* h, int8_t* dst, const int8_t* in, int64_t g, int64_t n, cudaStream_t st) {
+  g %= h->N;
+  if (g < 0) g += h->N;
+  while (n > 0) {
+    const int64_t run = std::min(n, h->N - g);
+    CU(cudaMemcpyAsync(dst, in + g * h->M, (size_t)(run * h->M), cudaMemcpyHostToDevice, st));
+    dst += run * h->M;
+    n -= run;
+    g = 0;
+  }
+  return ISING_OK;
+}
+
+}  // namespace
+
+// ======================================================================= C ABI
+extern "C" {
+
+int ising_create(ising_t* out, int64_t L_rows, int64_t L_cols, uint64_t seed, int n_gpus) {
+  if (n_gpus < 1) return ISING_ERR_ARG;
+  std::vector<int> devs(n_gpus);
+  for (int k = 0; k < n_gpus; ++k) devs[k] = k;
+  return create_local(out, L_rows, L_cols, seed, n_gpus, devs.data());
+}
+
+int ising_create_slabs(ising_t* out, int64_t L_rows, int64_t L_cols, uint64_t seed, int n_slabs,
+                       const int* devices) {
+  if (!devices || n_slabs < 1) return ISING_ERR_ARG;
+  return create_local(out, L_rows, L_cols, seed, n_slabs, devices);
+}
+
+int ising_nccl_unique_id(void* id, size_t id_len) {
+  if (!id || id_len < sizeof(ncclUniqueId)) return ISING_ERR_ARG;
+  ncclUniqueId u;
+  NC(ncclGetUniqueId(&u));
+  memcpy(id, &u, sizeof u);
+  return ISING_OK;
+}
+
+int ising_create_rank(ising_t* out, int64_t L_rows, int64_t L_cols, uint64_t seed, int rank,
+                      int world, int device, const void* nccl_id, size_t id_len) {
+  if (!out || world < 1 || rank < 0 || rank >= world) return ISING_ERR_ARG;
+  if (world > 1 && (!nccl_id || id_len < sizeof(ncclUniqueId))) return ISING_ERR_ARG;
+  *out = nullptr;
+  TRY(check_shape(L_rows, L_cols, world));
+  ising_ctx* h = new (std::nothrow) ising_ctx;
+  if (!h) return ISING_ERR_OOM;
+  h->N = L_rows;
+  h->M = L_cols;
+  h->W = L_cols / 32;
+  h->seed = seed;
+  h->rank_mode = true;
+  h->rank = rank;
+  h->world = world;
+  make_keys(seed, &h->keys);
+  h->devs.emplace_back();
+  int st = setup_device(h->devs[0], device);
+  if (st != ISING_OK) {
+    destroy_ctx(h);
+    return st;
+  }
+  Slab s;
+  s.devi = 0;
+  s.R = L_rows / world;
+  s.row0 = rank * s.R;
+  h->slabs.push_back(s);
+  st = alloc_slabs(h);
+  if (st == ISING_OK && world > 1) {
+    ncclUniqueId u;
+    memcpy(&u, nccl_id, sizeof u);
+    cudaSetDevice(device);
+    ncclResult_t r = ncclCommInitRank(&h->comm, world, u, rank);
+    if (r != ncclSuccess) st = fail_nccl(r, "ncclCommInitRank", __LINE__);
+  }
+  if (st != ISING_OK) {
+    destroy_ctx(h);
+    return st;
+  }
+  const char* env = getenv("ISING_ROWS_PER_ITEM");
+  if (env) h->rows_per_item_override = atoi(env);
+  *out = h;
+  return ISING_OK;
+}
+
+int ising_destroy(ising_t h) {
+  destroy_ctx(h);
+  return ISING_OK;
+}
+
+int ising_set_rule(ising_t h, int rule) {
+  if (!h || (rule != ISING_RULE_METROPOLIS && rule != ISING_RULE_HEATBATH)) return ISING_ERR_ARG;
+  h->rule = rule;
+  if (h->beta_set) return ising_set_beta(h, h->beta);
+  return ISING_OK;
+}
+
+int ising_set_beta(ising_t h, double beta) {
+  if (!h || std::isnan(beta) || beta < 0) return ISING_ERR_ARG;
+  h->beta = beta;
+  compute_thresholds(beta, h->rule, h->T);
+  h->acc.always_mask = 0;
+  for (int a = 0; a < 5; ++a) {
+    if (h->T[a] >= (uint64_t(1) << 32)) {
+      h->acc.always_mask |= 1u << a;
+      h->acc.thr[a] = 0xffffffffu;
+    } else {
+      h->acc.thr[a] = (uint32_t)h->T[a];
+    }
+  }
+  h->beta_set = true;
+  return ISING_OK;
+}
+
+int ising_init_random(ising_t h) { return h ? run_init(h, 0) : ISING_ERR_ARG; }
+int ising_init_cold(ising_t h) { return h ? run_init(h, 1) : ISING_ERR_ARG; }
+
+int ising_write_lattice(ising_t h, const int8_t* in, int64_t in_len, uint64_t t) {
+  if (!h || !in) return ISING_ERR_ARG;
+  if (in_len < h->N * h->M) return ISING_ERR_RANGE;
+  if (t > 0xffffffffull) return ISING_ERR_RANGE;
+  // rank mode packs its rows and halos directly from the full host lattice, so no
+  // exchange is needed either.
+  for (auto& s : h->slabs) {
+    Device& d = h->devs[s.devi];
+    CU(cudaSetDevice(d.dev));
+    TRY(ensure_staging(d));
+    CU(cudaMemsetAsync(d.red, 0, 4 * sizeof(unsigned long long), d.stream));
+    const int64_t rows_per_chunk = std::max<int64_t>(1, (int64_t)kStagingBytes / h->M);
+    for (int64_t ra = -1; ra < s.R + 1; ra += rows_per_chunk) {
+      const int64_t rb = std::min<int64_t>(ra + rows_per_chunk, s.R + 1);
+      TRY(h2d_rows(h, d.staging, in, s.row0 + ra, rb - ra, d.stream));
+      PackParams p;
+      p.plane[0] = s.plane[0];
+      p.plane[1] = s.plane[1];
+      p.full = d.staging;
+      p.W = h->W;
+      p.M = h->M;
+      p.row0 = s.row0;
+      p.N = h->N;
+      p.ra = (int32_t)ra;
+      p.rb = (int32_t)rb;
+      p.bad = reinterpret_cast<unsigned int*>(d.red + 2);
+      const int64_t total = 2 * (rb - ra) * h->W;
+      const int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)d.sms * 64);
+      k_pack<<<grid, 256, 0, d.stream>>>(p);
+      CU(cudaGetLastError());
+      ++h->launch_count;
+    }
+  }
+  TRY(sync_all(h));
+  for (auto& s : h->slabs) {
+    Device& d = h->devs[s.devi];
+    CU(cudaSetDevice(d.dev));
+    unsigned long long bad = 0;
+    CU(cudaMemcpy(&bad, d.red + 2, sizeof bad, cudaMemcpyDeviceToHost));
+    if (bad & 0xffffffffull) {
+      g_last_error = "ising_write_lattice: values must be -1 or +1";
+      return ISING_ERR_ARG;
+    }
+  }
+  h->t = t;
+  h->state_set = true;
+  return ISING_OK;
+}
+
+int ising_sweep(ising_t h, int64_t n) {
+  if (!h || n < 0) return ISING_ERR_ARG;
+  if (!h->beta_set || !h->state_set) return ISING_ERR_STATE;
+  if (h->t + (uint64_t)n > 0xffffffffull) return ISING_ERR_RANGE;
+  if (h->profiling) {
+    const size_t per_phase = std::max<size_t>(3, h->slabs.size());
+    const size_t need = (size_t)n * 2 * 2 * per_phase;
+    if (!h->devs.empty()) CU(cudaSetDevice(h->devs[0].dev));
+    while (h->prof_events.size() < need) {
+      cudaEvent_t e;
+      CU(cudaEventCreate(&e));
+      h->prof_events.push_back(e);
+    }
+  }
+  h->kernel_launches = 0;
+  for (auto& d : h->devs) {
+    CU(cudaSetDevice(d.dev));
+    CU(cudaEventRecord(d.ev_t0, d.stream));
+  }
+  for (int64_t k = 1; k <= n; ++k) {
+    const uint32_t t = (uint32_t)(h->t + (uint64_t)k);
+    for (int c = 0; c < 2; ++c) {
+      if (h->rank_mode && h->world > 1)
+        TRY(phase_rank(h, c, t));
+      else
+        TRY(phase_local(h, c, t));
+    }
+  }
+  for (auto& d : h->devs) {
+    CU(cudaSetDevice(d.dev));
+    CU(cudaEventRecord(d.ev_t1, d.stream));
+  }
+  TRY(sync_all(h));
+  double mx = 0;
+  for (auto& d : h->devs) {
+    float ms = 0;
+    CU(cudaEventElapsedTime(&ms, d.ev_t0, d.ev_t1));
+    mx = std::max(mx, (double)ms);
+  }
+  h->last_ms = mx;
+  if (h->profiling) {
+    double tot = 0;
+    for (int64_t k = 0; k < h->kernel_launches; ++k) {
+      float ms = 0;
+      CU(cudaEventElapsedTime(&ms, h->prof_events[2 * k], h->prof_events[2 * k + 1]));
+      tot += ms;
+    }
+    h->kernel_ms = tot;
+  }
+  h->t += (uint64_t)n;
+  return ISING_OK;
+}
+
+int ising_read_lattice(ising_t h, int8_t* out, int64_t out_len) {
+  if (!h || !out) return ISING_ERR_ARG;
+  if (out_len < h->N * h->M) return ISING_ERR_RANGE;
+  if (!h->state_set) return ISING_ERR_STATE;
+  for (auto& s : h->slabs) {
+    Device& d = h->devs[s.devi];
+    CU(cudaSetDevice(d.dev));
+    TRY(ensure_staging(d));
+    const int64_t rows_per_chunk = std::max<int64_t>(1, (int64_t)kStagingBytes / h->M);
+    for (int64_t ra = 0; ra < s.R; ra += rows_per_chunk) {
+      const int64_t rb = std::min<int64_t>(ra + rows_per_chunk, s.R);
+      UnpackParams p;
+      p.plane[0] = s.plane[0];
+      p.plane[1] = s.plane[1];
+      p.full = d.staging;
+      p.W = h->W;
+      p.M = h->M;
+      p.row0 = s.row0;
+      p.ra = (int32_t)ra;
+      p.rb = (int32_t)rb;
+      const int64_t total = 2 * (rb - ra) * h->W;
+      const int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)d.sms * 64);
+      k_unpack<<<grid, 256, 0, d.stream>>>(p);
+      CU(cudaGetLastError());
+      ++h->launch_count;
+      CU(cudaMemcpyAsync(out + (s.row0 + ra) * h->M, d.staging, (size_t)((rb - ra) * h->M),
+                         cudaMemcpyDeviceToHost, d.stream));
+    }
+  }
+  TRY(sync_all(h));
+  return ISING_OK;
+}
+
+int ising_observables(ising_t h, int64_t* up_count, int64_t* bond_energy) {
+  if (!h || !up_count || !bond_energy) return ISING_ERR_ARG;
+  if (!h->state_set) return ISING_ERR_STATE;
+  for (auto& d : h->devs) {
+    CU(cudaSetDevice(d.dev));
+    CU(cudaMemsetAsync(d.red, 0, 2 * sizeof(unsigned long long), d.stream));
+  }
+  for (auto& s : h->slabs) {
+    Device& d = h->devs[s.devi];
+    CU(cudaSetDevice(d.dev));
+    ObsParams p;
+    p.black = s.plane[0];
+    p.white = s.plane[1];
+    p.W = h->W;
+    p.row0 = s.row0;
+    p.R = (int32_t)s.R;
+    p.out = d.red;
+    const int64_t total = s.R * h->W;
+    const int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)d.sms * 8);
+    k_observables<<<grid, 256, 0, d.stream>>>(p);
+    CU(cudaGetLastError());
+    ++h->launch_count;
+  }
+  if (h->rank_mode && h->world > 1) {
+    Device& d = h->devs[0];
+    NC(ncclAllReduce(d.red, d.red, 2, ncclUint64, ncclSum, h->comm, d.stream));
+  }
+  TRY(sync_all(h));
+  unsigned long long up = 0, anti = 0;
+  for (auto& d : h->devs) {
+    unsigned long long v[2];
+    CU(cudaSetDevice(d.dev));
+    CU(cudaMemcpy(v, d.red, sizeof v, cudaMemcpyDeviceToHost));
+    up += v[0];
+    anti += v[1];
+  }
+  *up_count = (int64_t)up;
+  *bond_energy = 2 * (int64_t)anti - 2 * h->N * h->M;
+  return ISING_OK;
+}
+
+int ising_last_sweep_ms(ising_t h, double* device_ms) {
+  if (!h || !device_ms) return ISING_ERR_ARG;
+  *device_ms = h->last_ms;
+  return ISING_OK;
+}
+
+int ising_set_profiling(ising_t h, int enable) {
+  if (!h) return ISING_ERR_ARG;
+  h->profiling = enable != 0;
+  return ISING_OK;
+}
+
+int ising_kernel_stats(ising_t h, double* kernel_ms, int64_t* launches) {
+  if (!h || !kernel_ms || !launches) return ISING_ERR_ARG;
+  *kernel_ms = h->kernel_ms;
+  *launches = h->kernel_launches;
+  return ISING_OK;
+}
+
+int ising_get_sweep(ising_t h, uint64_t* t) {
+  if (!h || !t) return ISING_ERR_ARG;
+  *t = h->t;
+  return ISING_OK;
+}
+
+int ising_slab_info(ising_t h, int64_t* row0, int64_t* rows) {
+  if (!h || !row0 || !rows) return ISING_ERR_ARG;
+  if (h->rank_mode) {
+    *row0 = h->slabs[0].row0;
+    *rows = h->slabs[0].R;
+  } else {
+    *row0 = 0;
+    *rows = h->N;
+  }
+  return ISING_OK;
+}
+
+int ising_thresholds(ising_t h, uint64_t T[5]) {
+  if (!h || !T) return ISING_ERR_ARG;
+  if (!h->beta_set) return ISING_ERR_STATE;
+  for (int a = 0; a < 5; ++a) T[a] = h->T[a];
+  return ISING_OK;
+}
+
+int ising_launch_count(ising_t h, int64_t* launches) {
+  if (!h || !launches) return ISING_ERR_ARG;
+  *launches = h->launch_count;
+  return ISING_OK;
+}
+
+int ising_probe_philox(int device, double* draws_per_ns) {
+  if (!draws_per_ns) return ISING_ERR_ARG;
+  Device d;
+  int st = setup_device(d, device);
+  if (st != ISING_OK) return st;
+  PhiloxKeys K;
+  make_keys(0x0123456789abcdefull, &K);
+  unsigned int* sink = nullptr;
+  CU(cudaMalloc(&sink, sizeof(unsigned int)));
+  const int grid = d.sms * 16;  // 2048 threads per SM
+  const uint32_t per_thread = 2048;
+  cudaEvent_t a, b;
+  CU(cudaEventCreate(&a));
+  CU(cudaEventCreate(&b));
+  double best = 0;
+  for (int rep = 0; rep < 4; ++rep) {
+    CU(cudaEventRecord(a, d.stream));
+    CU(launch_philox_probe(grid, d.stream, K, per_thread, sink));
+    CU(cudaEventRecord(b, d.stream));
+    CU(cudaEventSynchronize(b));
+    float ms = 0;
+    CU(cudaEventElapsedTime(&ms, a, b));
+    const double draws = 4.0 * grid * 128.0 * per_thread;
+    if (rep > 0) best = std::max(best, draws / (ms * 1e6));
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(sink);
+  cudaFree(d.red);
+  cudaStreamDestroy(d.stream);
+  cudaStreamDestroy(d.comm);
+  for (cudaEvent_t e : {d.ev_phase, d.ev_bnd, d.ev_comm, d.ev_t0, d.ev_t1}) cudaEventDestroy(e);
+  *draws_per_ns = best;
+  return ISING_OK;
+}
+
+const char* ising_strerror(int status) {
+  switch (status) {
+    case ISING_OK: return "ok";
+    case ISING_ERR_ARG: return "invalid argument";
+    case ISING_ERR_STATE: return "invalid call order (set_beta and init/write first)";
+    case ISING_ERR_DEVICE: return "no suitable sm_100 device";
+    case ISING_ERR_OOM: return "out of memory";
+    case ISING_ERR_CUDA: return "CUDA error";
+    case ISING_ERR_NCCL: return "NCCL error";
+    case ISING_ERR_RANGE: return "out of range";
+    default: return "unknown status";
+  }
+}
+
+const char* ising_last_error(void) { return g_last_error.c_str(); }
+
+}  // extern "C"

@@ -1,0 +1,327 @@
+"""Thin ctypes binding of libising.so (include/ising.h): argument marshalling only.
+
+Every step of the sweep runs in the library's sm_100a kernels.  There is no CPU
+fallback: if libising.so is missing or no sm_100 device is present, the calls fail
+with an exception.  The functions ``ising_*`` mirror the C ABI one to one;
+``IsingLattice`` is a convenience wrapper that owns a handle.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libising.so")
+
+ISING_OK = 0
+ISING_ERR_ARG = -1
+ISING_ERR_STATE = -2
+ISING_ERR_DEVICE = -3
+ISING_ERR_OOM = -4
+ISING_ERR_CUDA = -5
+ISING_ERR_NCCL = -6
+ISING_ERR_RANGE = -7
+RULE_METROPOLIS = 0
+RULE_HEATBATH = 1
+NCCL_ID_BYTES = 128
+
+# name -> (restype, argtypes); the exported symbols of include/ising.h
+_VP = ctypes.c_void_p
+_I64, _U64, _INT, _DBL, _SZ = ctypes.c_int64, ctypes.c_uint64, ctypes.c_int, ctypes.c_double, ctypes.c_size_t
+_I64P, _U64P, _DBLP = ctypes.POINTER(_I64), ctypes.POINTER(_U64), ctypes.POINTER(_DBL)
+SIGNATURES = {
+    "ising_create": (_INT, [ctypes.POINTER(_VP), _I64, _I64, _U64, _INT]),
+    "ising_create_slabs": (_INT, [ctypes.POINTER(_VP), _I64, _I64, _U64, _INT, ctypes.POINTER(_INT)]),
+    "ising_create_rank": (_INT, [ctypes.POINTER(_VP), _I64, _I64, _U64, _INT, _INT, _INT, _VP, _SZ]),
+    "ising_nccl_unique_id": (_INT, [_VP, _SZ]),
+    "ising_destroy": (_INT, [_VP]),
+    "ising_set_beta": (_INT, [_VP, _DBL]),
+    "ising_set_rule": (_INT, [_VP, _INT]),
+    "ising_init_random": (_INT, [_VP]),
+    "ising_init_cold": (_INT, [_VP]),
+    "ising_write_lattice": (_INT, [_VP, _VP, _I64, _U64]),
+    "ising_sweep": (_INT, [_VP, _I64]),
+    "ising_read_lattice": (_INT, [_VP, _VP, _I64]),
+    "ising_observables": (_INT, [_VP, _I64P, _I64P]),
+    "ising_last_sweep_ms": (_INT, [_VP, _DBLP]),
+    "ising_set_profiling": (_INT, [_VP, _INT]),
+    "ising_kernel_stats": (_INT, [_VP, _DBLP, _I64P]),
+    "ising_get_sweep": (_INT, [_VP, _U64P]),
+    "ising_slab_info": (_INT, [_VP, _I64P, _I64P]),
+    "ising_thresholds": (_INT, [_VP, _U64P]),
+    "ising_launch_count": (_INT, [_VP, _I64P]),
+    "ising_probe_philox": (_INT, [_INT, _DBLP]),
+    "ising_strerror": (ctypes.c_char_p, [_INT]),
+    "ising_last_error": (ctypes.c_char_p, []),
+}
+
+_lib = None
+
+
+class IsingError(RuntimeError):
+    def __init__(self, status: int, call: str):
+        lib = load()
+        msg = lib.ising_strerror(status).decode()
+        detail = lib.ising_last_error().decode()
+        super().__init__(f"{call} -> {status} ({msg}){': ' + detail if detail else ''}")
+        self.status = status
+
+
+def load() -> ctypes.CDLL:
+    """Load libising.so (built by __graft_entry__.build()); fails loudly if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build the CUDA library first "
+                "(python -c 'import __graft_entry__ as g; g.build()')"
+            )
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            f = getattr(lib, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def _check(status: int, call: str) -> None:
+    if status != ISING_OK:
+        raise IsingError(status, call)
+
+
+def _buf_ptr(buf, nbytes_needed: int, writable: bool):
+    """Pointer + length of a host int8 buffer (numpy array or CPU torch tensor)."""
+    if isinstance(buf, np.ndarray):
+        if buf.dtype != np.int8 or not buf.flags["C_CONTIGUOUS"]:
+            raise ValueError("lattice buffers must be C-contiguous int8")
+        if writable and not buf.flags["WRITEABLE"]:
+            raise ValueError("output buffer is read-only")
+        return buf.ctypes.data, buf.size
+    # torch tensor (e.g. pinned host memory)
+    if hasattr(buf, "data_ptr"):
+        import torch
+
+        if buf.dtype != torch.int8 or not buf.is_contiguous() or buf.is_cuda:
+            raise ValueError("lattice tensors must be contiguous int8 host tensors")
+        return buf.data_ptr(), buf.numel()
+    raise TypeError("expected a numpy int8 array or an int8 torch tensor")
+
+
+# ------------------------------------------------------------ raw ABI mirror
+def ising_create(L_rows: int, L_cols: int, seed: int, n_gpus: int = 1) -> int:
+    h = _VP()
+    _check(load().ising_create(ctypes.byref(h), L_rows, L_cols, seed, n_gpus), "ising_create")
+    return h.value
+
+
+def ising_create_slabs(L_rows: int, L_cols: int, seed: int, devices) -> int:
+    h = _VP()
+    arr = (_INT * len(devices))(*devices)
+    _check(load().ising_create_slabs(ctypes.byref(h), L_rows, L_cols, seed, len(devices), arr),
+           "ising_create_slabs")
+    return h.value
+
+
+def ising_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(NCCL_ID_BYTES)
+    _check(load().ising_nccl_unique_id(buf, NCCL_ID_BYTES), "ising_nccl_unique_id")
+    return buf.raw
+
+
+def ising_create_rank(L_rows: int, L_cols: int, seed: int, rank: int, world: int, device: int,
+                      nccl_id: bytes | None) -> int:
+    h = _VP()
+    idbuf = ctypes.create_string_buffer(nccl_id, NCCL_ID_BYTES) if nccl_id else None
+    _check(load().ising_create_rank(ctypes.byref(h), L_rows, L_cols, seed, rank, world, device,
+                                    idbuf, NCCL_ID_BYTES if nccl_id else 0), "ising_create_rank")
+    return h.value
+
+
+def ising_destroy(h: int) -> None:
+    _check(load().ising_destroy(h), "ising_destroy")
+
+
+def ising_set_beta(h: int, beta: float) -> None:
+    _check(load().ising_set_beta(h, float(beta)), "ising_set_beta")
+
+
+def ising_set_rule(h: int, rule: int) -> None:
+    _check(load().ising_set_rule(h, int(rule)), "ising_set_rule")
+
+
+def ising_init_random(h: int) -> None:
+    _check(load().ising_init_random(h), "ising_init_random")
+
+
+def ising_init_cold(h: int) -> None:
+    _check(load().ising_init_cold(h), "ising_init_cold")
+
+
+def ising_write_lattice(h: int, buf, t: int = 0) -> None:
+    ptr, n = _buf_ptr(buf, 0, writable=False)
+    _check(load().ising_write_lattice(h, ptr, n, int(t)), "ising_write_lattice")
+
+
+def ising_sweep(h: int, n: int) -> None:
+    _check(load().ising_sweep(h, int(n)), "ising_sweep")
+
+
+def ising_read_lattice(h: int, out) -> None:
+    ptr, n = _buf_ptr(out, 0, writable=True)
+    _check(load().ising_read_lattice(h, ptr, n), "ising_read_lattice")
+
+
+def ising_observables(h: int) -> tuple[int, int]:
+    up, E = _I64(), _I64()
+    _check(load().ising_observables(h, ctypes.byref(up), ctypes.byref(E)), "ising_observables")
+    return up.value, E.value
+
+
+def ising_last_sweep_ms(h: int) -> float:
+    v = _DBL()
+    _check(load().ising_last_sweep_ms(h, ctypes.byref(v)), "ising_last_sweep_ms")
+    return v.value
+
+
+def ising_set_profiling(h: int, enable: bool) -> None:
+    _check(load().ising_set_profiling(h, int(bool(enable))), "ising_set_profiling")
+
+
+def ising_kernel_stats(h: int) -> tuple[float, int]:
+    ms, n = _DBL(), _I64()
+    _check(load().ising_kernel_stats(h, ctypes.byref(ms), ctypes.byref(n)), "ising_kernel_stats")
+    return ms.value, n.value
+
+
+def ising_get_sweep(h: int) -> int:
+    t = _U64()
+    _check(load().ising_get_sweep(h, ctypes.byref(t)), "ising_get_sweep")
+    return t.value
+
+
+def ising_slab_info(h: int) -> tuple[int, int]:
+    a, b = _I64(), _I64()
+    _check(load().ising_slab_info(h, ctypes.byref(a), ctypes.byref(b)), "ising_slab_info")
+    return a.value, b.value
+
+
+def ising_thresholds(h: int) -> list[int]:
+    T = (_U64 * 5)()
+    _check(load().ising_thresholds(h, T), "ising_thresholds")
+    return [int(x) for x in T]
+
+
+def ising_launch_count(h: int) -> int:
+    n = _I64()
+    _check(load().ising_launch_count(h, ctypes.byref(n)), "ising_launch_count")
+    return n.value
+
+
+def ising_probe_philox(device: int = 0) -> float:
+    v = _DBL()
+    _check(load().ising_probe_philox(device, ctypes.byref(v)), "ising_probe_philox")
+    return v.value
+
+
+# ------------------------------------------------------------ convenience
+class IsingLattice:
+    """Owns one handle.  ``devices`` maps slabs to CUDA devices (ising_create_slabs)."""
+
+    def __init__(self, L_rows: int, L_cols: int, seed: int = 1, n_gpus: int = 1, devices=None,
+                 _handle: int | None = None):
+        self.N, self.M, self.seed = int(L_rows), int(L_cols), int(seed)
+        if _handle is not None:
+            self.h = _handle
+        elif devices is not None:
+            self.h = ising_create_slabs(self.N, self.M, self.seed, list(devices))
+        else:
+            self.h = ising_create(self.N, self.M, self.seed, n_gpus)
+
+    @classmethod
+    def distributed(cls, L_rows: int, L_cols: int, seed: int = 1, device: int | None = None):
+        """One process per GPU under torch.distributed: rank 0's NCCL id is broadcast
+        through the default process group, then every rank creates its slab."""
+        import torch.distributed as dist
+
+        rank, world = dist.get_rank(), dist.get_world_size()
+        if device is None:
+            device = int(os.environ.get("LOCAL_RANK", rank))
+        obj = [ising_nccl_unique_id() if (rank == 0 and world > 1) else None]
+        if world > 1:
+            dist.broadcast_object_list(obj, src=0)
+        h = ising_create_rank(L_rows, L_cols, seed, rank, world, device, obj[0])
+        return cls(L_rows, L_cols, seed, _handle=h)
+
+    def close(self):
+        if getattr(self, "h", None):
+            ising_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def set_beta(self, beta: float, rule: int | None = None):
+        if rule is not None:
+            ising_set_rule(self.h, rule)
+        ising_set_beta(self.h, beta)
+        return self
+
+    def init_random(self):
+        ising_init_random(self.h)
+        return self
+
+    def init_cold(self):
+        ising_init_cold(self.h)
+        return self
+
+    def write_lattice(self, full, t: int = 0):
+        ising_write_lattice(self.h, full, t)
+        return self
+
+    def sweep(self, n: int = 1):
+        ising_sweep(self.h, n)
+        return self
+
+    def read_lattice(self, out=None) -> np.ndarray:
+        if out is None:
+            out = np.empty((self.N, self.M), dtype=np.int8)
+        ising_read_lattice(self.h, out)
+        return out
+
+    def observables(self) -> tuple[int, int]:
+        return ising_observables(self.h)
+
+    @property
+    def t(self) -> int:
+        return ising_get_sweep(self.h)
+
+    def last_sweep_ms(self) -> float:
+        return ising_last_sweep_ms(self.h)
+
+    def thresholds(self) -> list[int]:
+        return ising_thresholds(self.h)
+
+    def slab_info(self) -> tuple[int, int]:
+        return ising_slab_info(self.h)
+
+    def set_profiling(self, enable: bool = True):
+        ising_set_profiling(self.h, enable)
+        return self
+
+    def kernel_stats(self) -> tuple[float, int]:
+        return ising_kernel_stats(self.h)
+
+    def launch_count(self) -> int:
+        return ising_launch_count(self.h)

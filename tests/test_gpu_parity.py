@@ -1,0 +1,224 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, bit for bit.
+
+Lattices are compared as full +-1 byte arrays; observables as exact integers.
+Inputs are the seeded configurations of tests/cases.py (no method arithmetic)."""
+import hashlib
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_1906_06297_b200 import ising
+from paper_1906_06297_b200.ising import IsingLattice
+from tests import cases
+
+pytestmark = pytest.mark.gpu
+
+
+def gpu_lattice(N, M, seed, start, beta, rule=ising.RULE_METROPOLIS, devices=None):
+    g = IsingLattice(N, M, seed, devices=devices)
+    g.set_beta(beta, rule)
+    if start == "random":
+        g.init_random()
+    elif start == "cold":
+        g.init_cold()
+    else:
+        g.write_lattice(start)
+    return g
+
+
+def oracle_lattice(N, M, seed, start, beta, rule=oracle.RULE_METROPOLIS):
+    o = oracle.Lattice(N, M, seed).set_beta(beta, rule)
+    if start == "random":
+        o.init_random()
+    elif start == "cold":
+        o.init_cold()
+    else:
+        o.load_full(start)
+    return o
+
+
+def assert_same(g, o, what=""):
+    a, b = g.read_lattice(), o.full()
+    if not np.array_equal(a, b):
+        bad = np.argwhere(a != b)
+        raise AssertionError(f"{what}: {len(bad)} sites differ, first {bad[:5].tolist()}")
+    assert g.observables() == o.observables(), what
+
+
+def test_c1_bit_exact_1000_sweeps():
+    # BASELINE configs[0]: 64x64, beta = 0.4406868, random start, seed 1, 1000 sweeps
+    N, M, beta, seed = 64, 64, 0.4406868, 1
+    g = gpu_lattice(N, M, seed, "random", beta)
+    o = oracle_lattice(N, M, seed, "random", beta)
+    assert_same(g, o, "init")
+    done = 0
+    for target in [1, 10, 100, 1000]:
+        g.sweep(target - done)
+        o.sweep(target - done)
+        done = target
+        assert_same(g, o, f"after {target} sweeps")
+    assert g.t == 1000
+
+
+@pytest.mark.parametrize("N,M", cases.PARITY_SHAPES)
+@pytest.mark.parametrize("beta", cases.PARITY_BETAS)
+@pytest.mark.parametrize("start", ["random", "cold"])
+def test_parity_matrix(N, M, beta, start):
+    for seed in cases.PARITY_SEEDS:
+        g = gpu_lattice(N, M, seed, start, beta)
+        o = oracle_lattice(N, M, seed, start, beta)
+        for n in [1, 1, 8]:
+            g.sweep(n)
+            o.sweep(n)
+            assert_same(g, o, f"{N}x{M} beta={beta} seed={seed} start={start} t={o.t}")
+
+
+@pytest.mark.parametrize("N,M,nslab", cases.SLAB_CASES)
+def test_virtual_slabs_match_oracle(N, M, nslab):
+    # slab decomposition on one device (halo rows exchanged by fused stores into the
+    # neighbouring slab's halo): identical to the oracle and to n = 1 (reading R19)
+    seed, beta = 3, 0.4406868
+    g = gpu_lattice(N, M, seed, "random", beta, devices=[0] * nslab)
+    o = oracle_lattice(N, M, seed, "random", beta)
+    for n in [1, 4, 20]:
+        g.sweep(n)
+        o.sweep(n)
+        assert_same(g, o, f"{nslab} slabs t={o.t}")
+
+
+def test_heatbath_parity():
+    for N, M, beta in [(64, 64, 0.4406868), (66, 128, 0.2), (32, 64, math.inf), (32, 64, 0.0)]:
+        g = gpu_lattice(N, M, 5, "random", beta, ising.RULE_HEATBATH)
+        o = oracle_lattice(N, M, 5, "random", beta, oracle.RULE_HEATBATH)
+        assert g.thresholds() == [int(x) for x in o_thresholds(beta, oracle.RULE_HEATBATH)]
+        for n in [1, 10]:
+            g.sweep(n)
+            o.sweep(n)
+            assert_same(g, o, f"heat bath {N}x{M} beta={beta}")
+
+
+def o_thresholds(beta, rule):
+    return oracle.thresholds(beta, rule)
+
+
+def test_thresholds_equal_oracle():
+    g = IsingLattice(64, 64, 1)
+    for beta in [0.0, 0.1, 0.2, 1 / 3, 0.4406868, 0.44068679350977147, 2 / 3, 0.8, 5.0, math.inf]:
+        for rule in [ising.RULE_METROPOLIS, ising.RULE_HEATBATH]:
+            g.set_beta(beta, rule)
+            assert g.thresholds() == [int(x) for x in oracle.thresholds(beta, rule)], (beta, rule)
+
+
+def test_write_read_round_trip_and_resume():
+    rng = np.random.default_rng(17)
+    for N, M in [(64, 64), (130, 192), (2, 64)]:
+        full = cases.random_pm1(rng, N, M)
+        g = IsingLattice(N, M, 9).write_lattice(full, t=37)
+        assert np.array_equal(g.read_lattice(), full)
+        assert g.t == 37
+        g.set_beta(0.4406868).sweep(3)
+        o = oracle.Lattice(N, M, 9).load_full(full, t=37).set_beta(0.4406868).sweep(3)
+        assert_same(g, o, "resume")
+
+
+def test_chunking_invariance():
+    a = gpu_lattice(128, 128, 2, "random", 0.4406868)
+    b = gpu_lattice(128, 128, 2, "random", 0.4406868)
+    a.sweep(500).sweep(500)
+    b.sweep(1000)
+    assert np.array_equal(a.read_lattice(), b.read_lattice())
+
+
+def test_trap_state_period_two():
+    N, M = 64, 128
+    full = cases.alternating_rows(N, M)
+    for beta in [0.2, 0.4406868, math.inf]:
+        g = IsingLattice(N, M, 1).write_lattice(full).set_beta(beta)
+        g.sweep(1)
+        assert np.array_equal(g.read_lattice(), -full)
+        g.sweep(1)
+        assert np.array_equal(g.read_lattice(), full)
+
+
+def test_observables_closed_forms():
+    N, M = 64, 128
+    g = IsingLattice(N, M, 1).init_cold()
+    assert g.observables() == (N * M, -2 * N * M)
+    g.write_lattice(cases.neel(N, M))
+    assert g.observables() == (N * M // 2, 2 * N * M)
+    one = np.ones((N, M), dtype=np.int8)
+    one[5, 7] = -1
+    g.write_lattice(one)
+    assert g.observables() == (N * M - 1, -2 * N * M + 8)
+
+
+def test_beta_zero_flips_everything():
+    g = gpu_lattice(64, 256, 4, "random", 0.0)
+    f0 = g.read_lattice()
+    up0, E0 = g.observables()
+    g.sweep(1)
+    assert np.array_equal(g.read_lattice(), -f0)
+    assert g.observables() == (64 * 256 - up0, E0)
+
+
+def test_error_behaviour():
+    g = IsingLattice(64, 64, 1)
+    with pytest.raises(ising.IsingError) as e:
+        g.sweep(1)
+    assert e.value.status == ising.ISING_ERR_STATE
+    g.init_random()
+    with pytest.raises(ising.IsingError) as e:
+        g.sweep(1)  # no beta yet
+    assert e.value.status == ising.ISING_ERR_STATE
+    with pytest.raises(ising.IsingError) as e:
+        g.set_beta(-1.0)
+    assert e.value.status == ising.ISING_ERR_ARG
+    with pytest.raises(ising.IsingError) as e:
+        g.set_beta(float("nan"))
+    assert e.value.status == ising.ISING_ERR_ARG
+    with pytest.raises(ising.IsingError) as e:
+        g.read_lattice(np.empty(64 * 64 - 1, dtype=np.int8))
+    assert e.value.status == ising.ISING_ERR_RANGE
+    bad = np.ones((64, 64), dtype=np.int8)
+    bad[3, 3] = 0
+    with pytest.raises(ising.IsingError) as e:
+        g.write_lattice(bad)
+    assert e.value.status == ising.ISING_ERR_ARG
+    g.set_beta(0.3)
+    g.write_lattice(np.ones((64, 64), dtype=np.int8), t=2**32 - 3)
+    g.sweep(2)
+    with pytest.raises(ising.IsingError) as e:
+        g.sweep(1)
+    assert e.value.status == ising.ISING_ERR_RANGE
+    g.sweep(0)
+
+
+def test_random_start_golden():
+    # tests/golden/rng_contract.txt (independent evaluation of the contract)
+    from tests import golden_io
+
+    _, inits, _ = golden_io.rng_contract()
+    for (N, M, seed), up, E, sha in inits:
+        g = IsingLattice(N, M, seed).init_random()
+        assert g.observables() == (up, E)
+        assert hashlib.sha256(g.read_lattice().tobytes()).hexdigest().startswith(sha)
+
+
+@pytest.mark.slow
+def test_full_size_c3_one_sweep_matches_oracle():
+    # BASELINE configs[2] shape (32768^2, beta_c, random start, seed 1) in the launch
+    # configuration bench.py times; the whole lattice after one sweep, hashed.
+    N = M = cases.C3[0]
+    beta = cases.C3[2]
+    g = gpu_lattice(N, M, 1, "random", beta)
+    g.sweep(1)
+    got = g.read_lattice()
+    up_g = g.observables()
+    g.close()
+    o = oracle_lattice(N, M, 1, "random", beta)
+    o.sweep(1)
+    exp = o.full()
+    assert hashlib.sha256(got.tobytes()).digest() == hashlib.sha256(exp.tobytes()).digest()
+    assert up_g == o.observables()

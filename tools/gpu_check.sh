@@ -1,0 +1,13 @@
+#!/bin/bash
+# One gpurun session: GPU tests, smoke, bench, ncu launch list + full capture of k_halfsweep.
+set -x
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/gpu.txt
+timeout 900 python -m pytest tests -m gpu -x -q ${PYTEST_ARGS} > gpurun_out/pytest_gpu.txt 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.txt
+timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.txt 2>&1
+timeout 600 python bench.py ${BENCH_ARGS} > gpurun_out/bench.json 2> gpurun_out/bench.err
+if [ -n "${NCU}" ]; then
+  timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python tools/profile_sweep.py > gpurun_out/ncu_launch.log 2>&1
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_halfsweep -s 2 -c 1 -o gpurun_out/prof_halfsweep python tools/profile_sweep.py > gpurun_out/ncu_full.log 2>&1
+fi
+tail -3 gpurun_out/pytest_gpu.txt; cat gpurun_out/smoke.txt; cat gpurun_out/bench.json; tail -5 gpurun_out/bench.err
