@@ -244,8 +244,9 @@ def run_ours(args):
     kms, klaunches = lat.kernel_stats()
     sweep_ms_prof = lat.last_sweep_ms()
     lat.set_profiling(False)
-    # dominant kernel = k_halfsweep; flips per launch = slab rows * M / 2 for n == 1
-    flips_per_launch = rows * M * 2 * kprof_sweeps / max(klaunches, 1)
+    # dominant kernel = k_halfsweep; a sweep attempts rows*M flips over its launches
+    # (2 per sweep for one slab: rows*M/2 flips each)
+    flips_per_launch = rows * M * kprof_sweeps / max(klaunches, 1)
     avg_launch_ms = kms / max(klaunches, 1)
     peaks, peak_src = measured_peaks()
     hbm_gbs = BYTES_PER_FLIP * flips_per_launch / (avg_launch_ms * 1e6)

@@ -63,6 +63,8 @@ def lib() -> ctypes.CDLL:
             "oracle_from_full": (None, [i8p, i8p, i8p, I64, I64]),
             "oracle_observables": (None, [i8p, i8p, I64, I64, i64p, i64p]),
             "oracle_chain": (None, [i8p, i8p, I64, I64, U64, U32, I64, DBL, INT, i64p, i64p]),
+            "oracle_update_slab": (None, [i8p, i8p, i8p, i8p, INT, I64, I64, I64, U64, U32, u64p,
+                                           INT]),
             "oracle_set_threads": (None, [INT]),
             "oracle_get_threads": (INT, []),
         }
@@ -104,6 +106,19 @@ def set_threads(n: int) -> None:
 
 def get_threads() -> int:
     return int(lib().oracle_get_threads())
+
+
+def update_slab(target: np.ndarray, source: np.ndarray, above: np.ndarray, below: np.ndarray,
+                is_black: bool, row0: int, seed: int, t: int, beta: float,
+                rule: int = RULE_METROPOLIS) -> None:
+    """One colour phase on one horizontal slab, in place on ``target``."""
+    T = thresholds(beta, rule)
+    nrows, ny = target.shape
+    for a in (target, source, above, below):
+        assert a.dtype == np.int8 and a.flags["C_CONTIGUOUS"]
+    lib().oracle_update_slab(_p(target, ctypes.c_int8), _p(source, ctypes.c_int8),
+                             _p(above, ctypes.c_int8), _p(below, ctypes.c_int8), int(bool(is_black)),
+                             row0, nrows, ny, seed, t, _p(T, ctypes.c_uint64), rule)
 
 
 class Lattice:

@@ -170,6 +170,46 @@ void oracle_update_lattice(int8_t* lattice, const int8_t* op_lattice, int is_bla
   }
 }
 
+/* The same phase for one horizontal slab of a lattice split across GPUs
+ * (§4: "partitioned into horizontal slabs ... each GPU needs only read
+ * access to the memory of the two GPUs that handle the slabs on top and bottom").
+ * lattice / op_lattice hold the slab's nrows rows (global rows row0 .. row0+nrows-1)
+ * of the target / source colour; op_above / op_below are the source rows of the
+ * neighbouring slabs (global rows row0-1 and row0+nrows, mod N).  Identical to
+ * oracle_update_lattice except that the listing's inn / ipp rows at the slab edge
+ * come from the neighbours, and parity and the draw use the global row (R19). */
+void oracle_update_slab(int8_t* lattice, const int8_t* op_lattice, const int8_t* op_above,
+                        const int8_t* op_below, int is_black, int64_t row0, int64_t nrows,
+                        int64_t ny, uint64_t seed, uint32_t t, const uint64_t T[5], int rule) {
+  const uint32_t colour = is_black ? 0u : 1u;
+  for (int64_t i = 0; i < nrows; ++i) {
+    const int64_t gi = row0 + i;
+    const int8_t* up = (i == 0) ? op_above : op_lattice + (i - 1) * ny;
+    const int8_t* dn = (i == nrows - 1) ? op_below : op_lattice + (i + 1) * ny;
+    const int8_t* me = op_lattice + i * ny;
+    for (int64_t j = 0; j < ny; ++j) {
+      int64_t jpp = (j + 1 < ny) ? j + 1 : 0;
+      int64_t jnn = (j - 1 >= 0) ? j - 1 : ny - 1;
+      int64_t joff;
+      if (is_black) {
+        joff = (gi % 2) ? jpp : jnn;
+      } else {
+        joff = (gi % 2) ? jnn : jpp;
+      }
+      int nn_sum = up[j] + me[j] + dn[j] + me[joff];
+      int8_t lij = lattice[i * ny + j];
+      int e = nn_sum * lij;
+      uint32_t r = oracle_rand(seed, t, colour, (uint32_t)gi, (uint64_t)j);
+      int flip;
+      if (rule == RULE_METROPOLIS)
+        flip = (e <= 0) || ((uint64_t)r < T[(e + 4) / 2]);
+      else
+        flip = (uint64_t)r < T[(e + 4) / 2];
+      if (flip) lattice[i * ny + j] = (int8_t)(-lij);
+    }
+  }
+}
+
 /* Sweeps t0+1 .. t0+nsweeps; each is black then white (reading R7). */
 void oracle_sweep(int8_t* black, int8_t* white, int64_t nx, int64_t ny, uint64_t seed, uint32_t t0,
                   int64_t nsweeps, double beta, int rule) {

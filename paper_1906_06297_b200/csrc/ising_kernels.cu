@@ -74,47 +74,116 @@ __device__ __forceinline__ uint64_t update_word(uint64_t tgt, uint64_t n, uint64
                                                 uint64_t side, uint32_t ctr0, uint32_t row,
                                                 const HalfSweepParams& p);
 
-template <>
-__device__ __forceinline__ uint64_t update_word<0>(uint64_t tgt, uint64_t n, uint64_t c, uint64_t s,
-                                                   uint64_t side, uint32_t ctr0, uint32_t row,
-                                                   const HalfSweepParams& p) {
+// Horner step of the acceptance test for one lane, on the carry chain: the borrow-free
+// carry of r - T is [r >= T] ("no flip for this class"), and madc shifts it into the
+// accumulator's next nibble: acc = 16 acc + [r >= T].  sub.cc -> IADD3 (ALU pipe),
+// madc -> IMAD.X (FMA pipe), so the compare and the bit insertion cost one
+// instruction each on different pipes.
+template <bool SINGLE, int K>
+__device__ __forceinline__ void nc_step(uint32_t& a3, uint32_t& a4, uint32_t r, uint32_t t3,
+                                        uint32_t t4) {
+  if (SINGLE) {
+    // [r >= T3] on the carry chain (IADD3 + IMAD.X on the FMA pipe); [r >= T4] as a
+    // compare + predicated OR (both ALU pipe) into a separate bit-at-nibble accumulator.
+    // Splits the per-lane work between the two pipes.  Here a4's bit is placed by the
+    // caller-supplied `bit` (lane position), a3 by Horner order.
+    asm("{\n\t.reg .u32 d;\n\t"
+        "sub.cc.u32 d, %1, %2;\n\t"
+        "madc.lo.u32 %0, %0, 16, 0;\n\t}"
+        : "+r"(a3)
+        : "r"(r), "r"(t3));
+    asm("{\n\t.reg .pred q;\n\t"
+        "setp.ge.u32 q, %1, %2;\n\t"
+        "@q or.b32 %0, %0, %3;\n\t}"
+        : "+r"(a4)
+        : "r"(r), "r"(t4), "n"(1u << (4 * (K & 7))));
+  } else {
+    asm("{\n\t.reg .u32 d;\n\t"
+        "sub.cc.u32 d, %2, %3;\n\t"
+        "madc.lo.u32 %0, %0, 16, 0;\n\t"
+        "sub.cc.u32 d, %2, %4;\n\t"
+        "madc.lo.u32 %1, %1, 16, 0;\n\t}"
+        : "+r"(a3), "+r"(a4)
+        : "r"(r), "r"(t3), "r"(t4));
+  }
+}
+
+// Flip decision for 8 lanes (one 32-bit half).  With a = aligned neighbours, b = 4 - a
+// (anti-aligned), cnt = [r < T_3] + [r < T_4] and T_4 <= T_3, Metropolis flips iff
+// a - 2 <= cnt, i.e. iff b - nc >= 0 with nc = 2 - cnt = a3 + a4 (the Horner
+// accumulators).  Per lane x = b + 8 - nc lies in [6, 12]; bit 3 of x is the flip bit.
+//   b = s ? 4 - n : n  =  (n ^ 15 s) - 11 s   (n = neighbour sum, s = spin bit)
+__device__ __forceinline__ uint32_t accept8(uint32_t s, uint32_t n, uint32_t nc) {
+  const uint32_t x = (n ^ (s * 15u)) + (s * (uint32_t)-11 + 0x88888888u) - nc;
+  return s ^ ((x >> 3) & kLane0);
+}
+
+// RULE 0: Metropolis, both thresholds < 2^32 (one Horner accumulator per half).
+// RULE 2: Metropolis, generic (a threshold may be 2^32: two accumulators + keep masks).
+template <int RULE>
+__device__ __forceinline__ uint64_t update_word_metropolis(uint64_t tgt, uint64_t n, uint64_t c,
+                                                           uint64_t s, uint64_t side, uint32_t ctr0,
+                                                           uint32_t row, const HalfSweepParams& p) {
+  constexpr bool kSingle = RULE == 0;
   // "three additions are sufficient to compute the neighbors sums":
   // lanes hold 0/1 and sums <= 4, so the 64-bit adds split into independent halves.
   const uint32_t sum_lo = (uint32_t)n + (uint32_t)c + (uint32_t)s + (uint32_t)side;
   const uint32_t sum_hi =
       (uint32_t)(n >> 32) + (uint32_t)(c >> 32) + (uint32_t)(s >> 32) + (uint32_t)(side >> 32);
-  const uint32_t t_lo = (uint32_t)tgt, t_hi = (uint32_t)(tgt >> 32);
-  const Class8 cl = classify8(t_lo, sum_lo);
-  const Class8 ch = classify8(t_hi, sum_hi);
-
-  const uint32_t thr3 = p.acc.thr[3], thr4 = p.acc.thr[4];
-  uint32_t c3lo = 0, c3hi = 0, c4lo = 0, c4hi = 0;
-#pragma unroll
-  for (int b = 0; b < 4; ++b) {
-    const uint4 r = philox4x32_10(ctr0 + b, row, p.t, p.colour, p.keys);
-    const uint32_t rr[4] = {r.x, r.y, r.z, r.w};
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int k = 4 * b + q;
-      const uint32_t bit = 1u << (4 * (k & 7));
-      if (k < 8) {
-        if (rr[q] < thr3) c3lo |= bit;
-        if (rr[q] < thr4) c4lo |= bit;
-      } else {
-        if (rr[q] < thr3) c3hi |= bit;
-        if (rr[q] < thr4) c4hi |= bit;
-      }
-    }
+  const uint32_t t3 = p.acc.thr[3], t4 = p.acc.thr[4];
+  // lanes k = 4b + q; Horner order is lane 7 .. 0 (lo half) and 15 .. 8 (hi half)
+  uint32_t a3lo = 0, a4lo = 0, a3hi = 0, a4hi = 0;
+  {
+    const uint4 r1 = philox4x32_10(ctr0 + 1, row, p.t, p.colour, p.keys);
+    nc_step<kSingle, 7>(a3lo, a4lo, r1.w, t3, t4);
+    nc_step<kSingle, 6>(a3lo, a4lo, r1.z, t3, t4);
+    nc_step<kSingle, 5>(a3lo, a4lo, r1.y, t3, t4);
+    nc_step<kSingle, 4>(a3lo, a4lo, r1.x, t3, t4);
+    const uint4 r0 = philox4x32_10(ctr0 + 0, row, p.t, p.colour, p.keys);
+    nc_step<kSingle, 3>(a3lo, a4lo, r0.w, t3, t4);
+    nc_step<kSingle, 2>(a3lo, a4lo, r0.z, t3, t4);
+    nc_step<kSingle, 1>(a3lo, a4lo, r0.y, t3, t4);
+    nc_step<kSingle, 0>(a3lo, a4lo, r0.x, t3, t4);
   }
-  // classes whose threshold is 2^32 ("always") need no draw
-  const uint32_t need3 = (p.acc.always_mask & 8u) ? 0u : kLane0;
-  const uint32_t need4 = (p.acc.always_mask & 16u) ? 0u : kLane0;
-  const uint32_t is3lo = cl.ge3 & ~cl.is4, is3hi = ch.ge3 & ~ch.is4;
-  const uint32_t needlo = (is3lo & need3) | (cl.is4 & need4);
-  const uint32_t needhi = (is3hi & need3) | (ch.is4 & need4);
-  const uint32_t flo = (~needlo | (c3lo & is3lo) | (c4lo & cl.is4)) & kLane0;
-  const uint32_t fhi = (~needhi | (c3hi & is3hi) | (c4hi & ch.is4)) & kLane0;
-  return tgt ^ (((uint64_t)fhi << 32) | flo);
+  {
+    const uint4 r3 = philox4x32_10(ctr0 + 3, row, p.t, p.colour, p.keys);
+    nc_step<kSingle, 15>(a3hi, a4hi, r3.w, t3, t4);
+    nc_step<kSingle, 14>(a3hi, a4hi, r3.z, t3, t4);
+    nc_step<kSingle, 13>(a3hi, a4hi, r3.y, t3, t4);
+    nc_step<kSingle, 12>(a3hi, a4hi, r3.x, t3, t4);
+    const uint4 r2 = philox4x32_10(ctr0 + 2, row, p.t, p.colour, p.keys);
+    nc_step<kSingle, 11>(a3hi, a4hi, r2.w, t3, t4);
+    nc_step<kSingle, 10>(a3hi, a4hi, r2.z, t3, t4);
+    nc_step<kSingle, 9>(a3hi, a4hi, r2.y, t3, t4);
+    nc_step<kSingle, 8>(a3hi, a4hi, r2.x, t3, t4);
+  }
+  uint32_t nclo, nchi;
+  if (kSingle) {
+    nclo = a3lo + a4lo;
+    nchi = a3hi + a4hi;
+  } else {
+    // a class whose threshold is 2^32 ("always", tiny beta) never blocks a flip
+    const uint32_t k3 = p.acc.keep3, k4 = p.acc.keep4;
+    nclo = (a3lo & k3) + (a4lo & k4);
+    nchi = (a3hi & k3) + (a4hi & k4);
+  }
+  const uint32_t lo = accept8((uint32_t)tgt, sum_lo, nclo);
+  const uint32_t hi = accept8((uint32_t)(tgt >> 32), sum_hi, nchi);
+  return ((uint64_t)hi << 32) | lo;
+}
+
+template <>
+__device__ __forceinline__ uint64_t update_word<0>(uint64_t tgt, uint64_t n, uint64_t c, uint64_t s,
+                                                   uint64_t side, uint32_t ctr0, uint32_t row,
+                                                   const HalfSweepParams& p) {
+  return update_word_metropolis<0>(tgt, n, c, s, side, ctr0, row, p);
+}
+
+template <>
+__device__ __forceinline__ uint64_t update_word<2>(uint64_t tgt, uint64_t n, uint64_t c, uint64_t s,
+                                                   uint64_t side, uint32_t ctr0, uint32_t row,
+                                                   const HalfSweepParams& p) {
+  return update_word_metropolis<2>(tgt, n, c, s, side, ctr0, row, p);
 }
 
 // Heat bath: flip iff r < T[a] for every class.
@@ -153,8 +222,11 @@ __device__ __forceinline__ uint64_t update_word<1>(uint64_t tgt, uint64_t n, uin
 // column q); the thread walks down the band keeping the N/C/S source chunks in
 // registers, so each source word is read from memory once per band (plus one halo
 // row per band).  Grid-stride over items; the grid is a multiple of the SM count.
+#ifndef ISING_MINB
+#define ISING_MINB 1
+#endif
 template <int RULE>
-__global__ void __launch_bounds__(128) k_halfsweep(const HalfSweepParams p) {
+__global__ void __launch_bounds__(128, ISING_MINB) k_halfsweep(const HalfSweepParams p) {
   const int64_t W = p.W;
   const int64_t chunks = W >> 1;
   const uint64_t* src = p.src + W;  // local row r (r = -1 .. R) at src + r * W
@@ -222,6 +294,8 @@ cudaError_t launch_philox_probe(int grid, cudaStream_t st, const PhiloxKeys& K,
 cudaError_t launch_halfsweep(int rule, int grid, cudaStream_t st, const HalfSweepParams& p) {
   if (rule == 0)
     k_halfsweep<0><<<grid, 128, 0, st>>>(p);
+  else if (rule == 2)
+    k_halfsweep<2><<<grid, 128, 0, st>>>(p);
   else
     k_halfsweep<1><<<grid, 128, 0, st>>>(p);
   return cudaGetLastError();

@@ -32,6 +32,7 @@ struct PhiloxKeys {
 struct Accept {
   uint32_t thr[5];
   uint32_t always_mask;
+  uint32_t keep3, keep4;  // Metropolis: 0 if T[a=3] / T[a=4] is 2^32, else ~0
 };
 
 struct HalfSweepParams {

@@ -292,7 +292,11 @@ int run_halfsweep(ising_ctx* h, Slab& s, int c, int r_begin, int r_end, uint64_t
   p.acc = h->acc;
   const bool prof = h->profiling && s.devi == 0;
   if (prof) CU(cudaEventRecord(h->prof_events[2 * h->kernel_launches], d.stream));
-  CU(launch_halfsweep(h->rule, grid, d.stream, p));
+  // kernel variant: 0 = Metropolis with both thresholds < 2^32 (the fast path),
+  // 2 = Metropolis generic (tiny beta), 1 = heat bath
+  int variant = 1;
+  if (h->rule == ISING_RULE_METROPOLIS) variant = (h->acc.keep3 & h->acc.keep4) ? 0 : 2;
+  CU(launch_halfsweep(variant, grid, d.stream, p));
   if (prof) {
     CU(cudaEventRecord(h->prof_events[2 * h->kernel_launches + 1], d.stream));
     ++h->kernel_launches;
@@ -567,10 +571,13 @@ int ising_set_beta(ising_t h, double beta) {
   h->beta = beta;
   compute_thresholds(beta, h->rule, h->T);
   h->acc.always_mask = 0;
+  h->acc.keep3 = h->acc.keep4 = 0xffffffffu;
   for (int a = 0; a < 5; ++a) {
     if (h->T[a] >= (uint64_t(1) << 32)) {
       h->acc.always_mask |= 1u << a;
       h->acc.thr[a] = 0xffffffffu;
+      if (a == 3) h->acc.keep3 = 0;
+      if (a == 4) h->acc.keep4 = 0;
     } else {
       h->acc.thr[a] = (uint32_t)h->T[a];
     }

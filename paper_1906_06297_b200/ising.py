@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libising.so")
+LIB_PATH = os.environ.get("ISING_LIB") or os.path.join(_HERE, "libising.so")
 
 ISING_OK = 0
 ISING_ERR_ARG = -1
