@@ -34,6 +34,19 @@ BETA = 0.4406868
 SEED = 1
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 BYTES_PER_FLIP = 1.5  # 4-bit spins: read target + read source + write target
+MULWIDE_PER_FLIP = 4.5  # varying 32x32->64 multiplies per draw (18 per Philox block / 4)
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+
+
+def ncu_traffic(config: str, n: int):
+    """DRAM bytes per k_halfsweep launch from the committed ncu --set full capture."""
+    try:
+        with open(TRAFFIC_FILE) as f:
+            d = json.load(f)
+    except (OSError, ValueError):
+        return None
+    e = d.get(f"{config}_n{n}")
+    return None if e is None else e.get("dram_bytes_per_launch")
 
 
 def config_for(name: str, n: int):
@@ -251,9 +264,16 @@ def run_ours(args):
     peaks, peak_src = measured_peaks()
     hbm_gbs = BYTES_PER_FLIP * flips_per_launch / (avg_launch_ms * 1e6)
 
-    # ---- ALU roofline denominator: Philox-only draws/ns on this device, now ----
-    philox_peak = ising_probe_philox(local)
+    # ---- ALU roofline: the Philox multiplier.  Every attempted flip needs
+    # one draw = 1/4 Philox4x32-10 block = 4.5 varying 32x32->64 multiplies (18 of the 20
+    # per block; 2 are warp-uniform under reading R6).  IMAD.WIDE.U32 issues on the 16-lane
+    # FMA-heavy pipe of each SMSP in two passes: 8 lanes/clk/SMSP = 32 per SM per clock.
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
+    clk_mhz = clocks.get("sm_mhz") or clocks.get("sm_max_mhz") or 1965.0
+    alu_peak = sms * 32 * clk_mhz * 1e6 / MULWIDE_PER_FLIP / 1e9  # flips/ns
+    philox_probe = ising_probe_philox(local)  # Philox-only draws/ns, same device function
     flips_per_ns_kernel = flips_per_launch / (avg_launch_ms * 1e6)
+    traffic = ncu_traffic(args.config, n)
 
     # ---- end to end through the C ABI with host buffers ----
     e2e = None
@@ -321,16 +341,21 @@ def run_ours(args):
             "roofline": {
                 "bound": "alu",
                 "achieved": flips_per_ns_kernel,
-                "peak": philox_peak,
+                "peak": alu_peak,
                 "unit": "flips/ns",
-                "frac": flips_per_ns_kernel / philox_peak,
-                "traffic": None,
+                "frac": flips_per_ns_kernel / alu_peak,
+                "traffic": traffic,
                 "kernel": "k_halfsweep<0>",
                 "avg_launch_ms": avg_launch_ms,
                 "launches": klaunches,
                 "kernel_share_of_step": kms / max(sweep_ms_prof, 1e-9),
-                "peak_source": "Philox4x32-10-only draws/ns measured in this run (ising_probe_philox); "
-                               "1 draw per attempted flip",
+                "peak_source": f"derived: {sms} SMs x 32 IMAD.WIDE.U32/clk/SM x {clk_mhz:.0f} MHz "
+                               f"(median SM clock in the timed region) / {MULWIDE_PER_FLIP} varying "
+                               "mul.wide per attempted flip (DESIGN.md §5)",
+                "philox_only_probe": {"value": philox_probe, "unit": "draws/ns",
+                                      "frac": flips_per_ns_kernel / philox_probe},
+                "traffic_source": "profiles/ncu_traffic.json (dram__bytes_read.sum + "
+                                  "dram__bytes_write.sum per launch, ncu --set full)",
                 "hbm": {"achieved_gbs": hbm_gbs, "peak_gbs": peaks.get("hbm_gbs"),
                         "frac": hbm_gbs / peaks.get("hbm_gbs", 6650.0), "peak_source": peak_src,
                         "bytes_per_flip": BYTES_PER_FLIP},
