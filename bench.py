@@ -207,13 +207,20 @@ def run_ours(args):
     rank, world, local = dist_env()
     assert world == args.gpus or world == 1, "launch N>1 with torch.distributed.run"
     n = world
-    torch.cuda.set_device(local)
+    # ISING_BENCH_SAME_DEVICE=1 puts every rank on cuda:0 (a functional check of the
+    # multi-rank path on a one-GPU box; its numbers are not scaling results)
+    same_dev = os.environ.get("ISING_BENCH_SAME_DEVICE") == "1"
+    dev = 0 if same_dev else local
+    torch.cuda.set_device(dev)
     dist = None
     if n > 1:
         import torch.distributed as dist_mod
 
         dist = dist_mod
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if same_dev:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
     N, M, scaling, workload = config_for(args.config, n)
 
     def barrier():
@@ -224,12 +231,12 @@ def run_ours(args):
     def allmax(x: float) -> float:
         if dist is None:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if same_dev else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
     if n > 1:
-        lat = IsingLattice.distributed(N, M, SEED, device=local)
+        lat = IsingLattice.distributed(N, M, SEED, device=dev)
     else:
         lat = IsingLattice(N, M, SEED, n_gpus=1)
     row0, rows = lat.slab_info()
@@ -237,7 +244,7 @@ def run_ours(args):
     lat.sweep(args.warmup)
 
     # ---- device-timed region: K sweeps, events inside the library ----
-    clk = ClockSampler(local)
+    clk = ClockSampler(dev)
     barrier()
     clk.start()
     time.sleep(0.3)
@@ -268,31 +275,28 @@ def run_ours(args):
     # one draw = 1/4 Philox4x32-10 block = 4.5 varying 32x32->64 multiplies (18 of the 20
     # per block; 2 are warp-uniform under reading R6).  IMAD.WIDE.U32 issues on the 16-lane
     # FMA-heavy pipe of each SMSP in two passes: 8 lanes/clk/SMSP = 32 per SM per clock.
-    sms = torch.cuda.get_device_properties(local).multi_processor_count
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
     clk_mhz = clocks.get("sm_mhz") or clocks.get("sm_max_mhz") or 1965.0
     alu_peak = sms * 32 * clk_mhz * 1e6 / MULWIDE_PER_FLIP / 1e9  # flips/ns
-    philox_probe = ising_probe_philox(local)  # Philox-only draws/ns, same device function
+    philox_probe = ising_probe_philox(dev)  # Philox-only draws/ns, same device function
     flips_per_ns_kernel = flips_per_launch / (avg_launch_ms * 1e6)
     traffic = ncu_traffic(args.config, n)
 
     # ---- end to end through the C ABI with host buffers ----
+    # Each rank owns its rows: the input is this rank's slab (rows x M int8, pinned host
+    # memory; rank mode exchanges the halo rows on the device), the per-step result the
+    # global observables (16 B), and the final lattice rows come back to pinned memory.
     e2e = None
-    if N * M <= (1 << 34):  # host copy of the full int8 lattice (C5 would need 1 TiB)
-        full = torch.empty((N, M), dtype=torch.int8, pin_memory=True)
-        lat.read_lattice(full.numpy())  # current state as the e2e input (rank rows only)
+    if rows * M <= (1 << 34):
+        slab = torch.empty((rows, M), dtype=torch.int8, pin_memory=True)
         if n > 1:
-            # every rank needs the whole input lattice: rank mode writes its own rows and halos
-            g = torch.empty((N, M), dtype=torch.int8, device="cuda")
-            g[row0:row0 + rows].copy_(full[row0:row0 + rows])
-            # gather slabs (each rank's rows) into every rank's buffer
-            parts = [torch.empty((rows, M), dtype=torch.int8, device="cuda") for _ in range(n)]
-            dist.all_gather(parts, g[row0:row0 + rows].contiguous())
-            full.copy_(torch.cat(parts).cpu())
-            del g, parts
-        out = torch.empty((N, M), dtype=torch.int8, pin_memory=True)
+            lat.read_lattice(slab.numpy())
+        else:
+            lat.read_lattice(slab.numpy().reshape(N, M))
+        out = torch.empty((rows, M), dtype=torch.int8, pin_memory=True)
         barrier()
         t0 = time.perf_counter()
-        lat.write_lattice(full.numpy(), t=0)
+        lat.write_lattice(slab.numpy(), t=0)
         obs = []
         for _ in range(args.steps):
             lat.sweep(1)
@@ -303,12 +307,13 @@ def run_ours(args):
         e2e = {
             "value": N * M * args.steps / (e2e_s * 1e9),
             "unit": "flips/ns",
-            "h2d_bytes_per_step": rows * M // args.steps if n > 1 else N * M // args.steps,
-            "d2h_bytes_per_step": (rows * M if n > 1 else N * M) // args.steps + 16,
-            "how": "write_lattice(pinned int8) + per sweep: ising_sweep(1) + ising_observables; "
-                   "read_lattice(pinned int8); wall clock, max over ranks",
+            "h2d_bytes_per_step": N * M // args.steps,
+            "d2h_bytes_per_step": N * M // args.steps + 16 * n,
+            "how": "per rank: write_lattice(own rows, pinned int8) + per sweep: ising_sweep(1) + "
+                   "ising_observables (all-reduced); read_lattice(own rows, pinned int8); wall "
+                   "clock, max over ranks; bytes summed over ranks",
         }
-        del full, out
+        del slab, out
 
     cpu = None
     if rank == 0 and n == 1 and not args.no_cpu_baseline:

@@ -83,6 +83,20 @@ int ising_create_slabs(ising_t* out, int64_t L_rows, int64_t L_cols, uint64_t se
 int ising_create_rank(ising_t* out, int64_t L_rows, int64_t L_cols, uint64_t seed, int rank,
                       int world, int device, const void* nccl_id, size_t id_len);
 
+/* One process per GPU, halos moved by the half-sweep kernel itself: each rank maps its
+ * neighbours' colour planes (CUDA IPC, NVLink P2P), stores its boundary rows straight
+ * into their halo rows and raises a flag in their memory when the phase is done; the next
+ * phase's kernel waits on the flags of both neighbours (the paper's
+ * "read access to the memory of the two GPUs that handle the slabs on top and bottom",
+ * PAPER.md:227).  After creation every rank exports ising_ipc_handle, the caller
+ * all-gathers the blobs in rank order (e.g. torch.distributed) and passes them to
+ * ising_ipc_connect.  world <= 8.  Ranks may share a device (for testing). */
+#define ISING_IPC_BLOB_BYTES 256
+int ising_create_rank_p2p(ising_t* out, int64_t L_rows, int64_t L_cols, uint64_t seed, int rank,
+                          int world, int device);
+int ising_ipc_handle(ising_t h, void* blob, size_t len);            /* len >= 256 */
+int ising_ipc_connect(ising_t h, const void* blobs, size_t len);    /* world * 256 bytes */
+
 /* Writes an NCCL unique id (id_len >= 128 bytes) into id. */
 int ising_nccl_unique_id(void* id, size_t id_len);
 
@@ -110,8 +124,10 @@ int ising_init_cold(ising_t h);
 /* Load a full lattice from host memory: in[i*L_cols + J] in {-1, +1}, row-major,
  * in_len >= L_rows*L_cols (else RANGE); any other value -> ARG.  Sets the sweep
  * counter to t (the next sweep is t+1) — with the counter-based draws this is an
- * exact resume (checkpoint/restart).  In rank mode every rank
- * passes the full lattice and keeps its own rows. */
+ * exact resume (checkpoint/restart).  Rank mode (world > 1): either
+ * the full lattice (every rank keeps its own rows and halo rows) or exactly this rank's
+ * R x L_cols rows (in_len == R*L_cols; the halo rows are then exchanged on the device).
+ * Collective in rank mode. */
 int ising_write_lattice(ising_t h, const int8_t* in, int64_t in_len, uint64_t t);
 
 /* Run n >= 0 full sweeps (black then white), t += n.  STATE if set_beta or an
@@ -120,8 +136,8 @@ int ising_write_lattice(ising_t h, const int8_t* in, int64_t in_len, uint64_t t)
 int ising_sweep(ising_t h, int64_t n);
 
 /* Unpack to host: out[i*L_cols + J] = spin (i, J) in {-1, +1}, row-major;
- * out_len >= L_rows*L_cols (else RANGE).  In rank mode only this rank's rows
- * are written. */
+ * out_len >= L_rows*L_cols (else RANGE).  Rank mode (world > 1): only this rank's rows
+ * are written — at their global offset, or at offset 0 when out_len == R*L_cols. */
 int ising_read_lattice(ising_t h, int8_t* out, int64_t out_len);
 
 /* Integer observables of the whole lattice (Eq. 1):

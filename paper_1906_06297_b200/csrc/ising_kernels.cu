@@ -83,10 +83,10 @@ template <bool SINGLE, int K>
 __device__ __forceinline__ void nc_step(uint32_t& a3, uint32_t& a4, uint32_t r, uint32_t t3,
                                         uint32_t t4) {
   if (SINGLE) {
-    // [r >= T3] on the carry chain (IADD3 + IMAD.X on the FMA pipe); [r >= T4] as a
-    // compare + predicated OR (both ALU pipe) into a separate bit-at-nibble accumulator.
-    // Splits the per-lane work between the two pipes.  Here a4's bit is placed by the
-    // caller-supplied `bit` (lane position), a3 by Horner order.
+    // [r >= T3] on the carry chain (IADD3 + IMAD.X, Horner order); [r >= T4] as a
+    // compare + predicated OR (ISETP + VIADD) at the lane's bit.  Measured alternatives
+    // (profiles/r01_ncu_halfsweep.md): both on the carry chain, both as compare + OR —
+    // equal speed; an ALU-only insert (3-input LOP3) — 11 % slower.
     asm("{\n\t.reg .u32 d;\n\t"
         "sub.cc.u32 d, %1, %2;\n\t"
         "madc.lo.u32 %0, %0, 16, 0;\n\t}"
@@ -225,8 +225,28 @@ __device__ __forceinline__ uint64_t update_word<1>(uint64_t tgt, uint64_t n, uin
 #ifndef ISING_MINB
 #define ISING_MINB 1
 #endif
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ void spin_until(const unsigned long long* flags, int n,
+                                           unsigned long long v) {
+  for (int k = 0; k < n; ++k)
+    while (ld_acquire_sys(flags + k) < v) __nanosleep(64);
+}
+
 template <int RULE>
 __global__ void __launch_bounds__(128, ISING_MINB) k_halfsweep(const HalfSweepParams p) {
+  if (p.wait_flags) {  // rank-p2p: neighbours done with the previous phase
+    if (threadIdx.x == 0) spin_until(p.wait_flags, 2, p.wait_value);
+    __syncthreads();
+  }
   const int64_t W = p.W;
   const int64_t chunks = W >> 1;
   const uint64_t* src = p.src + W;  // local row r (r = -1 .. R) at src + r * W
@@ -269,6 +289,55 @@ __global__ void __launch_bounds__(128, ISING_MINB) k_halfsweep(const HalfSweepPa
       cv = sv;
     }
   }
+  if (p.signal_up) {  // rank-p2p: the last block publishes "phase done" to both neighbours
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned int prev = atomicAdd(p.done_counter, 1u);
+      if (prev == gridDim.x - 1) {
+        *p.done_counter = 0;  // re-armed for the next launch (stream-ordered)
+        __threadfence_system();
+        st_release_sys(p.signal_up, p.signal_value);
+        st_release_sys(p.signal_dn, p.signal_value);
+      }
+    }
+  }
+}
+
+__global__ void k_sync(const SyncParams p) {
+  if (p.wait_flags) spin_until(p.wait_flags, p.wait_count, p.wait_value);
+  __threadfence_system();
+  for (int k = 0; k < 2; ++k)
+    if (p.signal[k]) st_release_sys(p.signal[k], p.signal_value);
+}
+
+__global__ void k_gather(const GatherParams p) {
+  const unsigned long long up = p.local[0], anti = p.local[1];
+  for (int r = 0; r < p.world; ++r) {
+    unsigned long long* s = p.slots[r] + 3 * p.rank;
+    s[0] = up;
+    s[1] = anti;
+  }
+  __threadfence_system();
+  for (int r = 0; r < p.world; ++r) st_release_sys(p.slots[r] + 3 * p.rank + 2, p.epoch);
+  unsigned long long su = 0, sa = 0;
+  for (int r = 0; r < p.world; ++r) {
+    while (ld_acquire_sys(p.mine + 3 * r + 2) < p.epoch) __nanosleep(64);
+    su += p.mine[3 * r];
+    sa += p.mine[3 * r + 1];
+  }
+  p.out[0] = su;
+  p.out[1] = sa;
+}
+
+cudaError_t launch_sync(cudaStream_t st, const SyncParams& p) {
+  k_sync<<<1, 1, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather(cudaStream_t st, const GatherParams& p) {
+  k_gather<<<1, 1, 0, st>>>(p);
+  return cudaGetLastError();
 }
 
 // Philox-only throughput probe (ALU roofline denominator):

@@ -51,6 +51,38 @@ struct HalfSweepParams {
   uint32_t colour;        // 0 black, 1 white
   PhiloxKeys keys;
   Accept acc;
+  // Peer synchronisation of rank-p2p mode (all null otherwise).  The kernel starts when
+  // both neighbours have finished phase wait_value (their halo stores into this slab are
+  // done and they have finished reading the halo rows this launch overwrites), and its
+  // last block publishes signal_value into the neighbours' flags after a system fence.
+  const unsigned long long* wait_flags;  // this rank's [from_up, from_dn]
+  unsigned long long wait_value;
+  unsigned long long* signal_up;         // upper neighbour's from_dn flag (peer memory)
+  unsigned long long* signal_dn;         // lower neighbour's from_up flag (peer memory)
+  unsigned long long signal_value;
+  unsigned int* done_counter;            // block counter for the last-block signal
+};
+
+// Rank-p2p synchronisation helpers (one thread each).
+struct SyncParams {
+  const unsigned long long* wait_flags;  // spin until all wait_count flags >= wait_value
+  int wait_count;
+  unsigned long long wait_value;
+  unsigned long long* signal[2];         // then store signal_value into these (peer) flags
+  unsigned long long signal_value;
+};
+
+// Observable all-reduce across ranks over peer memory: each rank stores its partials
+// into slot `rank` of every rank's gather area, then spins until all slots carry epoch.
+constexpr int kMaxRanks = 8;
+struct GatherParams {
+  const unsigned long long* local;       // this rank's [up, anti] partials
+  unsigned long long* slots[kMaxRanks];  // rank r's gather area (3 u64 per rank)
+  unsigned long long* mine;              // this rank's gather area
+  unsigned long long* out;               // summed [up, anti]
+  int world;
+  int rank;
+  unsigned long long epoch;
 };
 
 struct InitParams {
@@ -95,6 +127,8 @@ struct UnpackParams {
 };
 
 // Host-side launchers (defined in ising_kernels.cu).
+cudaError_t launch_sync(cudaStream_t st, const SyncParams& p);
+cudaError_t launch_gather(cudaStream_t st, const GatherParams& p);
 cudaError_t launch_halfsweep(int rule, int grid, cudaStream_t st, const HalfSweepParams& p);
 cudaError_t halfsweep_occupancy(int* blocks_per_sm);
 cudaError_t launch_philox_probe(int grid, cudaStream_t st, const PhiloxKeys& K,

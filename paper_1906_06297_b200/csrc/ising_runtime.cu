@@ -77,6 +77,17 @@ int fail_nccl(ncclResult_t r, const char* what, int line) {
   } while (0)
 
 constexpr size_t kStagingBytes = size_t(64) << 20;  // pack/unpack staging chunk
+constexpr size_t kSyncBytes = 4096;                  // rank-p2p flags + gather area
+constexpr uint32_t kIpcMagic = 0x49534e47u;           // "ISNG"
+
+struct IpcBlob {  // ising_ipc_handle payload (<= ISING_IPC_BLOB_BYTES)
+  uint32_t magic;
+  int32_t rank, world, pad;
+  int64_t R, W;
+  cudaIpcMemHandle_t plane[2];
+  cudaIpcMemHandle_t sync;
+};
+static_assert(sizeof(IpcBlob) <= ISING_IPC_BLOB_BYTES, "IPC blob too large");
 
 struct Device {
   int dev = -1;
@@ -124,6 +135,16 @@ struct ising_ctx {
   int64_t launch_count = 0;
   std::vector<cudaEvent_t> prof_events;
   int rows_per_item_override = 0;
+  // rank-p2p transport (ising_create_rank_p2p): halos by peer stores, flags in peer memory
+  bool p2p = false, connected = false;
+  unsigned long long* sync = nullptr;      // [0] from_up, [1] from_dn, [8 + 3 r ..] gather
+  unsigned int* done_counter = nullptr;
+  uint64_t* up_plane[2] = {nullptr, nullptr};
+  uint64_t* dn_plane[2] = {nullptr, nullptr};
+  unsigned long long* peer_sync[kMaxRanks] = {};
+  std::vector<void*> opened;               // IPC mappings to close
+  unsigned long long phase = 0;            // completed phases (init/write count as one)
+  unsigned long long gather_epoch = 0;
 };
 
 namespace {
@@ -239,6 +260,9 @@ void destroy_ctx(ising_ctx* h) {
       if (s.plane[c]) cudaFree(s.plane[c]);
   }
   if (h->comm) ncclCommDestroy(h->comm);
+  for (void* ptr : h->opened) cudaIpcCloseMemHandle(ptr);
+  if (h->sync) cudaFree(h->sync);
+  if (h->done_counter) cudaFree(h->done_counter);
   for (auto& d : h->devs) {
     if (d.dev < 0) continue;
     cudaSetDevice(d.dev);
@@ -274,7 +298,7 @@ int run_halfsweep(ising_ctx* h, Slab& s, int c, int r_begin, int r_end, uint64_t
                      uint64_t* halo_dn, uint32_t t) {
   if (r_end <= r_begin) return ISING_OK;
   Device& d = h->devs[s.devi];
-  HalfSweepParams p;
+  HalfSweepParams p{};
   p.tgt = s.plane[c];
   p.src = s.plane[1 - c];
   p.halo_up = halo_up;
@@ -290,6 +314,16 @@ int run_halfsweep(ising_ctx* h, Slab& s, int c, int r_begin, int r_end, uint64_t
   p.colour = (uint32_t)c;
   p.keys = h->keys;
   p.acc = h->acc;
+  if (h->p2p && h->world > 1) {
+    // wait for both neighbours to finish the previous phase; publish this one
+    const int up = (h->rank + h->world - 1) % h->world, dn = (h->rank + 1) % h->world;
+    p.wait_flags = h->sync;
+    p.wait_value = h->phase;
+    p.signal_up = h->peer_sync[up] + 1;  // I am my upper neighbour's lower neighbour
+    p.signal_dn = h->peer_sync[dn] + 0;
+    p.signal_value = h->phase + 1;
+    p.done_counter = h->done_counter;
+  }
   const bool prof = h->profiling && s.devi == 0;
   if (prof) CU(cudaEventRecord(h->prof_events[2 * h->kernel_launches], d.stream));
   // kernel variant: 0 = Metropolis with both thresholds < 2^32 (the fast path),
@@ -376,6 +410,71 @@ int phase_rank(ising_ctx* h, int c, uint32_t t) {
   return ISING_OK;
 }
 
+// One colour phase, RANK-P2P mode (world >= 2): the half-sweep kernel waits for the
+// neighbours' previous phase, stores its boundary rows straight into their halo rows
+// over NVLink, and its last block raises their flags — compute and exchange in one kernel.
+int phase_p2p(ising_ctx* h, int c, uint32_t t) {
+  Slab& s = h->slabs[0];
+  TRY(run_halfsweep(h, s, c, 0, (int)s.R, h->up_plane[c] + (s.R + 1) * h->W, h->dn_plane[c], t));
+  ++h->phase;
+  return ISING_OK;
+}
+
+// Rank mode after loading only this rank's rows: move both planes' boundary rows into the
+// neighbours' halo rows (peer stores for p2p, ncclSend/Recv for NCCL).
+int exchange_halos(ising_ctx* h) {
+  Slab& s = h->slabs[0];
+  Device& d = h->devs[0];
+  const size_t W = (size_t)h->W;
+  const int R = (int)s.R;
+  if (h->p2p) {
+    for (int c = 0; c < 2; ++c) {
+      CU(cudaMemcpyAsync(h->up_plane[c] + (size_t)(R + 1) * W, s.plane[c] + W, W * 8,
+                         cudaMemcpyDeviceToDevice, d.stream));
+      CU(cudaMemcpyAsync(h->dn_plane[c], s.plane[c] + (size_t)R * W, W * 8,
+                         cudaMemcpyDeviceToDevice, d.stream));
+    }
+    return ISING_OK;
+  }
+  const int up = (h->rank + h->world - 1) % h->world, dn = (h->rank + 1) % h->world;
+  for (int c = 0; c < 2; ++c) {
+    uint64_t* pl = s.plane[c];
+    NC(ncclGroupStart());
+    NC(ncclSend(pl + W, W, ncclUint64, up, h->comm, d.stream));
+    NC(ncclRecv(pl + (size_t)(R + 1) * W, W, ncclUint64, dn, h->comm, d.stream));
+    NC(ncclSend(pl + (size_t)R * W, W, ncclUint64, dn, h->comm, d.stream));
+    NC(ncclRecv(pl, W, ncclUint64, up, h->comm, d.stream));
+    NC(ncclGroupEnd());
+  }
+  return ISING_OK;
+}
+
+// RANK-P2P: wait until both neighbours have finished every phase issued so far (before
+// this rank overwrites its halo rows or reads them).
+int p2p_wait(ising_ctx* h) {
+  if (!(h->p2p && h->world > 1)) return ISING_OK;
+  SyncParams p{};
+  p.wait_flags = h->sync;
+  p.wait_count = 2;
+  p.wait_value = h->phase;
+  CU(launch_sync(h->devs[0].stream, p));
+  ++h->launch_count;
+  return ISING_OK;
+}
+
+// RANK-P2P: a state reset (init / write) counts as a phase: publish it to the neighbours.
+int p2p_publish(ising_ctx* h) {
+  if (!(h->p2p && h->world > 1)) return ISING_OK;
+  const int up = (h->rank + h->world - 1) % h->world, dn = (h->rank + 1) % h->world;
+  SyncParams p{};
+  p.signal[0] = h->peer_sync[up] + 1;
+  p.signal[1] = h->peer_sync[dn] + 0;
+  p.signal_value = ++h->phase;
+  CU(launch_sync(h->devs[0].stream, p));
+  ++h->launch_count;
+  return ISING_OK;
+}
+
 int enable_peers(ising_ctx* h) {
   const int n = (int)h->slabs.size();
   for (int k = 0; k < n; ++k) {
@@ -445,6 +544,11 @@ int create_local(ising_t* out, int64_t N, int64_t M, uint64_t seed, int n_slabs,
 }
 
 int run_init(ising_ctx* h, int cold) {
+  if (h->p2p && h->world > 1 && !h->connected) {
+    g_last_error = "rank-p2p handle used before ising_ipc_connect";
+    return ISING_ERR_STATE;
+  }
+  TRY(p2p_wait(h));
   for (auto& s : h->slabs) {
     Device& d = h->devs[s.devi];
     CU(cudaSetDevice(d.dev));
@@ -463,6 +567,7 @@ int run_init(ising_ctx* h, int cold) {
     CU(cudaGetLastError());
     ++h->launch_count;
   }
+  TRY(p2p_publish(h));
   TRY(sync_all(h));
   h->t = 0;
   h->state_set = true;
@@ -554,6 +659,109 @@ int ising_create_rank(ising_t* out, int64_t L_rows, int64_t L_cols, uint64_t see
   return ISING_OK;
 }
 
+int ising_create_rank_p2p(ising_t* out, int64_t L_rows, int64_t L_cols, uint64_t seed, int rank,
+                          int world, int device) {
+  if (!out || world < 1 || world > kMaxRanks || rank < 0 || rank >= world) return ISING_ERR_ARG;
+  *out = nullptr;
+  TRY(check_shape(L_rows, L_cols, world));
+  ising_ctx* h = new (std::nothrow) ising_ctx;
+  if (!h) return ISING_ERR_OOM;
+  h->N = L_rows;
+  h->M = L_cols;
+  h->W = L_cols / 32;
+  h->seed = seed;
+  h->rank_mode = true;
+  h->p2p = true;
+  h->rank = rank;
+  h->world = world;
+  make_keys(seed, &h->keys);
+  h->devs.emplace_back();
+  int st = setup_device(h->devs[0], device);
+  if (st != ISING_OK) {
+    destroy_ctx(h);
+    return st;
+  }
+  Slab s;
+  s.devi = 0;
+  s.R = L_rows / world;
+  s.row0 = rank * s.R;
+  h->slabs.push_back(s);
+  st = alloc_slabs(h);
+  if (st == ISING_OK) {
+    cudaError_t e = cudaMalloc(&h->sync, kSyncBytes);
+    if (e == cudaSuccess) e = cudaMemset(h->sync, 0, kSyncBytes);
+    if (e == cudaSuccess) e = cudaMalloc(&h->done_counter, sizeof(unsigned int));
+    if (e == cudaSuccess) e = cudaMemset(h->done_counter, 0, sizeof(unsigned int));
+    if (e != cudaSuccess) st = fail_cuda(e, "rank-p2p sync buffers", __LINE__);
+  }
+  if (st != ISING_OK) {
+    destroy_ctx(h);
+    return st;
+  }
+  if (world == 1) {  // its own neighbour: plain fused halos, no flags
+    h->up_plane[0] = h->dn_plane[0] = h->slabs[0].plane[0];
+    h->up_plane[1] = h->dn_plane[1] = h->slabs[0].plane[1];
+    h->connected = true;
+  }
+  const char* env = getenv("ISING_ROWS_PER_ITEM");
+  if (env) h->rows_per_item_override = atoi(env);
+  *out = h;
+  return ISING_OK;
+}
+
+int ising_ipc_handle(ising_t h, void* blob, size_t len) {
+  if (!h || !blob || len < ISING_IPC_BLOB_BYTES || !h->p2p) return ISING_ERR_ARG;
+  IpcBlob b{};
+  b.magic = kIpcMagic;
+  b.rank = h->rank;
+  b.world = h->world;
+  b.R = h->slabs[0].R;
+  b.W = h->W;
+  CU(cudaSetDevice(h->devs[0].dev));
+  CU(cudaIpcGetMemHandle(&b.plane[0], h->slabs[0].plane[0]));
+  CU(cudaIpcGetMemHandle(&b.plane[1], h->slabs[0].plane[1]));
+  CU(cudaIpcGetMemHandle(&b.sync, h->sync));
+  memset(blob, 0, ISING_IPC_BLOB_BYTES);
+  memcpy(blob, &b, sizeof b);
+  return ISING_OK;
+}
+
+int ising_ipc_connect(ising_t h, const void* blobs, size_t len) {
+  if (!h || !h->p2p || !blobs || len < (size_t)h->world * ISING_IPC_BLOB_BYTES) return ISING_ERR_ARG;
+  if (h->connected) return ISING_OK;
+  CU(cudaSetDevice(h->devs[0].dev));
+  const int up = (h->rank + h->world - 1) % h->world, dn = (h->rank + 1) % h->world;
+  std::vector<IpcBlob> all(h->world);
+  for (int r = 0; r < h->world; ++r) {
+    memcpy(&all[r], (const char*)blobs + (size_t)r * ISING_IPC_BLOB_BYTES, sizeof(IpcBlob));
+    if (all[r].magic != kIpcMagic || all[r].rank != r || all[r].world != h->world ||
+        all[r].R != h->slabs[0].R || all[r].W != h->W) {
+      g_last_error = "ising_ipc_connect: blobs not from this lattice / rank order";
+      return ISING_ERR_ARG;
+    }
+  }
+  for (int r = 0; r < h->world; ++r) {
+    if (r == h->rank) {
+      h->peer_sync[r] = h->sync;
+      continue;
+    }
+    void* ptr = nullptr;
+    CU(cudaIpcOpenMemHandle(&ptr, all[r].sync, cudaIpcMemLazyEnablePeerAccess));
+    h->opened.push_back(ptr);
+    h->peer_sync[r] = (unsigned long long*)ptr;
+    if (r == up || r == dn) {
+      for (int c = 0; c < 2; ++c) {
+        CU(cudaIpcOpenMemHandle(&ptr, all[r].plane[c], cudaIpcMemLazyEnablePeerAccess));
+        h->opened.push_back(ptr);
+        if (r == up) h->up_plane[c] = (uint64_t*)ptr;
+        if (r == dn) h->dn_plane[c] = (uint64_t*)ptr;
+      }
+    }
+  }
+  h->connected = true;
+  return ISING_OK;
+}
+
 int ising_destroy(ising_t h) {
   destroy_ctx(h);
   return ISING_OK;
@@ -591,19 +799,27 @@ int ising_init_cold(ising_t h) { return h ? run_init(h, 1) : ISING_ERR_ARG; }
 
 int ising_write_lattice(ising_t h, const int8_t* in, int64_t in_len, uint64_t t) {
   if (!h || !in) return ISING_ERR_ARG;
-  if (in_len < h->N * h->M) return ISING_ERR_RANGE;
   if (t > 0xffffffffull) return ISING_ERR_RANGE;
-  // rank mode packs its rows and halos directly from the full host lattice, so no
-  // exchange is needed either.
+  // Rank mode takes either the full lattice (its rows and halo rows are packed straight
+  // from it) or exactly its own R x M rows (then the halo rows are exchanged on device).
+  const bool slab_only = h->rank_mode && h->world > 1 && in_len == h->slabs[0].R * h->M;
+  if (!slab_only && in_len < h->N * h->M) return ISING_ERR_RANGE;
+  if (h->p2p && h->world > 1 && !h->connected) return ISING_ERR_STATE;
+  TRY(p2p_wait(h));
   for (auto& s : h->slabs) {
     Device& d = h->devs[s.devi];
     CU(cudaSetDevice(d.dev));
     TRY(ensure_staging(d));
     CU(cudaMemsetAsync(d.red, 0, 4 * sizeof(unsigned long long), d.stream));
     const int64_t rows_per_chunk = std::max<int64_t>(1, (int64_t)kStagingBytes / h->M);
-    for (int64_t ra = -1; ra < s.R + 1; ra += rows_per_chunk) {
-      const int64_t rb = std::min<int64_t>(ra + rows_per_chunk, s.R + 1);
-      TRY(h2d_rows(h, d.staging, in, s.row0 + ra, rb - ra, d.stream));
+    const int64_t r_lo = slab_only ? 0 : -1, r_hi = slab_only ? s.R : s.R + 1;
+    for (int64_t ra = r_lo; ra < r_hi; ra += rows_per_chunk) {
+      const int64_t rb = std::min<int64_t>(ra + rows_per_chunk, r_hi);
+      if (slab_only)
+        CU(cudaMemcpyAsync(d.staging, in + ra * h->M, (size_t)((rb - ra) * h->M),
+                           cudaMemcpyHostToDevice, d.stream));
+      else
+        TRY(h2d_rows(h, d.staging, in, s.row0 + ra, rb - ra, d.stream));
       PackParams p;
       p.plane[0] = s.plane[0];
       p.plane[1] = s.plane[1];
@@ -622,6 +838,8 @@ int ising_write_lattice(ising_t h, const int8_t* in, int64_t in_len, uint64_t t)
       ++h->launch_count;
     }
   }
+  if (slab_only) TRY(exchange_halos(h));
+  TRY(p2p_publish(h));
   TRY(sync_all(h));
   for (auto& s : h->slabs) {
     Device& d = h->devs[s.devi];
@@ -641,6 +859,7 @@ int ising_write_lattice(ising_t h, const int8_t* in, int64_t in_len, uint64_t t)
 int ising_sweep(ising_t h, int64_t n) {
   if (!h || n < 0) return ISING_ERR_ARG;
   if (!h->beta_set || !h->state_set) return ISING_ERR_STATE;
+  if (h->p2p && h->world > 1 && !h->connected) return ISING_ERR_STATE;
   if (h->t + (uint64_t)n > 0xffffffffull) return ISING_ERR_RANGE;
   if (h->profiling) {
     const size_t per_phase = std::max<size_t>(3, h->slabs.size());
@@ -660,7 +879,9 @@ int ising_sweep(ising_t h, int64_t n) {
   for (int64_t k = 1; k <= n; ++k) {
     const uint32_t t = (uint32_t)(h->t + (uint64_t)k);
     for (int c = 0; c < 2; ++c) {
-      if (h->rank_mode && h->world > 1)
+      if (h->p2p && h->world > 1)
+        TRY(phase_p2p(h, c, t));
+      else if (h->rank_mode && h->world > 1)
         TRY(phase_rank(h, c, t));
       else
         TRY(phase_local(h, c, t));
@@ -693,7 +914,9 @@ int ising_sweep(ising_t h, int64_t n) {
 
 int ising_read_lattice(ising_t h, int8_t* out, int64_t out_len) {
   if (!h || !out) return ISING_ERR_ARG;
-  if (out_len < h->N * h->M) return ISING_ERR_RANGE;
+  // rank mode: a buffer of exactly R x M receives this rank's rows at offset 0
+  const bool slab_only = h->rank_mode && h->world > 1 && out_len == h->slabs[0].R * h->M;
+  if (!slab_only && out_len < h->N * h->M) return ISING_ERR_RANGE;
   if (!h->state_set) return ISING_ERR_STATE;
   for (auto& s : h->slabs) {
     Device& d = h->devs[s.devi];
@@ -716,8 +939,8 @@ int ising_read_lattice(ising_t h, int8_t* out, int64_t out_len) {
       k_unpack<<<grid, 256, 0, d.stream>>>(p);
       CU(cudaGetLastError());
       ++h->launch_count;
-      CU(cudaMemcpyAsync(out + (s.row0 + ra) * h->M, d.staging, (size_t)((rb - ra) * h->M),
-                         cudaMemcpyDeviceToHost, d.stream));
+      CU(cudaMemcpyAsync(out + ((slab_only ? 0 : s.row0) + ra) * h->M, d.staging,
+                         (size_t)((rb - ra) * h->M), cudaMemcpyDeviceToHost, d.stream));
     }
   }
   TRY(sync_all(h));
@@ -727,6 +950,7 @@ int ising_read_lattice(ising_t h, int8_t* out, int64_t out_len) {
 int ising_observables(ising_t h, int64_t* up_count, int64_t* bond_energy) {
   if (!h || !up_count || !bond_energy) return ISING_ERR_ARG;
   if (!h->state_set) return ISING_ERR_STATE;
+  TRY(p2p_wait(h));  // the neighbours' last phase wrote this slab's white halo rows
   for (auto& d : h->devs) {
     CU(cudaSetDevice(d.dev));
     CU(cudaMemsetAsync(d.red, 0, 2 * sizeof(unsigned long long), d.stream));
@@ -747,7 +971,20 @@ int ising_observables(ising_t h, int64_t* up_count, int64_t* bond_energy) {
     CU(cudaGetLastError());
     ++h->launch_count;
   }
-  if (h->rank_mode && h->world > 1) {
+  if (h->p2p && h->world > 1) {
+    // all-reduce of the two partials over peer memory
+    Device& d = h->devs[0];
+    GatherParams g{};
+    g.local = d.red;
+    for (int r = 0; r < h->world; ++r) g.slots[r] = h->peer_sync[r] + 8;
+    g.mine = h->sync + 8;
+    g.out = d.red;
+    g.world = h->world;
+    g.rank = h->rank;
+    g.epoch = ++h->gather_epoch;
+    CU(launch_gather(d.stream, g));
+    ++h->launch_count;
+  } else if (h->rank_mode && h->world > 1) {
     Device& d = h->devs[0];
     NC(ncclAllReduce(d.red, d.red, 2, ncclUint64, ncclSum, h->comm, d.stream));
   }

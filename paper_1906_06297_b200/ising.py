@@ -26,6 +26,7 @@ ISING_ERR_RANGE = -7
 RULE_METROPOLIS = 0
 RULE_HEATBATH = 1
 NCCL_ID_BYTES = 128
+IPC_BLOB_BYTES = 256
 
 # name -> (restype, argtypes); the exported symbols of include/ising.h
 _VP = ctypes.c_void_p
@@ -36,6 +37,9 @@ SIGNATURES = {
     "ising_create_slabs": (_INT, [ctypes.POINTER(_VP), _I64, _I64, _U64, _INT, ctypes.POINTER(_INT)]),
     "ising_create_rank": (_INT, [ctypes.POINTER(_VP), _I64, _I64, _U64, _INT, _INT, _INT, _VP, _SZ]),
     "ising_nccl_unique_id": (_INT, [_VP, _SZ]),
+    "ising_create_rank_p2p": (_INT, [ctypes.POINTER(_VP), _I64, _I64, _U64, _INT, _INT, _INT]),
+    "ising_ipc_handle": (_INT, [_VP, _VP, _SZ]),
+    "ising_ipc_connect": (_INT, [_VP, _VP, _SZ]),
     "ising_destroy": (_INT, [_VP]),
     "ising_set_beta": (_INT, [_VP, _DBL]),
     "ising_set_rule": (_INT, [_VP, _INT]),
@@ -140,6 +144,25 @@ def ising_create_rank(L_rows: int, L_cols: int, seed: int, rank: int, world: int
     return h.value
 
 
+def ising_create_rank_p2p(L_rows: int, L_cols: int, seed: int, rank: int, world: int,
+                          device: int) -> int:
+    h = _VP()
+    _check(load().ising_create_rank_p2p(ctypes.byref(h), L_rows, L_cols, seed, rank, world, device),
+           "ising_create_rank_p2p")
+    return h.value
+
+
+def ising_ipc_handle(h: int) -> bytes:
+    buf = ctypes.create_string_buffer(IPC_BLOB_BYTES)
+    _check(load().ising_ipc_handle(h, buf, IPC_BLOB_BYTES), "ising_ipc_handle")
+    return buf.raw
+
+
+def ising_ipc_connect(h: int, blobs: bytes) -> None:
+    buf = ctypes.create_string_buffer(blobs, len(blobs))
+    _check(load().ising_ipc_connect(h, buf, len(blobs)), "ising_ipc_connect")
+
+
 def ising_destroy(h: int) -> None:
     _check(load().ising_destroy(h), "ising_destroy")
 
@@ -241,18 +264,33 @@ class IsingLattice:
             self.h = ising_create(self.N, self.M, self.seed, n_gpus)
 
     @classmethod
-    def distributed(cls, L_rows: int, L_cols: int, seed: int = 1, device: int | None = None):
-        """One process per GPU under torch.distributed: rank 0's NCCL id is broadcast
-        through the default process group, then every rank creates its slab."""
+    def distributed(cls, L_rows: int, L_cols: int, seed: int = 1, device: int | None = None,
+                    transport: str | None = None):
+        """One process per GPU under torch.distributed (the default process group does the
+        plumbing: it moves the IPC handle blobs or the NCCL unique id between ranks).
+
+        transport "p2p" (default): the half-sweep kernel stores halo rows into the
+        neighbours' memory and synchronises through flags in peer memory
+        (ising_create_rank_p2p).  "nccl": ncclSend/ncclRecv of the halo rows on a comm
+        stream overlapped with the interior (ising_create_rank)."""
         import torch.distributed as dist
 
+        transport = transport or os.environ.get("ISING_TRANSPORT", "p2p")
         rank, world = dist.get_rank(), dist.get_world_size()
         if device is None:
             device = int(os.environ.get("LOCAL_RANK", rank))
-        obj = [ising_nccl_unique_id() if (rank == 0 and world > 1) else None]
-        if world > 1:
-            dist.broadcast_object_list(obj, src=0)
-        h = ising_create_rank(L_rows, L_cols, seed, rank, world, device, obj[0])
+        if transport == "p2p":
+            h = ising_create_rank_p2p(L_rows, L_cols, seed, rank, world, device)
+            blobs = [None] * world
+            dist.all_gather_object(blobs, ising_ipc_handle(h))
+            ising_ipc_connect(h, b"".join(blobs))
+        elif transport == "nccl":
+            obj = [ising_nccl_unique_id() if (rank == 0 and world > 1) else None]
+            if world > 1:
+                dist.broadcast_object_list(obj, src=0)
+            h = ising_create_rank(L_rows, L_cols, seed, rank, world, device, obj[0])
+        else:
+            raise ValueError(f"unknown transport {transport!r}")
         return cls(L_rows, L_cols, seed, _handle=h)
 
     def close(self):

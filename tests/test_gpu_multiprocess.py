@@ -1,0 +1,94 @@
+"""Multi-process rank mode on one GPU: world 2 and 4 processes, all on cuda:0, each owning a
+row slab and exchanging halo rows by peer stores + flags in peer memory
+(ising_create_rank_p2p, the path bench.py --gpus N uses).  The gathered lattice and the
+all-reduced observables must equal the oracle's bit for bit.  gloo carries only the
+plumbing (IPC handle blobs, the final gather)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, N, M, seed, beta, plan, transport, q):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    from paper_1906_06297_b200.ising import IsingLattice
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        lat = IsingLattice.distributed(N, M, seed, device=0, transport=transport)
+        row0, rows = lat.slab_info()
+        lat.set_beta(beta).init_random()
+        out = []
+        for n in plan:
+            lat.sweep(n)
+            obs = lat.observables()
+            full = np.zeros((N, M), dtype=np.int8)
+            lat.read_lattice(full)
+            parts = [torch.zeros((rows, M), dtype=torch.int8) for _ in range(world)]
+            dist.all_gather(parts, torch.from_numpy(full[row0:row0 + rows].copy()))
+            out.append((obs, torch.cat(parts).numpy()))
+        # load only this rank's rows (halos exchanged on the device), resume at t = 17
+        rng = np.random.default_rng(99)
+        full = np.where(rng.random((N, M)) < 0.6, 1, -1).astype(np.int8)
+        lat.write_lattice(np.ascontiguousarray(full[row0:row0 + rows]), t=17)
+        lat.sweep(2)
+        mine = np.empty((rows, M), dtype=np.int8)
+        lat.read_lattice(mine)
+        parts = [torch.zeros((rows, M), dtype=torch.int8) for _ in range(world)]
+        dist.all_gather(parts, torch.from_numpy(mine))
+        out.append((lat.observables(), torch.cat(parts).numpy()))
+        if rank == 0:
+            q.put(("ok", out))
+        lat.close()
+    except Exception as e:  # pragma: no cover - reported to the parent
+        q.put(("error", f"rank {rank}: {e!r}"))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,N,M", [(2, 64, 128), (4, 128, 64), (2, 4, 64)])
+def test_rank_p2p_matches_oracle(world, N, M):
+    import oracle
+
+    seed, beta, plan = 5, 0.4406868, [1, 3, 6]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, N, M, seed, beta, plan, "p2p", q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    status, payload = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+    assert status == "ok", payload
+    o = oracle.Lattice(N, M, seed).init_random().set_beta(beta)
+    for n, (obs, full) in zip(plan, payload):
+        o.sweep(n)
+        assert np.array_equal(full, o.full()), f"t={o.t}"
+        assert obs == o.observables()
+    rng = np.random.default_rng(99)
+    start = np.where(rng.random((N, M)) < 0.6, 1, -1).astype(np.int8)
+    o = oracle.Lattice(N, M, seed).load_full(start, t=17).set_beta(beta).sweep(2)
+    obs, full = payload[len(plan)]
+    assert np.array_equal(full, o.full()), "slab-only write + resume"
+    assert obs == o.observables()
