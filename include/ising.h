@@ -14,7 +14,7 @@
  * Conventions:
  *   - J = 1; beta = 1/T.  Site (i, J) is black iff i + J is even (R1).
  *   - Draw for plane site (i, j = J/2) of colour c (0 black, 1 white) in sweep t:
- *       r = Philox4x32-10(ctr = {j/4, i, t, c}, key = {lo32(seed), hi32(seed)})[j % 4] (R6).
+ *       r = Philox4x32-10(ctr = {t, j/4, c, i}, key = {lo32(seed), hi32(seed)})[j % 4] (R6).
  *   - Metropolis: with e = s*h (h = sum of the 4 neighbours),
  *     flip iff e <= 0 or r < T[e], T[e] = min(2^32, ceil(2^32 exp(-2 beta e))) (R5),
  *     computed on the host in IEEE double.  Heat bath:

@@ -78,9 +78,9 @@ void oracle_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t
 }
 
 /* The draw for plane site (i, j) of colour c in sweep t (t = 0: initialisation).
- * Reading R6: counter {j/4, i, t, c}, key {lo32(seed), hi32(seed)}, word j%4. */
+ * Reading R6: counter {t, j/4, c, i}, key {lo32(seed), hi32(seed)}, word j%4. */
 uint32_t oracle_rand(uint64_t seed, uint32_t t, uint32_t c, uint32_t i, uint64_t j) {
-  uint32_t ctr[4] = {(uint32_t)(j / 4), i, t, c};
+  uint32_t ctr[4] = {t, (uint32_t)(j / 4), c, i};
   uint32_t key[2] = {(uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32)};
   uint32_t out[4];
   oracle_philox4x32_10(ctr, key, out);

@@ -18,6 +18,9 @@ namespace ising {
 // Philox4x32-10 (Salmon et al., SC'11), the generator the paper uses through
 // cuRAND.  Counter {c0, c1, c2, c3}; the key schedule is
 // precomputed per launch (PhiloxKeys) so each round is 2 IMAD.WIDE.U32 + 2 LOP3.
+// With the site counter {t, j/4, c, i} (reading R6) only word 1 varies across a warp, so
+// round 1's two products and one product each of rounds 2 and 3 are warp-uniform:
+// 16 of the 20 multiplies per block are per-thread work.
 __device__ __forceinline__ uint4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
                                                const PhiloxKeys& K) {
 #pragma unroll
@@ -134,24 +137,24 @@ __device__ __forceinline__ uint64_t update_word_metropolis(uint64_t tgt, uint64_
   // lanes k = 4b + q; Horner order is lane 7 .. 0 (lo half) and 15 .. 8 (hi half)
   uint32_t a3lo = 0, a4lo = 0, a3hi = 0, a4hi = 0;
   {
-    const uint4 r1 = philox4x32_10(ctr0 + 1, row, p.t, p.colour, p.keys);
+    const uint4 r1 = philox4x32_10(p.t, ctr0 + 1, p.colour, row, p.keys);
     nc_step<kSingle, 7>(a3lo, a4lo, r1.w, t3, t4);
     nc_step<kSingle, 6>(a3lo, a4lo, r1.z, t3, t4);
     nc_step<kSingle, 5>(a3lo, a4lo, r1.y, t3, t4);
     nc_step<kSingle, 4>(a3lo, a4lo, r1.x, t3, t4);
-    const uint4 r0 = philox4x32_10(ctr0 + 0, row, p.t, p.colour, p.keys);
+    const uint4 r0 = philox4x32_10(p.t, ctr0 + 0, p.colour, row, p.keys);
     nc_step<kSingle, 3>(a3lo, a4lo, r0.w, t3, t4);
     nc_step<kSingle, 2>(a3lo, a4lo, r0.z, t3, t4);
     nc_step<kSingle, 1>(a3lo, a4lo, r0.y, t3, t4);
     nc_step<kSingle, 0>(a3lo, a4lo, r0.x, t3, t4);
   }
   {
-    const uint4 r3 = philox4x32_10(ctr0 + 3, row, p.t, p.colour, p.keys);
+    const uint4 r3 = philox4x32_10(p.t, ctr0 + 3, p.colour, row, p.keys);
     nc_step<kSingle, 15>(a3hi, a4hi, r3.w, t3, t4);
     nc_step<kSingle, 14>(a3hi, a4hi, r3.z, t3, t4);
     nc_step<kSingle, 13>(a3hi, a4hi, r3.y, t3, t4);
     nc_step<kSingle, 12>(a3hi, a4hi, r3.x, t3, t4);
-    const uint4 r2 = philox4x32_10(ctr0 + 2, row, p.t, p.colour, p.keys);
+    const uint4 r2 = philox4x32_10(p.t, ctr0 + 2, p.colour, row, p.keys);
     nc_step<kSingle, 11>(a3hi, a4hi, r2.w, t3, t4);
     nc_step<kSingle, 10>(a3hi, a4hi, r2.z, t3, t4);
     nc_step<kSingle, 9>(a3hi, a4hi, r2.y, t3, t4);
@@ -200,7 +203,7 @@ __device__ __forceinline__ uint64_t update_word<1>(uint64_t tgt, uint64_t n, uin
   uint64_t flip = 0;
 #pragma unroll
   for (int b = 0; b < 4; ++b) {
-    const uint4 r = philox4x32_10(ctr0 + b, row, p.t, p.colour, p.keys);
+    const uint4 r = philox4x32_10(p.t, ctr0 + b, p.colour, row, p.keys);
     const uint32_t rr[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -223,7 +226,7 @@ __device__ __forceinline__ uint64_t update_word<1>(uint64_t tgt, uint64_t n, uin
 // registers, so each source word is read from memory once per band (plus one halo
 // row per band).  Grid-stride over items; the grid is a multiple of the SM count.
 #ifndef ISING_MINB
-#define ISING_MINB 1
+#define ISING_MINB 4  // 116 registers, 4 blocks/SM: measured best of 1..8 (r01)
 #endif
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
   unsigned long long v;
@@ -348,7 +351,7 @@ __global__ void __launch_bounds__(128) k_philox_probe(PhiloxKeys K, uint32_t blo
   uint32_t acc = 0;
   const uint32_t row = blockIdx.x;
   for (uint32_t b = 0; b < blocks_per_thread; ++b) {
-    const uint4 r = philox4x32_10(b * blockDim.x + threadIdx.x, row, t, 1u, K);
+    const uint4 r = philox4x32_10(t, b * blockDim.x + threadIdx.x, 1u, row, K);
     acc ^= r.x ^ r.y ^ r.z ^ r.w;
   }
   if (acc == 0x9E3779B9u) atomicAdd(sink, 1u);  // practically never; keeps the work live
@@ -394,7 +397,7 @@ __global__ void k_init(const InitParams p) {
       word = 0;
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
-        const uint4 r = philox4x32_10((uint32_t)(4 * w + b), (uint32_t)gi, 0u, (uint32_t)c, p.keys);
+        const uint4 r = philox4x32_10(0u, (uint32_t)(4 * w + b), (uint32_t)c, (uint32_t)gi, p.keys);
         const uint32_t rr[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
         for (int q = 0; q < 4; ++q)

@@ -24,9 +24,9 @@ def test_draw_contract_golden():
 
 
 def test_draw_uses_one_block_per_four_sites():
-    # r(seed,t,c,i,j) is word j&3 of the block with counter {j>>2, i, t, c} (reading R6)
+    # r(seed,t,c,i,j) is word j&3 of the block with counter {t, j>>2, c, i} (reading R6)
     seed = 0x1234_5678_9ABC_DEF0
-    blk = oracle.philox4x32_10([7, 11, 13, 1], [seed & 0xFFFFFFFF, seed >> 32])
+    blk = oracle.philox4x32_10([13, 7, 1, 11], [seed & 0xFFFFFFFF, seed >> 32])
     assert [oracle.rand(seed, 13, 1, 11, 28 + k) for k in range(4)] == list(blk)
 
 
