@@ -34,7 +34,7 @@ BETA = 0.4406868
 SEED = 1
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 BYTES_PER_FLIP = 1.5  # 4-bit spins: read target + read source + write target
-MULWIDE_PER_FLIP = 4.5  # varying 32x32->64 multiplies per draw (18 per Philox block / 4)
+MULWIDE_PER_FLIP = 4.0  # per-thread 32x32->64 multiplies per draw (16 per Philox block / 4, R6)
 TRAFFIC_FILE = os.path.join(ROOT, "profiles", "ncu_traffic.json")
 
 
@@ -156,7 +156,7 @@ def cpu_baseline(cols: int) -> dict:
     # 2048 x cols torus), sweeps sized for ~10-20 s of CPU work on the box's cores
     rows = 2048
     rate, cores, dt = oracle_rate(rows, cols, 1)
-    sweeps = max(1, min(16, int(12.0 / max(dt, 1e-3))))
+    sweeps = max(1, min(256, int(12.0 / max(dt, 1e-3))))
     rate, cores, dt = oracle_rate(rows, cols, sweeps)
     return {"value": rate, "unit": "flips/ns", "cores": cores, "kind": "oracle",
             "sample": f"{rows}x{cols} torus (C3 row width), beta={BETA}, random start seed {SEED}, "
@@ -170,7 +170,7 @@ def run_reference(args):
     N, M, scaling, workload = config_for(args.config, world)
     import oracle
 
-    rows = 2048  # bounded sample: 2048 full-width rows per step
+    rows = 8192  # bounded sample: 8192 full-width rows per step
     lat = oracle.Lattice(rows, M, SEED).init_random().set_beta(BETA)
     for _ in range(args.warmup):
         lat.sweep(1)
@@ -272,8 +272,8 @@ def run_ours(args):
     hbm_gbs = BYTES_PER_FLIP * flips_per_launch / (avg_launch_ms * 1e6)
 
     # ---- ALU roofline: the Philox multiplier.  Every attempted flip needs
-    # one draw = 1/4 Philox4x32-10 block = 4.5 varying 32x32->64 multiplies (18 of the 20
-    # per block; 2 are warp-uniform under reading R6).  IMAD.WIDE.U32 issues on the 16-lane
+    # one draw = 1/4 Philox4x32-10 block = 4 per-thread 32x32->64 multiplies (16 of the 20
+    # per block; 4 are warp-uniform under reading R6's counter {t, j/4, c, i}).  IMAD.WIDE.U32 issues on the 16-lane
     # FMA-heavy pipe of each SMSP in two passes: 8 lanes/clk/SMSP = 32 per SM per clock.
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     clk_mhz = clocks.get("sm_mhz") or clocks.get("sm_max_mhz") or 1965.0

@@ -20,9 +20,32 @@ __device__ __forceinline__ uint32_t hi_dfma(uint32_t c, double mp, double cc) {
   return (uint32_t)__double2loint(__fma_rz(x, mp, cc));    // 2^52 + floor(c M / 2^32)
 }
 
+// V = 3: every hi half via DFMA.RZ with the operand pairs flowing between rounds (the
+// XOR rewrites only the low word of the previous DFMA result, whose high word is the
+// 2^52 exponent already), lo halves via IMAD.
+__device__ __forceinline__ uint4 philox_flow(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                                             const Keys& K, double mp0, double cc0, double mp1,
+                                             double cc1) {
+  double x0 = __hiloint2double(0x43300000, (int)c0);
+  double x2 = __hiloint2double(0x43300000, (int)c2);
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const double h0 = __fma_rz(x0, mp0, cc0);
+    const double h1 = __fma_rz(x2, mp1, cc1);
+    const uint32_t lo0 = (uint32_t)__double2loint(x0) * M0;
+    const uint32_t lo1 = (uint32_t)__double2loint(x2) * M1;
+    x0 = __hiloint2double(__double2hiint(h1), (int)((uint32_t)__double2loint(h1) ^ c1 ^ K.k0[r]));
+    x2 = __hiloint2double(__double2hiint(h0), (int)((uint32_t)__double2loint(h0) ^ c3 ^ K.k1[r]));
+    c1 = lo1;
+    c3 = lo0;
+  }
+  return make_uint4((uint32_t)__double2loint(x0), c1, (uint32_t)__double2loint(x2), c3);
+}
+
 template <int V>
 __device__ __forceinline__ uint4 philox(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, const Keys& K,
                                         double mp0, double cc0, double mp1, double cc1) {
+  if (V == 3) return philox_flow(c0, c1, c2, c3, K, mp0, cc0, mp1, cc1);
 #pragma unroll
   for (int r = 0; r < 10; ++r) {
     uint32_t hi0, lo0, hi1, lo1;
@@ -81,17 +104,18 @@ int main() {
   const double cc1 = 4503599627370496.0 - 1048576.0 * (double)M1;
   const int grid = sms * 16, threads = 128;
   const uint32_t iters = 256;
-  uint32_t* out[3];
-  for (int v = 0; v < 3; ++v) CK(cudaMalloc(&out[v], sizeof(uint32_t) * grid * threads));
+  uint32_t* out[4];
+  for (int v = 0; v < 4; ++v) CK(cudaMalloc(&out[v], sizeof(uint32_t) * grid * threads));
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
-  const char* names[3] = {"wide", "dfma", "mix"};
-  for (int v = 0; v < 3; ++v) {
+  const char* names[4] = {"wide", "dfma", "mix", "flow"};
+  for (int v = 0; v < 4; ++v) {
     float best = 1e30f;
     for (int rep = 0; rep < 5; ++rep) {
       cudaEventRecord(a);
       if (v == 0) k_philox<0><<<grid, threads>>>(K, iters, 7, 3, mp0, cc0, mp1, cc1, out[v]);
       if (v == 1) k_philox<1><<<grid, threads>>>(K, iters, 7, 3, mp0, cc0, mp1, cc1, out[v]);
       if (v == 2) k_philox<2><<<grid, threads>>>(K, iters, 7, 3, mp0, cc0, mp1, cc1, out[v]);
+      if (v == 3) k_philox<3><<<grid, threads>>>(K, iters, 7, 3, mp0, cc0, mp1, cc1, out[v]);
       cudaEventRecord(b); CK(cudaEventSynchronize(b)); CK(cudaGetLastError());
       float ms; cudaEventElapsedTime(&ms, a, b); if (rep && ms < best) best = ms;
     }
@@ -99,10 +123,11 @@ int main() {
     printf("philox %-5s: %.3f ms  %.0f draws/ns\n", names[v], best, draws / (best * 1e6));
   }
   // correctness: all variants fold to the same values
-  uint32_t* h = new uint32_t[3 * grid * threads];
-  for (int v = 0; v < 3; ++v) CK(cudaMemcpy(h + v * grid * threads, out[v], 4 * grid * threads, cudaMemcpyDeviceToHost));
+  uint32_t* h = new uint32_t[4 * grid * threads];
+  for (int v = 0; v < 4; ++v) CK(cudaMemcpy(h + v * grid * threads, out[v], 4 * grid * threads, cudaMemcpyDeviceToHost));
   int bad = 0;
-  for (int i = 0; i < grid * threads; ++i) bad += (h[i] != h[grid * threads + i]) + (h[i] != h[2 * grid * threads + i]);
+  for (int i = 0; i < grid * threads; ++i)
+    for (int v = 1; v < 4; ++v) bad += (h[i] != h[v * grid * threads + i]);
   printf("variants agree: %s (%d mismatches)\n", bad ? "NO" : "yes", bad);
   double* dout; CK(cudaMalloc(&dout, sizeof(double) * grid * threads));
   for (int rep = 0; rep < 3; ++rep) {
