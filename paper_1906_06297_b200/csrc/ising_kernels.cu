@@ -74,7 +74,7 @@ __device__ __forceinline__ Class8 classify8(uint32_t s, uint32_t n) {
 // flip iff a <= 2 (e <= 0) or r < T[e].
 template <int RULE>
 __device__ __forceinline__ uint64_t update_word(uint64_t tgt, uint64_t n, uint64_t c, uint64_t s,
-                                                uint64_t side, uint32_t ctr0, uint32_t row,
+                                                uint64_t side, uint32_t ctr0, uint32_t row, uint32_t t,
                                                 const HalfSweepParams& p);
 
 // Horner step of the acceptance test for one lane, on the carry chain: the borrow-free
@@ -126,7 +126,7 @@ __device__ __forceinline__ uint32_t accept8(uint32_t s, uint32_t n, uint32_t nc)
 template <int RULE>
 __device__ __forceinline__ uint64_t update_word_metropolis(uint64_t tgt, uint64_t n, uint64_t c,
                                                            uint64_t s, uint64_t side, uint32_t ctr0,
-                                                           uint32_t row, const HalfSweepParams& p) {
+                                                           uint32_t row, uint32_t t, const HalfSweepParams& p) {
   constexpr bool kSingle = RULE == 0;
   // "three additions are sufficient to compute the neighbors sums":
   // lanes hold 0/1 and sums <= 4, so the 64-bit adds split into independent halves.
@@ -137,24 +137,24 @@ __device__ __forceinline__ uint64_t update_word_metropolis(uint64_t tgt, uint64_
   // lanes k = 4b + q; Horner order is lane 7 .. 0 (lo half) and 15 .. 8 (hi half)
   uint32_t a3lo = 0, a4lo = 0, a3hi = 0, a4hi = 0;
   {
-    const uint4 r1 = philox4x32_10(p.t, ctr0 + 1, p.colour, row, p.keys);
+    const uint4 r1 = philox4x32_10(t, ctr0 + 1, p.colour, row, p.keys);
     nc_step<kSingle, 7>(a3lo, a4lo, r1.w, t3, t4);
     nc_step<kSingle, 6>(a3lo, a4lo, r1.z, t3, t4);
     nc_step<kSingle, 5>(a3lo, a4lo, r1.y, t3, t4);
     nc_step<kSingle, 4>(a3lo, a4lo, r1.x, t3, t4);
-    const uint4 r0 = philox4x32_10(p.t, ctr0 + 0, p.colour, row, p.keys);
+    const uint4 r0 = philox4x32_10(t, ctr0 + 0, p.colour, row, p.keys);
     nc_step<kSingle, 3>(a3lo, a4lo, r0.w, t3, t4);
     nc_step<kSingle, 2>(a3lo, a4lo, r0.z, t3, t4);
     nc_step<kSingle, 1>(a3lo, a4lo, r0.y, t3, t4);
     nc_step<kSingle, 0>(a3lo, a4lo, r0.x, t3, t4);
   }
   {
-    const uint4 r3 = philox4x32_10(p.t, ctr0 + 3, p.colour, row, p.keys);
+    const uint4 r3 = philox4x32_10(t, ctr0 + 3, p.colour, row, p.keys);
     nc_step<kSingle, 15>(a3hi, a4hi, r3.w, t3, t4);
     nc_step<kSingle, 14>(a3hi, a4hi, r3.z, t3, t4);
     nc_step<kSingle, 13>(a3hi, a4hi, r3.y, t3, t4);
     nc_step<kSingle, 12>(a3hi, a4hi, r3.x, t3, t4);
-    const uint4 r2 = philox4x32_10(p.t, ctr0 + 2, p.colour, row, p.keys);
+    const uint4 r2 = philox4x32_10(t, ctr0 + 2, p.colour, row, p.keys);
     nc_step<kSingle, 11>(a3hi, a4hi, r2.w, t3, t4);
     nc_step<kSingle, 10>(a3hi, a4hi, r2.z, t3, t4);
     nc_step<kSingle, 9>(a3hi, a4hi, r2.y, t3, t4);
@@ -177,23 +177,23 @@ __device__ __forceinline__ uint64_t update_word_metropolis(uint64_t tgt, uint64_
 
 template <>
 __device__ __forceinline__ uint64_t update_word<0>(uint64_t tgt, uint64_t n, uint64_t c, uint64_t s,
-                                                   uint64_t side, uint32_t ctr0, uint32_t row,
+                                                   uint64_t side, uint32_t ctr0, uint32_t row, uint32_t t,
                                                    const HalfSweepParams& p) {
-  return update_word_metropolis<0>(tgt, n, c, s, side, ctr0, row, p);
+  return update_word_metropolis<0>(tgt, n, c, s, side, ctr0, row, t, p);
 }
 
 template <>
 __device__ __forceinline__ uint64_t update_word<2>(uint64_t tgt, uint64_t n, uint64_t c, uint64_t s,
-                                                   uint64_t side, uint32_t ctr0, uint32_t row,
+                                                   uint64_t side, uint32_t ctr0, uint32_t row, uint32_t t,
                                                    const HalfSweepParams& p) {
-  return update_word_metropolis<2>(tgt, n, c, s, side, ctr0, row, p);
+  return update_word_metropolis<2>(tgt, n, c, s, side, ctr0, row, t, p);
 }
 
 // Heat bath: flip iff r < T[a] for every class.
 // T is non-increasing in a, so "r < T[a]" <=> a < #{m : r < T[m]}.
 template <>
 __device__ __forceinline__ uint64_t update_word<1>(uint64_t tgt, uint64_t n, uint64_t c, uint64_t s,
-                                                   uint64_t side, uint32_t ctr0, uint32_t row,
+                                                   uint64_t side, uint32_t ctr0, uint32_t row, uint32_t t,
                                                    const HalfSweepParams& p) {
   const uint64_t sum = n + c + s + side;  // no inter-lane carries (sums <= 4)
   // a = s ? n : 4 - n per lane
@@ -203,7 +203,7 @@ __device__ __forceinline__ uint64_t update_word<1>(uint64_t tgt, uint64_t n, uin
   uint64_t flip = 0;
 #pragma unroll
   for (int b = 0; b < 4; ++b) {
-    const uint4 r = philox4x32_10(p.t, ctr0 + b, p.colour, row, p.keys);
+    const uint4 r = philox4x32_10(t, ctr0 + b, p.colour, row, p.keys);
     const uint32_t rr[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -250,6 +250,8 @@ __global__ void __launch_bounds__(128, ISING_MINB) k_halfsweep(const HalfSweepPa
     if (threadIdx.x == 0) spin_until(p.wait_flags, 2, p.wait_value);
     __syncthreads();
   }
+  // sweep index: absolute, or (CUDA graph replays) a device-resident base + the offset
+  const uint32_t t = p.t_dev ? *p.t_dev + p.t : p.t;
   const int64_t W = p.W;
   const int64_t chunks = W >> 1;
   const uint64_t* src = p.src + W;  // local row r (r = -1 .. R) at src + r * W
@@ -283,8 +285,8 @@ __global__ void __launch_bounds__(128, ISING_MINB) k_halfsweep(const HalfSweepPa
         side1 = (cv.y >> 4) | (sw << 60);
       }
       const uint32_t ctr0 = (uint32_t)(4 * wc);  // Philox counter word 0 = j / 4 (reading R6)
-      tv.x = update_word<RULE>(tv.x, nv.x, cv.x, sv.x, side0, ctr0, (uint32_t)gi, p);
-      tv.y = update_word<RULE>(tv.y, nv.y, cv.y, sv.y, side1, ctr0 + 4, (uint32_t)gi, p);
+      tv.x = update_word<RULE>(tv.x, nv.x, cv.x, sv.x, side0, ctr0, (uint32_t)gi, t, p);
+      tv.y = update_word<RULE>(tv.y, nv.y, cv.y, sv.y, side1, ctr0 + 4, (uint32_t)gi, t, p);
       *reinterpret_cast<ulonglong2*>(tgt + (int64_t)r * W + wc) = tv;
       if (r == 0 && p.halo_up) *reinterpret_cast<ulonglong2*>(p.halo_up + wc) = tv;
       if (r == p.R - 1 && p.halo_dn) *reinterpret_cast<ulonglong2*>(p.halo_dn + wc) = tv;
@@ -331,6 +333,13 @@ __global__ void k_gather(const GatherParams p) {
   }
   p.out[0] = su;
   p.out[1] = sa;
+}
+
+__global__ void k_set_u32(uint32_t* dst, uint32_t v, int add) { *dst = add ? *dst + v : v; }
+
+cudaError_t launch_set_u32(cudaStream_t st, uint32_t* dst, uint32_t v, int add) {
+  k_set_u32<<<1, 1, 0, st>>>(dst, v, add);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_sync(cudaStream_t st, const SyncParams& p) {

@@ -47,7 +47,8 @@ struct HalfSweepParams {
   int32_t r_end;          // one past the last local row to update
   int32_t H;              // rows per work item (register-rolling band)
   int64_t items;          // number of work items = (W / 2) * ceil((r_end - r_begin) / H)
-  uint32_t t;             // sweep index (>= 1)
+  uint32_t t;             // sweep index (>= 1), or the offset added to *t_dev
+  const uint32_t* t_dev;  // graph replays: device-resident sweep base (null otherwise)
   uint32_t colour;        // 0 black, 1 white
   PhiloxKeys keys;
   Accept acc;
@@ -128,6 +129,7 @@ struct UnpackParams {
 
 // Host-side launchers (defined in ising_kernels.cu).
 cudaError_t launch_sync(cudaStream_t st, const SyncParams& p);
+cudaError_t launch_set_u32(cudaStream_t st, uint32_t* dst, uint32_t v, int add);
 cudaError_t launch_gather(cudaStream_t st, const GatherParams& p);
 cudaError_t launch_halfsweep(int rule, int grid, cudaStream_t st, const HalfSweepParams& p);
 cudaError_t halfsweep_occupancy(int* blocks_per_sm);

@@ -145,6 +145,11 @@ struct ising_ctx {
   std::vector<void*> opened;               // IPC mappings to close
   unsigned long long phase = 0;            // completed phases (init/write count as one)
   unsigned long long gather_epoch = 0;
+  // CUDA graph of kGraphSweeps sweeps for small lattices (launch-bound), single device
+  cudaGraphExec_t gexec = nullptr;
+  uint32_t* t_dev = nullptr;               // device-resident sweep base read by the kernels
+  int64_t graph_launches = 0;              // kernel nodes per graph replay
+  bool graphs_enabled = true;
 };
 
 namespace {
@@ -274,6 +279,8 @@ void destroy_ctx(ising_ctx* h) {
     if (d.comm) cudaStreamDestroy(d.comm);
   }
   for (cudaEvent_t e : h->prof_events) cudaEventDestroy(e);
+  if (h->gexec) cudaGraphExecDestroy(h->gexec);
+  if (h->t_dev) cudaFree(h->t_dev);
   delete h;
 }
 
@@ -295,7 +302,7 @@ void halfsweep_geometry(const ising_ctx* h, const Device& d, int64_t rows, int* 
 }
 
 int run_halfsweep(ising_ctx* h, Slab& s, int c, int r_begin, int r_end, uint64_t* halo_up,
-                     uint64_t* halo_dn, uint32_t t) {
+                     uint64_t* halo_dn, uint32_t t, bool t_from_dev = false) {
   if (r_end <= r_begin) return ISING_OK;
   Device& d = h->devs[s.devi];
   HalfSweepParams p{};
@@ -311,6 +318,7 @@ int run_halfsweep(ising_ctx* h, Slab& s, int c, int r_begin, int r_end, uint64_t
   int grid;
   halfsweep_geometry(h, d, r_end - r_begin, &p.H, &p.items, &grid);
   p.t = t;
+  p.t_dev = t_from_dev ? h->t_dev : nullptr;
   p.colour = (uint32_t)c;
   p.keys = h->keys;
   p.acc = h->acc;
@@ -349,7 +357,7 @@ int sync_all(ising_ctx* h) {
 }
 
 // One colour phase, LOCAL mode.
-int phase_local(ising_ctx* h, int c, uint32_t t) {
+int phase_local(ising_ctx* h, int c, uint32_t t, bool t_from_dev = false) {
   const int n = (int)h->slabs.size();
   const bool multi_dev = h->devs.size() > 1;
   if (multi_dev) {
@@ -374,7 +382,8 @@ int phase_local(ising_ctx* h, int c, uint32_t t) {
     CU(cudaSetDevice(h->devs[s.devi].dev));
     // local row 0 -> upper slab's bottom halo (padded row R+1); local row R-1 -> lower
     // slab's top halo (padded row 0).
-    TRY(run_halfsweep(h, s, c, 0, (int)s.R, up.plane[c] + (up.R + 1) * h->W, dn.plane[c], t));
+    TRY(run_halfsweep(h, s, c, 0, (int)s.R, up.plane[c] + (up.R + 1) * h->W, dn.plane[c], t,
+                      t_from_dev));
   }
   if (multi_dev) {
     for (auto& d : h->devs) {
@@ -475,6 +484,44 @@ int p2p_publish(ising_ctx* h) {
   return ISING_OK;
 }
 
+// Small lattices are launch-bound (a C2 half-sweep is ~1.5 us of GPU work): sweeps are
+// replayed from a CUDA graph of kGraphSweeps sweeps whose kernels read the sweep base from
+// device memory (h->t_dev) and whose last node advances it.  Single-device LOCAL mode only.
+constexpr int kGraphSweeps = 64;
+constexpr int64_t kGraphMaxSpins = int64_t(1) << 26;
+
+bool graph_eligible(const ising_ctx* h) {
+  return h->graphs_enabled && !h->rank_mode && h->devs.size() == 1 && !h->profiling &&
+         h->N * h->M <= kGraphMaxSpins;
+}
+
+int build_graph(ising_ctx* h) {
+  Device& d = h->devs[0];
+  CU(cudaSetDevice(d.dev));
+  if (!h->t_dev) CU(cudaMalloc(&h->t_dev, sizeof(uint32_t)));
+  if (h->gexec) {
+    CU(cudaGraphExecDestroy(h->gexec));
+    h->gexec = nullptr;
+  }
+  const int64_t before = h->launch_count;
+  cudaGraph_t g = nullptr;
+  CU(cudaStreamBeginCapture(d.stream, cudaStreamCaptureModeThreadLocal));
+  int st = ISING_OK;
+  for (int k = 1; k <= kGraphSweeps && st == ISING_OK; ++k)
+    for (int c = 0; c < 2 && st == ISING_OK; ++c) st = phase_local(h, c, (uint32_t)k, true);
+  cudaError_t e = launch_set_u32(d.stream, h->t_dev, kGraphSweeps, 1);
+  cudaError_t e2 = cudaStreamEndCapture(d.stream, &g);
+  if (st != ISING_OK) return st;
+  CU(e);
+  CU(e2);
+  e = cudaGraphInstantiate(&h->gexec, g, 0);
+  cudaGraphDestroy(g);
+  CU(e);
+  h->graph_launches = h->launch_count - before + 1;
+  h->launch_count = before;
+  return ISING_OK;
+}
+
 int enable_peers(ising_ctx* h) {
   const int n = (int)h->slabs.size();
   for (int k = 0; k < n; ++k) {
@@ -539,6 +586,8 @@ int create_local(ising_t* out, int64_t N, int64_t M, uint64_t seed, int n_slabs,
   }
   const char* env = getenv("ISING_ROWS_PER_ITEM");
   if (env) h->rows_per_item_override = atoi(env);
+  const char* genv = getenv("ISING_GRAPHS");
+  if (genv && genv[0] == '0') h->graphs_enabled = false;
   *out = h;
   return ISING_OK;
 }
@@ -770,6 +819,10 @@ int ising_destroy(ising_t h) {
 int ising_set_rule(ising_t h, int rule) {
   if (!h || (rule != ISING_RULE_METROPOLIS && rule != ISING_RULE_HEATBATH)) return ISING_ERR_ARG;
   h->rule = rule;
+  if (h->gexec) {  // the graph bakes the kernel variant and thresholds
+    cudaGraphExecDestroy(h->gexec);
+    h->gexec = nullptr;
+  }
   if (h->beta_set) return ising_set_beta(h, h->beta);
   return ISING_OK;
 }
@@ -777,6 +830,10 @@ int ising_set_rule(ising_t h, int rule) {
 int ising_set_beta(ising_t h, double beta) {
   if (!h || std::isnan(beta) || beta < 0) return ISING_ERR_ARG;
   h->beta = beta;
+  if (h->gexec) {
+    cudaGraphExecDestroy(h->gexec);
+    h->gexec = nullptr;
+  }
   compute_thresholds(beta, h->rule, h->T);
   h->acc.always_mask = 0;
   h->acc.keep3 = h->acc.keep4 = 0xffffffffu;
@@ -876,7 +933,20 @@ int ising_sweep(ising_t h, int64_t n) {
     CU(cudaSetDevice(d.dev));
     CU(cudaEventRecord(d.ev_t0, d.stream));
   }
-  for (int64_t k = 1; k <= n; ++k) {
+  int64_t k0 = 1;
+  if (graph_eligible(h) && n >= kGraphSweeps) {
+    if (!h->gexec) TRY(build_graph(h));
+    Device& d = h->devs[0];
+    CU(launch_set_u32(d.stream, h->t_dev, (uint32_t)h->t, 0));
+    ++h->launch_count;
+    const int64_t reps = n / kGraphSweeps;
+    for (int64_t r = 0; r < reps; ++r) {
+      CU(cudaGraphLaunch(h->gexec, d.stream));
+      h->launch_count += h->graph_launches;
+    }
+    k0 = reps * kGraphSweeps + 1;
+  }
+  for (int64_t k = k0; k <= n; ++k) {
     const uint32_t t = (uint32_t)(h->t + (uint64_t)k);
     for (int c = 0; c < 2; ++c) {
       if (h->p2p && h->world > 1)

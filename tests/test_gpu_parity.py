@@ -222,3 +222,17 @@ def test_full_size_c3_one_sweep_matches_oracle():
     exp = o.full()
     assert hashlib.sha256(got.tobytes()).digest() == hashlib.sha256(exp.tobytes()).digest()
     assert up_g == o.observables()
+
+
+def test_graph_replay_across_beta_and_rule_changes():
+    # small lattices replay sweeps from a CUDA graph (64 sweeps per replay, sweep base in
+    # device memory); set_beta / set_rule must rebuild it.  Plans mix replays and remainders.
+    N, M = 128, 192
+    g = gpu_lattice(N, M, 8, "random", 0.3)
+    o = oracle_lattice(N, M, 8, "random", 0.3)
+    for beta, rule, n in [(0.3, 0, 130), (0.4406868, 0, 64), (0.4406868, 1, 70), (0.8, 0, 200)]:
+        g.set_beta(beta, rule)
+        o.set_beta(beta, rule)
+        g.sweep(n)
+        o.sweep(n)
+        assert_same(g, o, f"beta={beta} rule={rule} t={o.t}")
