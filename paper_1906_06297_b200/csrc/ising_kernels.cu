@@ -77,38 +77,21 @@ __device__ __forceinline__ uint64_t update_word(uint64_t tgt, uint64_t n, uint64
                                                 uint64_t side, uint32_t ctr0, uint32_t row, uint32_t t,
                                                 const HalfSweepParams& p);
 
-// Horner step of the acceptance test for one lane, on the carry chain: the borrow-free
-// carry of r - T is [r >= T] ("no flip for this class"), and madc shifts it into the
-// accumulator's next nibble: acc = 16 acc + [r >= T].  sub.cc -> IADD3 (ALU pipe),
-// madc -> IMAD.X (FMA pipe), so the compare and the bit insertion cost one
-// instruction each on different pipes.
-template <bool SINGLE, int K>
+// Acceptance test of one lane against both thresholds, on the carry chain: the
+// borrow-free carry of r - T is [r >= T] ("no flip for this class"), and madc shifts it
+// into the accumulator's next nibble, acc = 16 acc + carry (sub.cc -> IADD3 on the ALU
+// pipe, madc -> IMAD.X on the FMA pipe), so lanes arrive in descending order.  Measured
+// alternatives (profiles/r01_ncu_halfsweep.md): ISETP + predicated OR for one threshold —
+// 1 % slower; an ALU-only insert (3-input LOP3) — 11 % slower.
 __device__ __forceinline__ void nc_step(uint32_t& a3, uint32_t& a4, uint32_t r, uint32_t t3,
                                         uint32_t t4) {
-  if (SINGLE) {
-    // [r >= T3] on the carry chain (IADD3 + IMAD.X, Horner order); [r >= T4] as a
-    // compare + predicated OR (ISETP + VIADD) at the lane's bit.  Measured alternatives
-    // (profiles/r01_ncu_halfsweep.md): both on the carry chain, both as compare + OR —
-    // equal speed; an ALU-only insert (3-input LOP3) — 11 % slower.
-    asm("{\n\t.reg .u32 d;\n\t"
-        "sub.cc.u32 d, %1, %2;\n\t"
-        "madc.lo.u32 %0, %0, 16, 0;\n\t}"
-        : "+r"(a3)
-        : "r"(r), "r"(t3));
-    asm("{\n\t.reg .pred q;\n\t"
-        "setp.ge.u32 q, %1, %2;\n\t"
-        "@q or.b32 %0, %0, %3;\n\t}"
-        : "+r"(a4)
-        : "r"(r), "r"(t4), "n"(1u << (4 * (K & 7))));
-  } else {
-    asm("{\n\t.reg .u32 d;\n\t"
-        "sub.cc.u32 d, %2, %3;\n\t"
-        "madc.lo.u32 %0, %0, 16, 0;\n\t"
-        "sub.cc.u32 d, %2, %4;\n\t"
-        "madc.lo.u32 %1, %1, 16, 0;\n\t}"
-        : "+r"(a3), "+r"(a4)
-        : "r"(r), "r"(t3), "r"(t4));
-  }
+  asm("{\n\t.reg .u32 d;\n\t"
+      "sub.cc.u32 d, %2, %3;\n\t"
+      "madc.lo.u32 %0, %0, 16, 0;\n\t"
+      "sub.cc.u32 d, %2, %4;\n\t"
+      "madc.lo.u32 %1, %1, 16, 0;\n\t}"
+      : "+r"(a3), "+r"(a4)
+      : "r"(r), "r"(t3), "r"(t4));
 }
 
 // Flip decision for 8 lanes (one 32-bit half).  With a = aligned neighbours, b = 4 - a
@@ -121,8 +104,8 @@ __device__ __forceinline__ uint32_t accept8(uint32_t s, uint32_t n, uint32_t nc)
   return s ^ ((x >> 3) & kLane0);
 }
 
-// RULE 0: Metropolis, both thresholds < 2^32 (one Horner accumulator per half).
-// RULE 2: Metropolis, generic (a threshold may be 2^32: two accumulators + keep masks).
+// RULE 0: Metropolis, both thresholds < 2^32.
+// RULE 2: Metropolis, generic (a threshold may be 2^32: the accumulators are masked).
 template <int RULE>
 __device__ __forceinline__ uint64_t update_word_metropolis(uint64_t tgt, uint64_t n, uint64_t c,
                                                            uint64_t s, uint64_t side, uint32_t ctr0,
@@ -138,27 +121,27 @@ __device__ __forceinline__ uint64_t update_word_metropolis(uint64_t tgt, uint64_
   uint32_t a3lo = 0, a4lo = 0, a3hi = 0, a4hi = 0;
   {
     const uint4 r1 = philox4x32_10(t, ctr0 + 1, p.colour, row, p.keys);
-    nc_step<kSingle, 7>(a3lo, a4lo, r1.w, t3, t4);
-    nc_step<kSingle, 6>(a3lo, a4lo, r1.z, t3, t4);
-    nc_step<kSingle, 5>(a3lo, a4lo, r1.y, t3, t4);
-    nc_step<kSingle, 4>(a3lo, a4lo, r1.x, t3, t4);
+    nc_step(a3lo, a4lo, r1.w, t3, t4);
+    nc_step(a3lo, a4lo, r1.z, t3, t4);
+    nc_step(a3lo, a4lo, r1.y, t3, t4);
+    nc_step(a3lo, a4lo, r1.x, t3, t4);
     const uint4 r0 = philox4x32_10(t, ctr0 + 0, p.colour, row, p.keys);
-    nc_step<kSingle, 3>(a3lo, a4lo, r0.w, t3, t4);
-    nc_step<kSingle, 2>(a3lo, a4lo, r0.z, t3, t4);
-    nc_step<kSingle, 1>(a3lo, a4lo, r0.y, t3, t4);
-    nc_step<kSingle, 0>(a3lo, a4lo, r0.x, t3, t4);
+    nc_step(a3lo, a4lo, r0.w, t3, t4);
+    nc_step(a3lo, a4lo, r0.z, t3, t4);
+    nc_step(a3lo, a4lo, r0.y, t3, t4);
+    nc_step(a3lo, a4lo, r0.x, t3, t4);
   }
   {
     const uint4 r3 = philox4x32_10(t, ctr0 + 3, p.colour, row, p.keys);
-    nc_step<kSingle, 15>(a3hi, a4hi, r3.w, t3, t4);
-    nc_step<kSingle, 14>(a3hi, a4hi, r3.z, t3, t4);
-    nc_step<kSingle, 13>(a3hi, a4hi, r3.y, t3, t4);
-    nc_step<kSingle, 12>(a3hi, a4hi, r3.x, t3, t4);
+    nc_step(a3hi, a4hi, r3.w, t3, t4);
+    nc_step(a3hi, a4hi, r3.z, t3, t4);
+    nc_step(a3hi, a4hi, r3.y, t3, t4);
+    nc_step(a3hi, a4hi, r3.x, t3, t4);
     const uint4 r2 = philox4x32_10(t, ctr0 + 2, p.colour, row, p.keys);
-    nc_step<kSingle, 11>(a3hi, a4hi, r2.w, t3, t4);
-    nc_step<kSingle, 10>(a3hi, a4hi, r2.z, t3, t4);
-    nc_step<kSingle, 9>(a3hi, a4hi, r2.y, t3, t4);
-    nc_step<kSingle, 8>(a3hi, a4hi, r2.x, t3, t4);
+    nc_step(a3hi, a4hi, r2.w, t3, t4);
+    nc_step(a3hi, a4hi, r2.z, t3, t4);
+    nc_step(a3hi, a4hi, r2.y, t3, t4);
+    nc_step(a3hi, a4hi, r2.x, t3, t4);
   }
   uint32_t nclo, nchi;
   if (kSingle) {
@@ -189,7 +172,72 @@ __device__ __forceinline__ uint64_t update_word<2>(uint64_t tgt, uint64_t n, uin
   return update_word_metropolis<2>(tgt, n, c, s, side, ctr0, row, t, p);
 }
 
-// Heat bath: flip iff r < T[a] for every class.
+// Heat bath, fast path (all five thresholds < 2^32, i.e. any finite beta < ~4.6): the
+// Horner accumulator counts nc = #{m : r >= T[m]} per lane on the carry chain (one madc
+// and four addc per lane), and since T is non-increasing in a, r < T[a] <=> a + nc <= 4.
+// With B = a + 3 from classify's SWAR form, x = B + nc <= 12 and flip <=> bit 3 of x clear.
+template <int K>
+__device__ __forceinline__ void hb_step(uint32_t& acc, uint32_t r, const uint32_t* T) {
+  asm("{\n\t.reg .u32 d;\n\t"
+      "sub.cc.u32 d, %1, %2;\n\t"
+      "madc.lo.u32 %0, %0, 16, 0;\n\t"
+      "sub.cc.u32 d, %1, %3;\n\t"
+      "addc.u32 %0, %0, 0;\n\t"
+      "sub.cc.u32 d, %1, %4;\n\t"
+      "addc.u32 %0, %0, 0;\n\t"
+      "sub.cc.u32 d, %1, %5;\n\t"
+      "addc.u32 %0, %0, 0;\n\t"
+      "sub.cc.u32 d, %1, %6;\n\t"
+      "addc.u32 %0, %0, 0;\n\t}"
+      : "+r"(acc)
+      : "r"(r), "r"(T[0]), "r"(T[1]), "r"(T[2]), "r"(T[3]), "r"(T[4]));
+}
+
+__device__ __forceinline__ uint32_t hb_accept8(uint32_t s, uint32_t n, uint32_t nc) {
+  const uint32_t B = (n + 3u * s) ^ (7u * s) ^ 0x77777777u;  // a + 3 per lane
+  const uint32_t x = B + nc;
+  return s ^ ((~x >> 3) & kLane0);
+}
+
+template <>
+__device__ __forceinline__ uint64_t update_word<3>(uint64_t tgt, uint64_t n, uint64_t c, uint64_t s,
+                                                   uint64_t side, uint32_t ctr0, uint32_t row, uint32_t t,
+                                                   const HalfSweepParams& p) {
+  const uint32_t sum_lo = (uint32_t)n + (uint32_t)c + (uint32_t)s + (uint32_t)side;
+  const uint32_t sum_hi =
+      (uint32_t)(n >> 32) + (uint32_t)(c >> 32) + (uint32_t)(s >> 32) + (uint32_t)(side >> 32);
+  const uint32_t* T = p.acc.thr;
+  uint32_t lo = 0, hi = 0;
+  {
+    const uint4 r1 = philox4x32_10(t, ctr0 + 1, p.colour, row, p.keys);
+    hb_step<7>(lo, r1.w, T);
+    hb_step<6>(lo, r1.z, T);
+    hb_step<5>(lo, r1.y, T);
+    hb_step<4>(lo, r1.x, T);
+    const uint4 r0 = philox4x32_10(t, ctr0 + 0, p.colour, row, p.keys);
+    hb_step<3>(lo, r0.w, T);
+    hb_step<2>(lo, r0.z, T);
+    hb_step<1>(lo, r0.y, T);
+    hb_step<0>(lo, r0.x, T);
+  }
+  {
+    const uint4 r3 = philox4x32_10(t, ctr0 + 3, p.colour, row, p.keys);
+    hb_step<15>(hi, r3.w, T);
+    hb_step<14>(hi, r3.z, T);
+    hb_step<13>(hi, r3.y, T);
+    hb_step<12>(hi, r3.x, T);
+    const uint4 r2 = philox4x32_10(t, ctr0 + 2, p.colour, row, p.keys);
+    hb_step<11>(hi, r2.w, T);
+    hb_step<10>(hi, r2.z, T);
+    hb_step<9>(hi, r2.y, T);
+    hb_step<8>(hi, r2.x, T);
+  }
+  const uint32_t flo = hb_accept8((uint32_t)tgt, sum_lo, lo);
+  const uint32_t fhi = hb_accept8((uint32_t)(tgt >> 32), sum_hi, hi);
+  return ((uint64_t)fhi << 32) | flo;
+}
+
+// Heat bath, generic (some threshold is 2^32): flip iff r < T[a] for every class.
 // T is non-increasing in a, so "r < T[a]" <=> a < #{m : r < T[m]}.
 template <>
 __device__ __forceinline__ uint64_t update_word<1>(uint64_t tgt, uint64_t n, uint64_t c, uint64_t s,
@@ -377,6 +425,8 @@ cudaError_t launch_halfsweep(int rule, int grid, cudaStream_t st, const HalfSwee
     k_halfsweep<0><<<grid, 128, 0, st>>>(p);
   else if (rule == 2)
     k_halfsweep<2><<<grid, 128, 0, st>>>(p);
+  else if (rule == 3)
+    k_halfsweep<3><<<grid, 128, 0, st>>>(p);
   else
     k_halfsweep<1><<<grid, 128, 0, st>>>(p);
   return cudaGetLastError();

@@ -336,7 +336,8 @@ int run_halfsweep(ising_ctx* h, Slab& s, int c, int r_begin, int r_end, uint64_t
   if (prof) CU(cudaEventRecord(h->prof_events[2 * h->kernel_launches], d.stream));
   // kernel variant: 0 = Metropolis with both thresholds < 2^32 (the fast path),
   // 2 = Metropolis generic (tiny beta), 1 = heat bath
-  int variant = 1;
+  // 3 = heat bath with all thresholds < 2^32 (the fast path), 1 = heat bath generic
+  int variant = (h->acc.always_mask == 0) ? 3 : 1;
   if (h->rule == ISING_RULE_METROPOLIS) variant = (h->acc.keep3 & h->acc.keep4) ? 0 : 2;
   CU(launch_halfsweep(variant, grid, d.stream, p));
   if (prof) {
