@@ -146,6 +146,15 @@ int ising_read_lattice(ising_t h, int8_t* out, int64_t out_len);
  * Collective in rank mode (int64 all-reduce over NCCL). */
 int ising_observables(ising_t h, int64_t* up_count, int64_t* bond_energy);
 
+/* A measured chain (the Fig. 5 / Fig. 6 methodology): n_samples
+ * times, run `every` sweeps and record the observables of the resulting state into
+ * up_counts[k] / bond_energies[k] (caller-owned arrays of n_samples).  The samples are
+ * reduced on the device into a device-side series and copied back once, so the chain
+ * does not synchronise per sample.  t += n_samples * every.  Same errors as ising_sweep;
+ * in rank mode every rank receives the global values. */
+int ising_sweep_measure(ising_t h, int64_t n_samples, int64_t every, int64_t* up_counts,
+                        int64_t* bond_energies);
+
 /* ------------------------------------------------------------ introspection */
 
 /* CUDA-event time of the last ising_sweep on this process's devices (max over

@@ -101,6 +101,8 @@ struct Device {
   cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;
   int8_t* staging = nullptr;
   unsigned long long* red = nullptr;  // [0] up, [1] antiparallel, [2] bad-value flag
+  unsigned long long* meas = nullptr; // ising_sweep_measure: 2 per sample
+  size_t meas_cap = 0;
 };
 
 struct Slab {
@@ -273,6 +275,7 @@ void destroy_ctx(ising_ctx* h) {
     cudaSetDevice(d.dev);
     if (d.staging) cudaFree(d.staging);
     if (d.red) cudaFree(d.red);
+    if (d.meas) cudaFree(d.meas);
     for (cudaEvent_t e : {d.ev_phase, d.ev_bnd, d.ev_comm, d.ev_t0, d.ev_t1})
       if (e) cudaEventDestroy(e);
     if (d.stream) cudaStreamDestroy(d.stream);
@@ -638,6 +641,58 @@ int h2d_rows(ising_ctx* h, int8_t* dst, const int8_t* in, int64_t g, int64_t n, 
   return ISING_OK;
 }
 
+// Enqueue sweeps t+1 .. t+n on the handle's streams (no synchronisation); t += n.
+int enqueue_sweeps(ising_ctx* h, int64_t n) {
+  int64_t k0 = 1;
+  if (graph_eligible(h) && n >= kGraphSweeps) {
+    if (!h->gexec) TRY(build_graph(h));
+    Device& d = h->devs[0];
+    CU(launch_set_u32(d.stream, h->t_dev, (uint32_t)h->t, 0));
+    ++h->launch_count;
+    const int64_t reps = n / kGraphSweeps;
+    for (int64_t r = 0; r < reps; ++r) {
+      CU(cudaGraphLaunch(h->gexec, d.stream));
+      h->launch_count += h->graph_launches;
+    }
+    k0 = reps * kGraphSweeps + 1;
+  }
+  for (int64_t k = k0; k <= n; ++k) {
+    const uint32_t t = (uint32_t)(h->t + (uint64_t)k);
+    for (int c = 0; c < 2; ++c) {
+      if (h->p2p && h->world > 1)
+        TRY(phase_p2p(h, c, t));
+      else if (h->rank_mode && h->world > 1)
+        TRY(phase_rank(h, c, t));
+      else
+        TRY(phase_local(h, c, t));
+    }
+  }
+  h->t += (uint64_t)n;
+  return ISING_OK;
+}
+
+// Enqueue the observables reduction of every slab; slab partials of device d are added
+// (atomics) into out[d][0..1] (zeroed by the caller).
+int enqueue_observables(ising_ctx* h, const std::vector<unsigned long long*>& out) {
+  for (auto& s : h->slabs) {
+    Device& d = h->devs[s.devi];
+    CU(cudaSetDevice(d.dev));
+    ObsParams p;
+    p.black = s.plane[0];
+    p.white = s.plane[1];
+    p.W = h->W;
+    p.row0 = s.row0;
+    p.R = (int32_t)s.R;
+    p.out = out[s.devi];
+    const int64_t total = s.R * h->W;
+    const int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)d.sms * 8);
+    k_observables<<<grid, 256, 0, d.stream>>>(p);
+    CU(cudaGetLastError());
+    ++h->launch_count;
+  }
+  return ISING_OK;
+}
+
 }  // namespace
 
 // ======================================================================= C ABI
@@ -934,30 +989,7 @@ int ising_sweep(ising_t h, int64_t n) {
     CU(cudaSetDevice(d.dev));
     CU(cudaEventRecord(d.ev_t0, d.stream));
   }
-  int64_t k0 = 1;
-  if (graph_eligible(h) && n >= kGraphSweeps) {
-    if (!h->gexec) TRY(build_graph(h));
-    Device& d = h->devs[0];
-    CU(launch_set_u32(d.stream, h->t_dev, (uint32_t)h->t, 0));
-    ++h->launch_count;
-    const int64_t reps = n / kGraphSweeps;
-    for (int64_t r = 0; r < reps; ++r) {
-      CU(cudaGraphLaunch(h->gexec, d.stream));
-      h->launch_count += h->graph_launches;
-    }
-    k0 = reps * kGraphSweeps + 1;
-  }
-  for (int64_t k = k0; k <= n; ++k) {
-    const uint32_t t = (uint32_t)(h->t + (uint64_t)k);
-    for (int c = 0; c < 2; ++c) {
-      if (h->p2p && h->world > 1)
-        TRY(phase_p2p(h, c, t));
-      else if (h->rank_mode && h->world > 1)
-        TRY(phase_rank(h, c, t));
-      else
-        TRY(phase_local(h, c, t));
-    }
-  }
+  TRY(enqueue_sweeps(h, n));
   for (auto& d : h->devs) {
     CU(cudaSetDevice(d.dev));
     CU(cudaEventRecord(d.ev_t1, d.stream));
@@ -979,7 +1011,6 @@ int ising_sweep(ising_t h, int64_t n) {
     }
     h->kernel_ms = tot;
   }
-  h->t += (uint64_t)n;
   return ISING_OK;
 }
 
@@ -1022,26 +1053,13 @@ int ising_observables(ising_t h, int64_t* up_count, int64_t* bond_energy) {
   if (!h || !up_count || !bond_energy) return ISING_ERR_ARG;
   if (!h->state_set) return ISING_ERR_STATE;
   TRY(p2p_wait(h));  // the neighbours' last phase wrote this slab's white halo rows
+  std::vector<unsigned long long*> outs;
   for (auto& d : h->devs) {
     CU(cudaSetDevice(d.dev));
     CU(cudaMemsetAsync(d.red, 0, 2 * sizeof(unsigned long long), d.stream));
+    outs.push_back(d.red);
   }
-  for (auto& s : h->slabs) {
-    Device& d = h->devs[s.devi];
-    CU(cudaSetDevice(d.dev));
-    ObsParams p;
-    p.black = s.plane[0];
-    p.white = s.plane[1];
-    p.W = h->W;
-    p.row0 = s.row0;
-    p.R = (int32_t)s.R;
-    p.out = d.red;
-    const int64_t total = s.R * h->W;
-    const int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)d.sms * 8);
-    k_observables<<<grid, 256, 0, d.stream>>>(p);
-    CU(cudaGetLastError());
-    ++h->launch_count;
-  }
+  TRY(enqueue_observables(h, outs));
   if (h->p2p && h->world > 1) {
     // all-reduce of the two partials over peer memory
     Device& d = h->devs[0];
@@ -1070,6 +1088,69 @@ int ising_observables(ising_t h, int64_t* up_count, int64_t* bond_energy) {
   }
   *up_count = (int64_t)up;
   *bond_energy = 2 * (int64_t)anti - 2 * h->N * h->M;
+  return ISING_OK;
+}
+
+int ising_sweep_measure(ising_t h, int64_t n_samples, int64_t every, int64_t* up_counts,
+                        int64_t* bond_energies) {
+  if (!h || n_samples < 0 || every < 1 || (n_samples > 0 && (!up_counts || !bond_energies)))
+    return ISING_ERR_ARG;
+  if (!h->beta_set || !h->state_set) return ISING_ERR_STATE;
+  if (h->t + (uint64_t)(n_samples * every) > 0xffffffffull) return ISING_ERR_RANGE;
+  if (h->rank_mode && h->world > 1) {
+    // rank mode: the observables need the cross-rank all-reduce per sample
+    double total = 0;
+    for (int64_t k = 0; k < n_samples; ++k) {
+      TRY(ising_sweep(h, every));
+      total += h->last_ms;
+      TRY(ising_observables(h, &up_counts[k], &bond_energies[k]));
+    }
+    h->last_ms = total;
+    return ISING_OK;
+  }
+  const size_t need = (size_t)std::max<int64_t>(n_samples, 1) * 2;
+  std::vector<unsigned long long*> base;
+  for (auto& d : h->devs) {
+    CU(cudaSetDevice(d.dev));
+    if (d.meas_cap < need) {
+      if (d.meas) CU(cudaFree(d.meas));
+      d.meas = nullptr;
+      d.meas_cap = 0;
+      CU(cudaMalloc(&d.meas, need * sizeof(unsigned long long)));
+      d.meas_cap = need;
+    }
+    CU(cudaMemsetAsync(d.meas, 0, need * sizeof(unsigned long long), d.stream));
+    base.push_back(d.meas);
+    CU(cudaEventRecord(d.ev_t0, d.stream));
+  }
+  h->kernel_launches = 0;
+  std::vector<unsigned long long*> slot(base.size());
+  for (int64_t k = 0; k < n_samples; ++k) {
+    TRY(enqueue_sweeps(h, every));
+    for (size_t d = 0; d < base.size(); ++d) slot[d] = base[d] + 2 * k;
+    TRY(enqueue_observables(h, slot));
+  }
+  for (auto& d : h->devs) {
+    CU(cudaSetDevice(d.dev));
+    CU(cudaEventRecord(d.ev_t1, d.stream));
+  }
+  TRY(sync_all(h));
+  double mx = 0;
+  std::vector<unsigned long long> host(need);
+  for (int64_t k = 0; k < n_samples; ++k) up_counts[k] = bond_energies[k] = 0;
+  for (auto& d : h->devs) {
+    CU(cudaSetDevice(d.dev));
+    float ms = 0;
+    CU(cudaEventElapsedTime(&ms, d.ev_t0, d.ev_t1));
+    mx = std::max(mx, (double)ms);
+    CU(cudaMemcpy(host.data(), d.meas, need * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    for (int64_t k = 0; k < n_samples; ++k) {
+      up_counts[k] += (int64_t)host[2 * k];
+      bond_energies[k] += (int64_t)host[2 * k + 1];  // antiparallel bonds for now
+    }
+  }
+  for (int64_t k = 0; k < n_samples; ++k) bond_energies[k] = 2 * bond_energies[k] - 2 * h->N * h->M;
+  h->last_ms = mx;
   return ISING_OK;
 }
 

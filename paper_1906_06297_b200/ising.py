@@ -49,6 +49,7 @@ SIGNATURES = {
     "ising_sweep": (_INT, [_VP, _I64]),
     "ising_read_lattice": (_INT, [_VP, _VP, _I64]),
     "ising_observables": (_INT, [_VP, _I64P, _I64P]),
+    "ising_sweep_measure": (_INT, [_VP, _I64, _I64, _I64P, _I64P]),
     "ising_last_sweep_ms": (_INT, [_VP, _DBLP]),
     "ising_set_profiling": (_INT, [_VP, _INT]),
     "ising_kernel_stats": (_INT, [_VP, _DBLP, _I64P]),
@@ -203,6 +204,15 @@ def ising_observables(h: int) -> tuple[int, int]:
     return up.value, E.value
 
 
+def ising_sweep_measure(h: int, n_samples: int, every: int) -> tuple[np.ndarray, np.ndarray]:
+    ups = np.zeros(int(n_samples), dtype=np.int64)
+    Es = np.zeros(int(n_samples), dtype=np.int64)
+    _check(load().ising_sweep_measure(h, int(n_samples), int(every),
+                                      ups.ctypes.data_as(_I64P), Es.ctypes.data_as(_I64P)),
+           "ising_sweep_measure")
+    return ups, Es
+
+
 def ising_last_sweep_ms(h: int) -> float:
     v = _DBL()
     _check(load().ising_last_sweep_ms(h, ctypes.byref(v)), "ising_last_sweep_ms")
@@ -331,6 +341,10 @@ class IsingLattice:
     def sweep(self, n: int = 1):
         ising_sweep(self.h, n)
         return self
+
+    def measure(self, n_samples: int, every: int = 1) -> tuple[np.ndarray, np.ndarray]:
+        """(up_count, bond_energy) after every `every` sweeps, n_samples times."""
+        return ising_sweep_measure(self.h, n_samples, every)
 
     def read_lattice(self, out=None) -> np.ndarray:
         if out is None:

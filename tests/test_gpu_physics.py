@@ -14,13 +14,9 @@ def measure_abs_m(L, T, start, seed, sweeps, discard, every):
     g = IsingLattice(L, L, seed).set_beta(1.0 / T)
     g.init_cold() if start == "cold" else g.init_random()
     g.sweep(discard)
-    ms = []
-    for _ in range((sweeps - discard) // every):
-        g.sweep(every)
-        up, _ = g.observables()
-        ms.append((2 * up - L * L) / (L * L))
+    ups, _ = g.measure((sweeps - discard) // every, every)  # device-side series
     g.close()
-    return np.asarray(ms)
+    return (2 * ups - L * L) / (L * L)
 
 
 @pytest.mark.parametrize("T,start,expect", [(1.5, "cold", exact.onsager_m(1.5)), (3.0, "random", 0.0)])
@@ -39,13 +35,9 @@ def test_c2_onsager(T, start, expect, seed):
 def binder_point(L, T, seed, sweeps, every=1):
     g = IsingLattice(L, L, seed).set_beta(1.0 / T).init_cold()
     g.sweep(2000)
-    m = []
-    for _ in range(sweeps // every):
-        g.sweep(every)
-        up, _ = g.observables()
-        m.append((2 * up - L * L) / (L * L))
+    ups, _ = g.measure(sweeps // every, every)
     g.close()
-    m = np.asarray(m)
+    m = (2 * ups - L * L) / (L * L)
     return exact.binder(np.mean(m**2), np.mean(m**4))
 
 
@@ -58,3 +50,16 @@ def test_binder_crossing_on_gpu():
     u128 = [binder_point(128, T, 12, 200_000, 10) for T in (lo, hi)]
     assert u128[0] > u64[0], (u64, u128)
     assert u128[1] < u64[1], (u64, u128)
+
+
+def test_measured_chain_matches_oracle_series():
+    # ising_sweep_measure's device-side series equals the oracle chain sample by sample
+    import oracle
+
+    for N, M, every, slabs in [(64, 64, 1, None), (128, 192, 7, None), (96, 128, 3, [0, 0, 0])]:
+        g = IsingLattice(N, M, 4, devices=slabs).set_beta(0.4406868).init_random()
+        o = oracle.Lattice(N, M, 4).set_beta(0.4406868).init_random()
+        ups, Es = g.measure(40, every)
+        ou, oE = o.chain(40 * every)
+        assert np.array_equal(ups, ou[every - 1::every]) and np.array_equal(Es, oE[every - 1::every])
+        assert g.t == o.t == 40 * every
