@@ -248,8 +248,14 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    basic = args.layout == "basic"
+    if basic and n > 1:
+        raise SystemExit("--layout basic is single-GPU (PAPER.md §3.1 basic implementation)")
+    bytes_per_flip = 3.0 if basic else BYTES_PER_FLIP
     if n > 1:
         lat = IsingLattice.distributed(N, M, SEED, device=dev)
+    elif basic:
+        lat = IsingLattice.basic(N, M, SEED, device=dev)
     else:
         lat = IsingLattice(N, M, SEED, n_gpus=1)
     row0, rows = lat.slab_info()
@@ -296,7 +302,7 @@ def run_ours(args):
     flips_per_launch = rows * M * kprof_sweeps / max(klaunches, 1)
     avg_launch_ms = kms / max(klaunches, 1)
     peaks, peak_src = measured_peaks()
-    hbm_gbs = BYTES_PER_FLIP * flips_per_launch / (avg_launch_ms * 1e6)
+    hbm_gbs = bytes_per_flip * flips_per_launch / (avg_launch_ms * 1e6)
 
     # ---- ALU roofline: the Philox multiplier.  Every attempted flip needs
     # one draw = 1/4 Philox4x32-10 block = 4 per-thread 32x32->64 multiplies (16 of the 20
@@ -307,7 +313,10 @@ def run_ours(args):
     alu_peak = sms * 32 * clk_mhz * 1e6 / MULWIDE_PER_FLIP / 1e9  # flips/ns
     philox_probe = ising_probe_philox(dev)  # Philox-only draws/ns, same device function
     flips_per_ns_kernel = flips_per_launch / (avg_launch_ms * 1e6)
-    traffic = ncu_traffic(args.config, n)
+    traffic = ncu_traffic(args.config + ("_basic" if basic else ""), n)
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    hbm_roof_flips = hbm_peak / bytes_per_flip  # flips/ns
+    alu_bound = alu_peak <= hbm_roof_flips
 
     # ---- end to end through the C ABI with host buffers ----
     # Each rank owns its rows: the input is this rank's slab (rows x M int8, pinned host
@@ -367,17 +376,20 @@ def run_ours(args):
                 "seed": SEED,
                 "start": "random",
                 "parallelism": f"slab{n}",
+                "layout": "basic byte/spin (PAPER.md §3.1)" if basic else "multi-spin 4 bit/spin (PAPER.md §3.3)",
                 "l2": f"inputs larger than L2: packed planes {N * M // 2 / 2**20:.0f} MiB per "
                       f"{'GPU' if n == 1 else 'lattice'} vs 126 MB L2; no flush",
             },
             "roofline": {
-                "bound": "alu",
-                "achieved": flips_per_ns_kernel,
-                "peak": alu_peak,
-                "unit": "flips/ns",
-                "frac": flips_per_ns_kernel / alu_peak,
+                "bound": "alu" if alu_bound else "hbm",
+                "achieved": flips_per_ns_kernel if alu_bound else hbm_gbs,
+                "peak": alu_peak if alu_bound else hbm_peak,
+                "unit": "flips/ns" if alu_bound else "GB/s",
+                "frac": flips_per_ns_kernel / alu_peak if alu_bound else hbm_gbs / hbm_peak,
                 "traffic": traffic,
-                "kernel": "k_halfsweep<0>",
+                "kernel": "k_basic_halfsweep<0>" if basic else "k_halfsweep<0>",
+                "alu_roof_flips_per_ns": alu_peak,
+                "hbm_roof_flips_per_ns": hbm_roof_flips,
                 "avg_launch_ms": avg_launch_ms,
                 "launches": klaunches,
                 "kernel_share_of_step": kms / max(sweep_ms_prof, 1e-9),
@@ -390,7 +402,7 @@ def run_ours(args):
                                   "dram__bytes_write.sum per launch, ncu --set full)",
                 "hbm": {"achieved_gbs": hbm_gbs, "peak_gbs": peaks.get("hbm_gbs"),
                         "frac": hbm_gbs / peaks.get("hbm_gbs", 6650.0), "peak_source": peak_src,
-                        "bytes_per_flip": BYTES_PER_FLIP},
+                        "bytes_per_flip": bytes_per_flip},
             },
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -413,6 +425,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="c3", choices=["c2", "c3", "c4", "c5"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--layout", default="multispin", choices=["multispin", "basic"])
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")

@@ -97,6 +97,13 @@ int ising_create_rank_p2p(ising_t* out, int64_t L_rows, int64_t L_cols, uint64_t
 int ising_ipc_handle(ising_t h, void* blob, size_t len);            /* len >= 256 */
 int ising_ipc_connect(ising_t h, const void* blobs, size_t len);    /* world * 256 bytes */
 
+/* The paper's basic layout (§3.1, Fig. 2 listing) on one
+ * device: one signed byte per spin in two colour planes, one Philox block per four sites,
+ * same draw contract and thresholds (bit-identical results), 3 algorithmic bytes per
+ * attempted flip instead of 1.5.  L_rows even, L_cols % 8 == 0.  Every other call works
+ * on the handle as on a one-slab multi-spin handle. */
+int ising_create_basic(ising_t* out, int64_t L_rows, int64_t L_cols, uint64_t seed, int device);
+
 /* Writes an NCCL unique id (id_len >= 128 bytes) into id. */
 int ising_nccl_unique_id(void* id, size_t id_len);
 

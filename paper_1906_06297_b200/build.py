@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libising.so")
-SOURCES = ["ising_kernels.cu", "ising_runtime.cu"]
+SOURCES = ["ising_kernels.cu", "ising_basic.cu", "ising_runtime.cu"]
 HEADERS = ["ising_kernels.cuh", os.path.join("..", "..", "include", "ising.h")]
 
 

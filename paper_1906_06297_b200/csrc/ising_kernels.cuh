@@ -127,6 +127,26 @@ struct UnpackParams {
   int32_t rb;
 };
 
+// The basic byte-per-spin layout (ising_basic.cu, §3.1).
+struct BasicParams {
+  int8_t* lattice;           // target colour plane, nx x ny
+  const int8_t* op_lattice;  // the other colour
+  int64_t nx, ny;
+  uint32_t t, colour;
+  uint32_t thr[5];
+  uint32_t always_mask;
+  PhiloxKeys keys;
+};
+cudaError_t launch_basic_halfsweep(int rule, int grid, cudaStream_t st, const BasicParams& p);
+cudaError_t launch_basic_init(int grid, cudaStream_t st, int8_t* black, int8_t* white, int64_t nx,
+                              int64_t ny, int cold, const PhiloxKeys& keys);
+cudaError_t launch_basic_observables(int grid, cudaStream_t st, const int8_t* black,
+                                     const int8_t* white, int64_t nx, int64_t ny,
+                                     unsigned long long* out);
+cudaError_t launch_basic_convert(int grid, cudaStream_t st, int8_t* black, int8_t* white,
+                                 int8_t* full, int64_t ny, int64_t r0, int64_t rows, int to_full,
+                                 unsigned int* bad);
+
 // Host-side launchers (defined in ising_kernels.cu).
 cudaError_t launch_sync(cudaStream_t st, const SyncParams& p);
 cudaError_t launch_set_u32(cudaStream_t st, uint32_t* dst, uint32_t v, int add);

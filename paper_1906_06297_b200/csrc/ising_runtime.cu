@@ -152,6 +152,9 @@ struct ising_ctx {
   uint32_t* t_dev = nullptr;               // device-resident sweep base read by the kernels
   int64_t graph_launches = 0;              // kernel nodes per graph replay
   bool graphs_enabled = true;
+  // basic byte-per-spin layout (ising_create_basic; §3.1)
+  bool basic = false;
+  int8_t* bplane[2] = {nullptr, nullptr};
 };
 
 namespace {
@@ -283,6 +286,8 @@ void destroy_ctx(ising_ctx* h) {
   }
   for (cudaEvent_t e : h->prof_events) cudaEventDestroy(e);
   if (h->gexec) cudaGraphExecDestroy(h->gexec);
+  for (int c = 0; c < 2; ++c)
+    if (h->bplane[c]) cudaFree(h->bplane[c]);
   if (h->t_dev) cudaFree(h->t_dev);
   delete h;
 }
@@ -693,6 +698,101 @@ int enqueue_observables(ising_ctx* h, const std::vector<unsigned long long*>& ou
   return ISING_OK;
 }
 
+// ------------------------------------------------------------- basic layout
+int basic_grid(const Device& d, int64_t work) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, (int64_t)d.sms * 32));
+}
+
+int basic_init(ising_ctx* h, int cold) {
+  Device& d = h->devs[0];
+  CU(cudaSetDevice(d.dev));
+  const int64_t ny = h->M / 2;
+  CU(launch_basic_init(basic_grid(d, 2 * h->N * (ny / 4)), d.stream, h->bplane[0], h->bplane[1],
+                       h->N, ny, cold, h->keys));
+  ++h->launch_count;
+  CU(cudaStreamSynchronize(d.stream));
+  h->t = 0;
+  h->state_set = true;
+  return ISING_OK;
+}
+
+int basic_enqueue_sweeps(ising_ctx* h, int64_t n) {
+  Device& d = h->devs[0];
+  const int64_t ny = h->M / 2;
+  const int grid = basic_grid(d, h->N * (ny / 4));
+  const int rule = h->rule == ISING_RULE_METROPOLIS ? 0 : 1;
+  for (int64_t k = 1; k <= n; ++k) {
+    for (int c = 0; c < 2; ++c) {
+      BasicParams p{};
+      p.lattice = h->bplane[c];
+      p.op_lattice = h->bplane[1 - c];
+      p.nx = h->N;
+      p.ny = ny;
+      p.t = (uint32_t)(h->t + (uint64_t)k);
+      p.colour = (uint32_t)c;
+      for (int a = 0; a < 5; ++a) p.thr[a] = h->acc.thr[a];
+      p.always_mask = h->acc.always_mask;
+      p.keys = h->keys;
+      const bool prof = h->profiling;
+      if (prof) CU(cudaEventRecord(h->prof_events[2 * h->kernel_launches], d.stream));
+      CU(launch_basic_halfsweep(rule, grid, d.stream, p));
+      if (prof) {
+        CU(cudaEventRecord(h->prof_events[2 * h->kernel_launches + 1], d.stream));
+        ++h->kernel_launches;
+      }
+      ++h->launch_count;
+    }
+  }
+  h->t += (uint64_t)n;
+  return ISING_OK;
+}
+
+int basic_convert(ising_ctx* h, int8_t* host, bool to_host) {
+  Device& d = h->devs[0];
+  CU(cudaSetDevice(d.dev));
+  TRY(ensure_staging(d));
+  const int64_t ny = h->M / 2;
+  CU(cudaMemsetAsync(d.red, 0, 4 * sizeof(unsigned long long), d.stream));
+  const int64_t rows_per_chunk = std::max<int64_t>(1, (int64_t)kStagingBytes / h->M);
+  for (int64_t r0 = 0; r0 < h->N; r0 += rows_per_chunk) {
+    const int64_t rows = std::min<int64_t>(rows_per_chunk, h->N - r0);
+    const size_t bytes = (size_t)(rows * h->M);
+    if (!to_host)
+      CU(cudaMemcpyAsync(d.staging, host + r0 * h->M, bytes, cudaMemcpyHostToDevice, d.stream));
+    CU(launch_basic_convert(basic_grid(d, rows * h->M), d.stream, h->bplane[0], h->bplane[1],
+                            d.staging, ny, r0, rows, to_host ? 1 : 0,
+                            reinterpret_cast<unsigned int*>(d.red + 2)));
+    ++h->launch_count;
+    if (to_host)
+      CU(cudaMemcpyAsync(host + r0 * h->M, d.staging, bytes, cudaMemcpyDeviceToHost, d.stream));
+  }
+  CU(cudaStreamSynchronize(d.stream));
+  if (!to_host) {
+    unsigned long long bad = 0;
+    CU(cudaMemcpy(&bad, d.red + 2, sizeof bad, cudaMemcpyDeviceToHost));
+    if (bad & 0xffffffffull) {
+      g_last_error = "ising_write_lattice: values must be -1 or +1";
+      return ISING_ERR_ARG;
+    }
+  }
+  return ISING_OK;
+}
+
+int basic_observables(ising_ctx* h, int64_t* up, int64_t* E) {
+  Device& d = h->devs[0];
+  CU(cudaSetDevice(d.dev));
+  CU(cudaMemsetAsync(d.red, 0, 2 * sizeof(unsigned long long), d.stream));
+  CU(launch_basic_observables(basic_grid(d, h->N * h->M / 2), d.stream, h->bplane[0],
+                              h->bplane[1], h->N, h->M / 2, d.red));
+  ++h->launch_count;
+  unsigned long long v[2];
+  CU(cudaMemcpyAsync(v, d.red, sizeof v, cudaMemcpyDeviceToHost, d.stream));
+  CU(cudaStreamSynchronize(d.stream));
+  *up = (int64_t)v[0];
+  *E = 2 * (int64_t)v[1] - 2 * h->N * h->M;
+  return ISING_OK;
+}
+
 }  // namespace
 
 // ======================================================================= C ABI
@@ -814,6 +914,39 @@ int ising_create_rank_p2p(ising_t* out, int64_t L_rows, int64_t L_cols, uint64_t
   return ISING_OK;
 }
 
+int ising_create_basic(ising_t* out, int64_t L_rows, int64_t L_cols, uint64_t seed, int device) {
+  if (!out) return ISING_ERR_ARG;
+  *out = nullptr;
+  if (L_rows < 2 || (L_rows & 1) || L_cols < 8 || (L_cols % 8) != 0 || L_rows > (int64_t(1) << 32)) {
+    g_last_error = "basic layout: need L_rows even >= 2 and L_cols % 8 == 0";
+    return ISING_ERR_ARG;
+  }
+  ising_ctx* h = new (std::nothrow) ising_ctx;
+  if (!h) return ISING_ERR_OOM;
+  h->N = L_rows;
+  h->M = L_cols;
+  h->W = 0;
+  h->seed = seed;
+  h->basic = true;
+  make_keys(seed, &h->keys);
+  h->devs.emplace_back();
+  int st = setup_device(h->devs[0], device);
+  if (st == ISING_OK) {
+    const size_t bytes = (size_t)(L_rows * (L_cols / 2));
+    for (int c = 0; c < 2 && st == ISING_OK; ++c) {
+      cudaError_t e = cudaMalloc(&h->bplane[c], bytes);
+      if (e == cudaSuccess) e = cudaMemset(h->bplane[c], 1, bytes);
+      if (e != cudaSuccess) st = fail_cuda(e, "basic planes", __LINE__);
+    }
+  }
+  if (st != ISING_OK) {
+    destroy_ctx(h);
+    return st;
+  }
+  *out = h;
+  return ISING_OK;
+}
+
 int ising_ipc_handle(ising_t h, void* blob, size_t len) {
   if (!h || !blob || len < ISING_IPC_BLOB_BYTES || !h->p2p) return ISING_ERR_ARG;
   IpcBlob b{};
@@ -907,14 +1040,27 @@ int ising_set_beta(ising_t h, double beta) {
   return ISING_OK;
 }
 
-int ising_init_random(ising_t h) { return h ? run_init(h, 0) : ISING_ERR_ARG; }
-int ising_init_cold(ising_t h) { return h ? run_init(h, 1) : ISING_ERR_ARG; }
+int ising_init_random(ising_t h) {
+  if (!h) return ISING_ERR_ARG;
+  return h->basic ? basic_init(h, 0) : run_init(h, 0);
+}
+int ising_init_cold(ising_t h) {
+  if (!h) return ISING_ERR_ARG;
+  return h->basic ? basic_init(h, 1) : run_init(h, 1);
+}
 
 int ising_write_lattice(ising_t h, const int8_t* in, int64_t in_len, uint64_t t) {
   if (!h || !in) return ISING_ERR_ARG;
   if (t > 0xffffffffull) return ISING_ERR_RANGE;
   // Rank mode takes either the full lattice (its rows and halo rows are packed straight
   // from it) or exactly its own R x M rows (then the halo rows are exchanged on device).
+  if (h->basic) {
+    if (in_len < h->N * h->M) return ISING_ERR_RANGE;
+    TRY(basic_convert(h, const_cast<int8_t*>(in), false));
+    h->t = t;
+    h->state_set = true;
+    return ISING_OK;
+  }
   const bool slab_only = h->rank_mode && h->world > 1 && in_len == h->slabs[0].R * h->M;
   if (!slab_only && in_len < h->N * h->M) return ISING_ERR_RANGE;
   if (h->p2p && h->world > 1 && !h->connected) return ISING_ERR_STATE;
@@ -989,7 +1135,7 @@ int ising_sweep(ising_t h, int64_t n) {
     CU(cudaSetDevice(d.dev));
     CU(cudaEventRecord(d.ev_t0, d.stream));
   }
-  TRY(enqueue_sweeps(h, n));
+  TRY(h->basic ? basic_enqueue_sweeps(h, n) : enqueue_sweeps(h, n));
   for (auto& d : h->devs) {
     CU(cudaSetDevice(d.dev));
     CU(cudaEventRecord(d.ev_t1, d.stream));
@@ -1020,6 +1166,7 @@ int ising_read_lattice(ising_t h, int8_t* out, int64_t out_len) {
   const bool slab_only = h->rank_mode && h->world > 1 && out_len == h->slabs[0].R * h->M;
   if (!slab_only && out_len < h->N * h->M) return ISING_ERR_RANGE;
   if (!h->state_set) return ISING_ERR_STATE;
+  if (h->basic) return basic_convert(h, out, true);
   for (auto& s : h->slabs) {
     Device& d = h->devs[s.devi];
     CU(cudaSetDevice(d.dev));
@@ -1052,6 +1199,7 @@ int ising_read_lattice(ising_t h, int8_t* out, int64_t out_len) {
 int ising_observables(ising_t h, int64_t* up_count, int64_t* bond_energy) {
   if (!h || !up_count || !bond_energy) return ISING_ERR_ARG;
   if (!h->state_set) return ISING_ERR_STATE;
+  if (h->basic) return basic_observables(h, up_count, bond_energy);
   TRY(p2p_wait(h));  // the neighbours' last phase wrote this slab's white halo rows
   std::vector<unsigned long long*> outs;
   for (auto& d : h->devs) {
@@ -1097,7 +1245,7 @@ int ising_sweep_measure(ising_t h, int64_t n_samples, int64_t every, int64_t* up
     return ISING_ERR_ARG;
   if (!h->beta_set || !h->state_set) return ISING_ERR_STATE;
   if (h->t + (uint64_t)(n_samples * every) > 0xffffffffull) return ISING_ERR_RANGE;
-  if (h->rank_mode && h->world > 1) {
+  if ((h->rank_mode && h->world > 1) || h->basic) {
     // rank mode: the observables need the cross-rank all-reduce per sample
     double total = 0;
     for (int64_t k = 0; k < n_samples; ++k) {

@@ -38,6 +38,7 @@ SIGNATURES = {
     "ising_create_rank": (_INT, [ctypes.POINTER(_VP), _I64, _I64, _U64, _INT, _INT, _INT, _VP, _SZ]),
     "ising_nccl_unique_id": (_INT, [_VP, _SZ]),
     "ising_create_rank_p2p": (_INT, [ctypes.POINTER(_VP), _I64, _I64, _U64, _INT, _INT, _INT]),
+    "ising_create_basic": (_INT, [ctypes.POINTER(_VP), _I64, _I64, _U64, _INT]),
     "ising_ipc_handle": (_INT, [_VP, _VP, _SZ]),
     "ising_ipc_connect": (_INT, [_VP, _VP, _SZ]),
     "ising_destroy": (_INT, [_VP]),
@@ -150,6 +151,13 @@ def ising_create_rank_p2p(L_rows: int, L_cols: int, seed: int, rank: int, world:
     h = _VP()
     _check(load().ising_create_rank_p2p(ctypes.byref(h), L_rows, L_cols, seed, rank, world, device),
            "ising_create_rank_p2p")
+    return h.value
+
+
+def ising_create_basic(L_rows: int, L_cols: int, seed: int, device: int = 0) -> int:
+    h = _VP()
+    _check(load().ising_create_basic(ctypes.byref(h), L_rows, L_cols, seed, device),
+           "ising_create_basic")
     return h.value
 
 
@@ -272,6 +280,11 @@ class IsingLattice:
             self.h = ising_create_slabs(self.N, self.M, self.seed, list(devices))
         else:
             self.h = ising_create(self.N, self.M, self.seed, n_gpus)
+
+    @classmethod
+    def basic(cls, L_rows: int, L_cols: int, seed: int = 1, device: int = 0):
+        """The paper's basic byte-per-spin layout (§3.1) on one device."""
+        return cls(L_rows, L_cols, seed, _handle=ising_create_basic(L_rows, L_cols, seed, device))
 
     @classmethod
     def distributed(cls, L_rows: int, L_cols: int, seed: int = 1, device: int | None = None,

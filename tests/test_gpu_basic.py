@@ -1,0 +1,50 @@
+"""The basic byte-per-spin layout (§3.1) against the oracle and
+against the multi-spin layout: bit-identical lattices and equal integer observables."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_1906_06297_b200 import ising
+from paper_1906_06297_b200.ising import IsingLattice
+from tests import cases
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("N,M", [(64, 64), (66, 64), (130, 192), (2, 8), (8, 24), (256, 512)])
+@pytest.mark.parametrize("beta,rule", [(0.4406868, 0), (0.2, 0), (0.0, 0), (math.inf, 0),
+                                       (0.4406868, 1), (math.inf, 1)])
+def test_basic_matches_oracle(N, M, beta, rule):
+    g = IsingLattice.basic(N, M, 3).set_beta(beta, rule).init_random()
+    o = oracle.Lattice(N, M, 3).set_beta(beta, rule).init_random()
+    for n in [1, 2, 9]:
+        g.sweep(n)
+        o.sweep(n)
+        assert np.array_equal(g.read_lattice(), o.full()), (N, M, beta, rule, o.t)
+        assert g.observables() == o.observables()
+
+
+def test_basic_equals_multispin():
+    N, M = 128, 256
+    a = IsingLattice.basic(N, M, 11).set_beta(0.4406868).init_random()
+    b = IsingLattice(N, M, 11).set_beta(0.4406868).init_random()
+    a.sweep(100)
+    b.sweep(100)
+    assert np.array_equal(a.read_lattice(), b.read_lattice())
+    assert a.observables() == b.observables()
+
+
+def test_basic_write_resume_and_measure():
+    rng = np.random.default_rng(5)
+    N, M = 64, 128
+    full = cases.random_pm1(rng, N, M)
+    g = IsingLattice.basic(N, M, 2).write_lattice(full, t=9).set_beta(0.3)
+    assert np.array_equal(g.read_lattice(), full)
+    ups, Es = g.measure(20, 2)
+    o = oracle.Lattice(N, M, 2).load_full(full, t=9).set_beta(0.3)
+    ou, oE = o.chain(40)
+    assert np.array_equal(ups, ou[1::2]) and np.array_equal(Es, oE[1::2])
+    with pytest.raises(ising.IsingError):
+        IsingLattice.basic(64, 60, 1)
