@@ -286,10 +286,17 @@ __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned l
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// Spin until every flag >= v.  A peer that never arrives (crashed rank) must not hang the
+// GPU: after ~2^36 SM cycles (tens of seconds) the kernel traps, so the host call returns
+// a CUDA error instead.
 __device__ __forceinline__ void spin_until(const unsigned long long* flags, int n,
                                            unsigned long long v) {
+  const long long t0 = clock64();
   for (int k = 0; k < n; ++k)
-    while (ld_acquire_sys(flags + k) < v) __nanosleep(64);
+    while (ld_acquire_sys(flags + k) < v) {
+      __nanosleep(64);
+      if (clock64() - t0 > (1ll << 36)) __trap();
+    }
 }
 
 template <int RULE>

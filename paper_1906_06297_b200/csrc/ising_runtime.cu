@@ -262,8 +262,17 @@ int ensure_staging(Device& d) {
   return ISING_OK;
 }
 
+int p2p_wait(ising_ctx* h);
+
 void destroy_ctx(ising_ctx* h) {
   if (!h) return;
+  if (h->p2p && h->connected && h->world > 1 && !h->devs.empty()) {
+    // the neighbours may still be storing into this slab's halo rows (their last phase):
+    // wait for them before the memory goes away (best effort: errors are ignored here)
+    cudaSetDevice(h->devs[0].dev);
+    if (p2p_wait(h) == ISING_OK) cudaStreamSynchronize(h->devs[0].stream);
+    cudaGetLastError();
+  }
   for (auto& s : h->slabs) {
     if (s.devi < (int)h->devs.size()) cudaSetDevice(h->devs[s.devi].dev);
     for (int c = 0; c < 2; ++c)
