@@ -273,6 +273,10 @@ __device__ __forceinline__ uint64_t update_word<1>(uint64_t tgt, uint64_t n, uin
 // column q); the thread walks down the band keeping the N/C/S source chunks in
 // registers, so each source word is read from memory once per band (plus one halo
 // row per band).  Grid-stride over items; the grid is a multiple of the SM count.
+#ifndef ISING_VPT
+#define ISING_VPT 1  // 128-bit vectors (2 words, 32 spins) per thread and row
+#endif
+constexpr int kWords = 2 * ISING_VPT;
 #ifndef ISING_MINB
 #define ISING_MINB 4  // 116 registers, 4 blocks/SM: measured best of 1..8 (r01)
 #endif
@@ -308,7 +312,7 @@ __global__ void __launch_bounds__(128, ISING_MINB) k_halfsweep(const HalfSweepPa
   // sweep index: absolute, or (CUDA graph replays) a device-resident base + the offset
   const uint32_t t = p.t_dev ? *p.t_dev + p.t : p.t;
   const int64_t W = p.W;
-  const int64_t chunks = W >> 1;
+  const int64_t chunks = W / kWords;
   const uint64_t* src = p.src + W;  // local row r (r = -1 .. R) at src + r * W
   uint64_t* tgt = p.tgt + W;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -318,35 +322,60 @@ __global__ void __launch_bounds__(128, ISING_MINB) k_halfsweep(const HalfSweepPa
     const int band = (int)(item / chunks);
     const int ra = p.r_begin + band * p.H;
     const int rb = min(ra + p.H, p.r_end);
-    const int64_t wc = 2 * q;
+    const int64_t wc = kWords * q;
     const int64_t wwest = (wc == 0) ? W - 1 : wc - 1;     // periodic wrap
-    const int64_t weast = (wc + 2 == W) ? 0 : wc + 2;
-    ulonglong2 nv = ld_nc_v2(src + (int64_t)(ra - 1) * W + wc);
-    ulonglong2 cv = ld_nc_v2(src + (int64_t)ra * W + wc);
+    const int64_t weast = (wc + kWords == W) ? 0 : wc + kWords;
+    uint64_t nv[kWords], cv[kWords];
+#pragma unroll
+    for (int v = 0; v < kWords / 2; ++v) {
+      const ulonglong2 a = ld_nc_v2(src + (int64_t)(ra - 1) * W + wc + 2 * v);
+      const ulonglong2 b = ld_nc_v2(src + (int64_t)ra * W + wc + 2 * v);
+      nv[2 * v] = a.x;
+      nv[2 * v + 1] = a.y;
+      cv[2 * v] = b.x;
+      cv[2 * v + 1] = b.y;
+    }
     for (int r = ra; r < rb; ++r) {
-      const ulonglong2 sv = ld_nc_v2(src + (int64_t)(r + 1) * W + wc);
+      uint64_t sv[kWords], tv[kWords];
+#pragma unroll
+      for (int v = 0; v < kWords / 2; ++v) {
+        const ulonglong2 a = ld_nc_v2(src + (int64_t)(r + 1) * W + wc + 2 * v);
+        const ulonglong2 b = *reinterpret_cast<const ulonglong2*>(tgt + (int64_t)r * W + wc + 2 * v);
+        sv[2 * v] = a.x;
+        sv[2 * v + 1] = a.y;
+        tv[2 * v] = b.x;
+        tv[2 * v + 1] = b.y;
+      }
       const int64_t gi = p.row0 + r;
       // side word: the left word if (black and i even) or (white and i odd), else the
       // right one (Fig. 3 caption PAPER.md:208; reading R2)
       const bool west = ((gi & 1) == 0) == (p.colour == 0);
       const uint64_t sw = ld_nc(src + (int64_t)r * W + (west ? wwest : weast));
-      ulonglong2 tv = *reinterpret_cast<const ulonglong2*>(tgt + (int64_t)r * W + wc);
-      uint64_t side0, side1;
-      if (west) {
-        side0 = (cv.x << 4) | (sw >> 60);
-        side1 = (cv.y << 4) | (cv.x >> 60);
-      } else {
-        side0 = (cv.x >> 4) | (cv.y << 60);
-        side1 = (cv.y >> 4) | (sw << 60);
+      uint64_t side[kWords];
+#pragma unroll
+      for (int k = 0; k < kWords; ++k) {
+        if (west)
+          side[k] = (cv[k] << 4) | ((k == 0 ? sw : cv[k - 1]) >> 60);
+        else
+          side[k] = (cv[k] >> 4) | ((k == kWords - 1 ? sw : cv[k + 1]) << 60);
       }
-      const uint32_t ctr0 = (uint32_t)(4 * wc);  // Philox counter word 0 = j / 4 (reading R6)
-      tv.x = update_word<RULE>(tv.x, nv.x, cv.x, sv.x, side0, ctr0, (uint32_t)gi, t, p);
-      tv.y = update_word<RULE>(tv.y, nv.y, cv.y, sv.y, side1, ctr0 + 4, (uint32_t)gi, t, p);
-      *reinterpret_cast<ulonglong2*>(tgt + (int64_t)r * W + wc) = tv;
-      if (r == 0 && p.halo_up) *reinterpret_cast<ulonglong2*>(p.halo_up + wc) = tv;
-      if (r == p.R - 1 && p.halo_dn) *reinterpret_cast<ulonglong2*>(p.halo_dn + wc) = tv;
-      nv = cv;
-      cv = sv;
+#pragma unroll
+      for (int k = 0; k < kWords; ++k) {
+        const uint32_t ctr0 = (uint32_t)(4 * (wc + k));  // Philox counter word 1 = j / 4 (R6)
+        tv[k] = update_word<RULE>(tv[k], nv[k], cv[k], sv[k], side[k], ctr0, (uint32_t)gi, t, p);
+      }
+#pragma unroll
+      for (int v = 0; v < kWords / 2; ++v) {
+        const ulonglong2 o = make_ulonglong2(tv[2 * v], tv[2 * v + 1]);
+        *reinterpret_cast<ulonglong2*>(tgt + (int64_t)r * W + wc + 2 * v) = o;
+        if (r == 0 && p.halo_up) *reinterpret_cast<ulonglong2*>(p.halo_up + wc + 2 * v) = o;
+        if (r == p.R - 1 && p.halo_dn) *reinterpret_cast<ulonglong2*>(p.halo_dn + wc + 2 * v) = o;
+      }
+#pragma unroll
+      for (int k = 0; k < kWords; ++k) {
+        nv[k] = cv[k];
+        cv[k] = sv[k];
+      }
     }
   }
   if (p.signal_up) {  // rank-p2p: the last block publishes "phase done" to both neighbours

@@ -77,6 +77,10 @@ int fail_nccl(ncclResult_t r, const char* what, int line) {
   } while (0)
 
 constexpr size_t kStagingBytes = size_t(64) << 20;  // pack/unpack staging chunk
+#ifndef ISING_VPT
+#define ISING_VPT 1
+#endif
+constexpr int64_t kWordsPerItem = 2 * ISING_VPT;  // must match the kernel's kWords
 constexpr size_t kSyncBytes = 4096;                  // rank-p2p flags + gather area
 constexpr uint32_t kIpcMagic = 0x49534e47u;           // "ISNG"
 
@@ -201,7 +205,8 @@ void make_keys(uint64_t seed, PhiloxKeys* K) {
 }
 
 int check_shape(int64_t N, int64_t M, int n_slabs) {
-  if (N < 2 || (N & 1) || M < 64 || (M % 64) != 0 || n_slabs < 1 || N % n_slabs != 0 ||
+  if (N < 2 || (N & 1) || M < 64 || (M % 64) != 0 || ((M / 32) % kWordsPerItem) != 0 ||
+      n_slabs < 1 || N % n_slabs != 0 ||
       N / n_slabs < 2 || N > (int64_t(1) << 32) || M > (int64_t(1) << 36)) {
     g_last_error = "shape: need L_rows even, L_rows % n == 0, L_rows/n >= 2, L_cols % 64 == 0";
     return ISING_ERR_ARG;
@@ -305,7 +310,7 @@ void destroy_ctx(ising_ctx* h) {
 // thread, blocks of 128; H chosen so the grid is >= ~4 waves of resident blocks.
 void halfsweep_geometry(const ising_ctx* h, const Device& d, int64_t rows, int* H,
                         int64_t* items, int* grid) {
-  const int64_t chunks = h->W / 2;
+  const int64_t chunks = h->W / kWordsPerItem;
   int hh = h->rows_per_item_override;
   if (hh <= 0) {
     const int64_t resident = (int64_t)d.sms * d.hs_blocks_per_sm * 128;
