@@ -351,6 +351,31 @@ def run_ours(args):
         }
         del slab, out
 
+    # ---- GPU-count invariance (reading R19): a small lattice split over the n ranks with
+    # the same transport must equal the one-slab result byte for byte ----
+    invariance = None
+    if n > 1:
+        import numpy as np
+
+        Ns, Ms, sw = 64 * n, 256, 20
+        small = IsingLattice.distributed(Ns, Ms, 7, device=dev)
+        r0s, rs = small.slab_info()
+        small.set_beta(BETA).init_random().sweep(sw)
+        mine = np.empty((rs, Ms), dtype=np.int8)
+        small.read_lattice(mine)
+        obs = small.observables()
+        small.close()
+        tdev = "cpu" if same_dev else "cuda"
+        parts = [torch.empty((rs, Ms), dtype=torch.int8, device=tdev) for _ in range(n)]
+        dist.all_gather(parts, torch.from_numpy(mine).to(tdev))
+        if rank == 0:
+            got = torch.cat(parts).cpu().numpy()
+            one = IsingLattice(Ns, Ms, 7, n_gpus=1).set_beta(BETA).init_random().sweep(sw)
+            invariance = {"lattice": [Ns, Ms], "sweeps": sw,
+                          "bit_identical_to_one_gpu": bool(np.array_equal(got, one.read_lattice())),
+                          "observables_equal": obs == one.observables()}
+            one.close()
+
     cpu = None
     if rank == 0 and n == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(M)
@@ -407,6 +432,7 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
+            "invariance": invariance,
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
