@@ -13,7 +13,7 @@
 
 constexpr uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u, W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
 
-struct Keys { uint32_t k0[10], k1[10]; };
+struct Keys { uint32_t k0[10], k1[10]; uint32_t m0, m1; };
 
 __device__ __forceinline__ uint32_t hi_dfma(uint32_t c, double mp, double cc) {
   const double x = __hiloint2double(0x43300000, (int)c);  // 2^52 + c
@@ -46,6 +46,17 @@ template <int V>
 __device__ __forceinline__ uint4 philox(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, const Keys& K,
                                         double mp0, double cc0, double mp1, double cc1) {
   if (V == 3) return philox_flow(c0, c1, c2, c3, K, mp0, cc0, mp1, cc1);
+  if (V == 4) return philox<0>(c0, c1, c2, c3, K, mp0, cc0, mp1, cc1);
+  if (V == 5) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+      const uint64_t p0 = (uint64_t)c0 * K.m0, p1 = (uint64_t)c2 * K.m1;
+      const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ K.k0[r];
+      const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ K.k1[r];
+      c1 = (uint32_t)p1; c3 = (uint32_t)p0; c0 = n0; c2 = n2;
+    }
+    return make_uint4(c0, c1, c2, c3);
+  }
 #pragma unroll
   for (int r = 0; r < 10; ++r) {
     uint32_t hi0, lo0, hi1, lo1;
@@ -76,7 +87,10 @@ __global__ void __launch_bounds__(128) k_philox(Keys K, uint32_t iters, uint32_t
   for (uint32_t it = 0; it < iters; ++it) {
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
-      const uint4 r = philox<V>(base + 4 * gridDim.x * blockDim.x * it + b, row, t, 1u, K, mp0, cc0, mp1, cc1);
+      const uint32_t c = base + 4 * gridDim.x * blockDim.x * it + b;
+      // V = 4: two blocks on the IMAD.WIDE path and two on the DFMA flow path per thread
+      const uint4 r = (V == 4 && b >= 2) ? philox_flow(c, row, t, 1u, K, mp0, cc0, mp1, cc1)
+                                         : philox<V>(c, row, t, 1u, K, mp0, cc0, mp1, cc1);
       acc += r.x ^ (r.y * 3) ^ (r.z * 5) ^ (r.w * 7);
     }
   }
@@ -99,16 +113,17 @@ int main() {
   const int sms = pr.multiProcessorCount;
   Keys K; uint32_t k0 = 1, k1 = 0;
   for (int r = 0; r < 10; ++r) { K.k0[r] = k0; K.k1[r] = k1; k0 += W0; k1 += W1; }
+  K.m0 = M0; K.m1 = M1;
   const double mp0 = (double)M0 / 4294967296.0, mp1 = (double)M1 / 4294967296.0;
   const double cc0 = 4503599627370496.0 - 1048576.0 * (double)M0;
   const double cc1 = 4503599627370496.0 - 1048576.0 * (double)M1;
   const int grid = sms * 16, threads = 128;
   const uint32_t iters = 256;
-  uint32_t* out[4];
-  for (int v = 0; v < 4; ++v) CK(cudaMalloc(&out[v], sizeof(uint32_t) * grid * threads));
+  uint32_t* out[6];
+  for (int v = 0; v < 6; ++v) CK(cudaMalloc(&out[v], sizeof(uint32_t) * grid * threads));
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
-  const char* names[4] = {"wide", "dfma", "mix", "flow"};
-  for (int v = 0; v < 4; ++v) {
+  const char* names[6] = {"wide", "dfma", "mix", "flow", "wide+flow", "wide(param M)"};
+  for (int v = 0; v < 6; ++v) {
     float best = 1e30f;
     for (int rep = 0; rep < 5; ++rep) {
       cudaEventRecord(a);
@@ -116,6 +131,8 @@ int main() {
       if (v == 1) k_philox<1><<<grid, threads>>>(K, iters, 7, 3, mp0, cc0, mp1, cc1, out[v]);
       if (v == 2) k_philox<2><<<grid, threads>>>(K, iters, 7, 3, mp0, cc0, mp1, cc1, out[v]);
       if (v == 3) k_philox<3><<<grid, threads>>>(K, iters, 7, 3, mp0, cc0, mp1, cc1, out[v]);
+      if (v == 4) k_philox<4><<<grid, threads>>>(K, iters, 7, 3, mp0, cc0, mp1, cc1, out[v]);
+      if (v == 5) k_philox<5><<<grid, threads>>>(K, iters, 7, 3, mp0, cc0, mp1, cc1, out[v]);
       cudaEventRecord(b); CK(cudaEventSynchronize(b)); CK(cudaGetLastError());
       float ms; cudaEventElapsedTime(&ms, a, b); if (rep && ms < best) best = ms;
     }
@@ -123,11 +140,11 @@ int main() {
     printf("philox %-5s: %.3f ms  %.0f draws/ns\n", names[v], best, draws / (best * 1e6));
   }
   // correctness: all variants fold to the same values
-  uint32_t* h = new uint32_t[4 * grid * threads];
-  for (int v = 0; v < 4; ++v) CK(cudaMemcpy(h + v * grid * threads, out[v], 4 * grid * threads, cudaMemcpyDeviceToHost));
+  uint32_t* h = new uint32_t[6 * grid * threads];
+  for (int v = 0; v < 6; ++v) CK(cudaMemcpy(h + v * grid * threads, out[v], 4 * grid * threads, cudaMemcpyDeviceToHost));
   int bad = 0;
   for (int i = 0; i < grid * threads; ++i)
-    for (int v = 1; v < 4; ++v) bad += (h[i] != h[v * grid * threads + i]);
+    for (int v = 1; v < 6; ++v) bad += (h[i] != h[v * grid * threads + i]);
   printf("variants agree: %s (%d mismatches)\n", bad ? "NO" : "yes", bad);
   double* dout; CK(cudaMalloc(&dout, sizeof(double) * grid * threads));
   for (int rep = 0; rep < 3; ++rep) {
