@@ -147,6 +147,12 @@ int ising_sweep(ising_t h, int64_t n);
  * are written — at their global offset, or at offset 0 when out_len == R*L_cols. */
 int ising_read_lattice(ising_t h, int8_t* out, int64_t out_len);
 
+/* Unpack global rows [row_begin, row_begin + nrows) to host: out[r*L_cols + J], r relative
+ * to row_begin; out_len >= nrows*L_cols (else RANGE).  The rows must belong to this
+ * process's slabs (rank mode: its own) — else ARG.  For lattices too large for one host
+ * buffer (C4, C5) and for sampled checks. */
+int ising_read_rows(ising_t h, int64_t row_begin, int64_t nrows, int8_t* out, int64_t out_len);
+
 /* Integer observables of the whole lattice (Eq. 1):
  * *up_count = number of +1 spins; *bond_energy = -sum over the 2 N M torus bonds
  * of s s' (each bond once, R11), in [-2NM, 2NM].  STATE before an init.

@@ -65,6 +65,8 @@ def lib() -> ctypes.CDLL:
             "oracle_chain": (None, [i8p, i8p, I64, I64, U64, U32, I64, DBL, INT, i64p, i64p]),
             "oracle_update_slab": (None, [i8p, i8p, i8p, i8p, INT, I64, I64, I64, U64, U32, u64p,
                                            INT]),
+            "oracle_sample_after_one_sweep": (INT, [U64, I64, I64, DBL, INT, I64, I64]),
+            "oracle_sample_row_after_one_sweep": (None, [U64, I64, I64, DBL, INT, I64, i8p]),
             "oracle_set_threads": (None, [INT]),
             "oracle_get_threads": (INT, []),
         }
@@ -119,6 +121,14 @@ def update_slab(target: np.ndarray, source: np.ndarray, above: np.ndarray, below
     lib().oracle_update_slab(_p(target, ctypes.c_int8), _p(source, ctypes.c_int8),
                              _p(above, ctypes.c_int8), _p(below, ctypes.c_int8), int(bool(is_black)),
                              row0, nrows, ny, seed, t, _p(T, ctypes.c_uint64), rule)
+
+
+def sample_row_after_one_sweep(seed: int, N: int, M: int, beta: float, i: int,
+                               rule: int = RULE_METROPOLIS) -> np.ndarray:
+    """Row i after sweep 1 from the random start, site by site (no N x M lattice in memory)."""
+    out = np.empty(M, dtype=np.int8)
+    lib().oracle_sample_row_after_one_sweep(seed, N, M, float(beta), rule, i, _p(out, ctypes.c_int8))
+    return out
 
 
 class Lattice:

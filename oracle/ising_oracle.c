@@ -297,6 +297,58 @@ void oracle_chain(int8_t* black, int8_t* white, int64_t nx, int64_t ny, uint64_t
   }
 }
 
+/* --------------------------------------------------- sampled single sites */
+/* Value of full-lattice site (i, J) of an N x M torus after sweep 1 from the random start,
+ * evaluated site by site without materialising the lattice (for lattices too large for
+ * this oracle, BASELINE configs C4 / C5).  The black phase of sweep 1 reads the four white
+ * neighbours at t = 0; the white phase reads the four black neighbours after the black
+ * phase.  Same stencil (readings R1-R2) and acceptance (R5) as
+ * oracle_update_lattice, same draws (R6, R8). */
+static int init_spin(uint64_t seed, int c, int64_t i, int64_t j) {
+  return oracle_rand(seed, 0, (uint32_t)c, (uint32_t)i, (uint64_t)j) < 0x80000000u ? 1 : -1;
+}
+
+static int accept(int rule, int e, uint32_t r, const uint64_t T[5]) {
+  if (rule == RULE_METROPOLIS) return (e <= 0) || ((uint64_t)r < T[(e + 4) / 2]);
+  return (uint64_t)r < T[(e + 4) / 2];
+}
+
+static int black_after_phase1(uint64_t seed, int64_t nx, int64_t ny, const uint64_t T[5], int rule,
+                              int64_t i, int64_t j) {
+  int64_t ipp = (i + 1 < nx) ? i + 1 : 0, inn = (i - 1 >= 0) ? i - 1 : nx - 1;
+  int64_t jpp = (j + 1 < ny) ? j + 1 : 0, jnn = (j - 1 >= 0) ? j - 1 : ny - 1;
+  int64_t joff = (i % 2) ? jpp : jnn;  /* black target */
+  int nn = init_spin(seed, 1, inn, j) + init_spin(seed, 1, i, j) + init_spin(seed, 1, ipp, j) +
+           init_spin(seed, 1, i, joff);
+  int s = init_spin(seed, 0, i, j);
+  return accept(rule, nn * s, oracle_rand(seed, 1, 0, (uint32_t)i, (uint64_t)j), T) ? -s : s;
+}
+
+int oracle_sample_after_one_sweep(uint64_t seed, int64_t N, int64_t M, double beta, int rule,
+                                  int64_t i, int64_t J) {
+  uint64_t T[5];
+  oracle_thresholds(beta, rule, T);
+  int64_t nx = N, ny = M / 2, j = J / 2;
+  if ((i + J) % 2 == 0) return black_after_phase1(seed, nx, ny, T, rule, i, j);
+  int64_t ipp = (i + 1 < nx) ? i + 1 : 0, inn = (i - 1 >= 0) ? i - 1 : nx - 1;
+  int64_t jpp = (j + 1 < ny) ? j + 1 : 0, jnn = (j - 1 >= 0) ? j - 1 : ny - 1;
+  int64_t joff = (i % 2) ? jnn : jpp;  /* white target */
+  int nn = black_after_phase1(seed, nx, ny, T, rule, inn, j) +
+           black_after_phase1(seed, nx, ny, T, rule, i, j) +
+           black_after_phase1(seed, nx, ny, T, rule, ipp, j) +
+           black_after_phase1(seed, nx, ny, T, rule, i, joff);
+  int s = init_spin(seed, 1, i, j);
+  return accept(rule, nn * s, oracle_rand(seed, 1, 1, (uint32_t)i, (uint64_t)j), T) ? -s : s;
+}
+
+/* Row i of the full lattice after sweep 1 (out: M bytes), site by site (OpenMP over J). */
+void oracle_sample_row_after_one_sweep(uint64_t seed, int64_t N, int64_t M, double beta, int rule,
+                                       int64_t i, int8_t* out) {
+#pragma omp parallel for schedule(static)
+  for (int64_t J = 0; J < M; ++J)
+    out[J] = (int8_t)oracle_sample_after_one_sweep(seed, N, M, beta, rule, i, J);
+}
+
 /* ------------------------------------------------------------- threading */
 void oracle_set_threads(int n) {
 #ifdef _OPENMP

@@ -1210,6 +1210,64 @@ int ising_read_lattice(ising_t h, int8_t* out, int64_t out_len) {
   return ISING_OK;
 }
 
+int ising_read_rows(ising_t h, int64_t row_begin, int64_t nrows, int8_t* out, int64_t out_len) {
+  if (!h || !out || row_begin < 0 || nrows < 0 || row_begin + nrows > h->N) return ISING_ERR_ARG;
+  if (out_len < nrows * h->M) return ISING_ERR_RANGE;
+  if (!h->state_set) return ISING_ERR_STATE;
+  if (nrows == 0) return ISING_OK;
+  if (h->basic) {
+    Device& d = h->devs[0];
+    CU(cudaSetDevice(d.dev));
+    TRY(ensure_staging(d));
+    const int64_t rows_per_chunk = std::max<int64_t>(1, (int64_t)kStagingBytes / h->M);
+    for (int64_t r0 = row_begin; r0 < row_begin + nrows; r0 += rows_per_chunk) {
+      const int64_t rows = std::min<int64_t>(rows_per_chunk, row_begin + nrows - r0);
+      CU(launch_basic_convert(basic_grid(d, rows * h->M), d.stream, h->bplane[0], h->bplane[1],
+                              d.staging, h->M / 2, r0, rows, 1, nullptr));
+      ++h->launch_count;
+      CU(cudaMemcpyAsync(out + (r0 - row_begin) * h->M, d.staging, (size_t)(rows * h->M),
+                         cudaMemcpyDeviceToHost, d.stream));
+    }
+    CU(cudaStreamSynchronize(d.stream));
+    return ISING_OK;
+  }
+  int64_t covered = 0;
+  for (auto& s : h->slabs) {
+    const int64_t lo = std::max(row_begin, s.row0), hi = std::min(row_begin + nrows, s.row0 + s.R);
+    if (lo >= hi) continue;
+    covered += hi - lo;
+    Device& d = h->devs[s.devi];
+    CU(cudaSetDevice(d.dev));
+    TRY(ensure_staging(d));
+    const int64_t rows_per_chunk = std::max<int64_t>(1, (int64_t)kStagingBytes / h->M);
+    for (int64_t ga = lo; ga < hi; ga += rows_per_chunk) {
+      const int64_t gb = std::min<int64_t>(ga + rows_per_chunk, hi);
+      UnpackParams p;
+      p.plane[0] = s.plane[0];
+      p.plane[1] = s.plane[1];
+      p.full = d.staging;
+      p.W = h->W;
+      p.M = h->M;
+      p.row0 = s.row0;
+      p.ra = (int32_t)(ga - s.row0);
+      p.rb = (int32_t)(gb - s.row0);
+      const int64_t total = 2 * (gb - ga) * h->W;
+      const int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)d.sms * 64);
+      k_unpack<<<grid, 256, 0, d.stream>>>(p);
+      CU(cudaGetLastError());
+      ++h->launch_count;
+      CU(cudaMemcpyAsync(out + (ga - row_begin) * h->M, d.staging, (size_t)((gb - ga) * h->M),
+                         cudaMemcpyDeviceToHost, d.stream));
+    }
+  }
+  TRY(sync_all(h));
+  if (covered != nrows) {
+    g_last_error = "ising_read_rows: rows outside this process's slab";
+    return ISING_ERR_ARG;
+  }
+  return ISING_OK;
+}
+
 int ising_observables(ising_t h, int64_t* up_count, int64_t* bond_energy) {
   if (!h || !up_count || !bond_energy) return ISING_ERR_ARG;
   if (!h->state_set) return ISING_ERR_STATE;

@@ -50,6 +50,7 @@ SIGNATURES = {
     "ising_sweep": (_INT, [_VP, _I64]),
     "ising_read_lattice": (_INT, [_VP, _VP, _I64]),
     "ising_observables": (_INT, [_VP, _I64P, _I64P]),
+    "ising_read_rows": (_INT, [_VP, _I64, _I64, _VP, _I64]),
     "ising_sweep_measure": (_INT, [_VP, _I64, _I64, _I64P, _I64P]),
     "ising_last_sweep_ms": (_INT, [_VP, _DBLP]),
     "ising_set_profiling": (_INT, [_VP, _INT]),
@@ -204,6 +205,11 @@ def ising_sweep(h: int, n: int) -> None:
 def ising_read_lattice(h: int, out) -> None:
     ptr, n = _buf_ptr(out, 0, writable=True)
     _check(load().ising_read_lattice(h, ptr, n), "ising_read_lattice")
+
+
+def ising_read_rows(h: int, row_begin: int, nrows: int, out) -> None:
+    ptr, n = _buf_ptr(out, 0, writable=True)
+    _check(load().ising_read_rows(h, int(row_begin), int(nrows), ptr, n), "ising_read_rows")
 
 
 def ising_observables(h: int) -> tuple[int, int]:
@@ -367,6 +373,12 @@ class IsingLattice:
 
     def observables(self) -> tuple[int, int]:
         return ising_observables(self.h)
+
+    def read_rows(self, row_begin: int, nrows: int, out=None) -> np.ndarray:
+        if out is None:
+            out = np.empty((nrows, self.M), dtype=np.int8)
+        ising_read_rows(self.h, row_begin, nrows, out)
+        return out
 
     @property
     def t(self) -> int:

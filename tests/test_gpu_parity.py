@@ -236,3 +236,25 @@ def test_graph_replay_across_beta_and_rule_changes():
         g.sweep(n)
         o.sweep(n)
         assert_same(g, o, f"beta={beta} rule={rule} t={o.t}")
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("N,M", [(cases.C4[0], cases.C4[1]), (cases.C5_ROWS_PER_GPU, cases.C5_COLS)])
+def test_full_size_sampled_rows_after_one_sweep(N, M):
+    # BASELINE configs[3] (131072^2) and the per-GPU slab of configs[4] (131072 x 1048576,
+    # 64 GiB packed) in bench.py's launch configuration: rows sampled across the lattice
+    # (including the wrap rows 0 and N-1) against the oracle's site-by-site evaluation.
+    beta = cases.BETA_TC
+    g = gpu_lattice(N, M, 1, "random", beta)
+    g.sweep(1)
+    rng = np.random.default_rng(N + M)
+    rows = sorted({0, 1, N - 1, N // 2} | set(int(x) for x in rng.integers(0, N, 4)))
+    for i in rows:
+        got = g.read_rows(i, 1)[0]
+        exp = oracle.sample_row_after_one_sweep(1, N, M, beta, i)
+        assert np.array_equal(got, exp), f"row {i}: {int((got != exp).sum())} sites differ"
+    # beta = 0 property at full size: one sweep flips every spin (up -> NM - up, E kept)
+    up0, E0 = g.observables()
+    g.set_beta(0.0).sweep(1)
+    assert g.observables() == (N * M - up0, E0)
+    g.close()

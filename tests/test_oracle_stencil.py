@@ -150,3 +150,14 @@ def test_heatbath_beta_zero_is_fair_coin():
             c = (i + J) % 2
             flipped = oracle.rand(seed, 1, c, i, J // 2) < 2**31
             assert full[i, J] == (-1 if flipped else 1)
+
+
+@pytest.mark.parametrize("N,M", [(8, 8), (12, 16), (64, 64), (6, 10)])
+@pytest.mark.parametrize("rule", [oracle.RULE_METROPOLIS, oracle.RULE_HEATBATH])
+def test_sampled_site_evaluation_matches_full_oracle(N, M, rule):
+    # the site-by-site evaluation used for full-size sampled parity (C4 / C5) equals the
+    # materialised oracle after one sweep
+    beta = 0.4406868
+    full = oracle.Lattice(N, M, 5).init_random().set_beta(beta, rule).sweep(1).full()
+    for i in range(N):
+        assert np.array_equal(oracle.sample_row_after_one_sweep(5, N, M, beta, i, rule), full[i])
