@@ -33,6 +33,22 @@ def onsager_m(T: float, J: float = 1.0) -> float:
     return (1.0 - math.sinh(2.0 * J / T) ** -4) ** 0.125
 
 
+def onsager_energy(T: float, J: float = 1.0) -> float:
+    """Onsager's internal energy per site of the infinite square lattice (each bond once):
+    u = -J coth(2K) [1 + (2/pi) (2 tanh^2(2K) - 1) K(k)],  K = J/T, k = 2 sinh(2K)/cosh^2(2K),
+    K(k) the complete elliptic integral of the first kind (scipy ellipk takes m = k^2).
+    The paper compares magnetizations with Onsager's solution; the energy
+    is the same exact solution's other observable."""
+    from scipy.special import ellipk
+
+    K = J / T
+    kp = 2.0 * math.tanh(2 * K) ** 2 - 1.0
+    if abs(kp) < 1e-12:  # T = Tc: the elliptic term vanishes (K(1) diverges only logarithmically)
+        return -J / math.tanh(2 * K)
+    k = 2.0 * math.sinh(2 * K) / math.cosh(2 * K) ** 2
+    return -J / math.tanh(2 * K) * (1.0 + 2.0 / math.pi * kp * ellipk(k * k))
+
+
 def binder(m2: float, m4: float, conventional: bool = True) -> float:
     """Binder cumulant.  PAPER.md:418 prints 1 - <m^4>/<m^2>^2; conventional adds 1/3."""
     return 1.0 - m4 / ((3.0 if conventional else 1.0) * m2 * m2)
@@ -121,6 +137,38 @@ def kaufman_Z(N: int, M: int, beta: float, J: float = 1.0) -> float:
     z3 = math.prod(2 * math.cosh(N * g / 2) for g in even)
     z4 = math.prod(2 * math.sinh(N * g / 2) for g in even)
     return 0.5 * (2 * math.sinh(2 * K)) ** (N * M / 2) * (z1 + z2 + z3 + z4)
+
+
+def kaufman_logZ(N: int, M: int, beta: float, J: float = 1.0) -> float:
+    """log of kaufman_Z in log-space arithmetic (large tori), same formula."""
+    K = beta * J
+
+    def gamma(k: int) -> float:
+        if k == 0:
+            return 2 * K + math.log(math.tanh(K))
+        return math.acosh(math.cosh(2 * K) / math.tanh(2 * K) - math.cos(math.pi * k / M))
+
+    def log2cosh(x):
+        x = abs(x)
+        return x + math.log1p(math.exp(-2 * x))
+
+    def log2sinh_signed(x):
+        a = abs(x)
+        return a + math.log1p(-math.exp(-2 * a)), (1.0 if x > 0 else -1.0)
+
+    terms = []
+    for ks in ([2 * r + 1 for r in range(M)], [2 * r for r in range(M)]):
+        g = [gamma(k) for k in ks]
+        terms.append((sum(log2cosh(N * x / 2) for x in g), 1.0))
+        logs, sign = 0.0, 1.0
+        for x in g:
+            l, sg = log2sinh_signed(N * x / 2)
+            logs += l
+            sign *= sg
+        terms.append((logs, sign))
+    mx = max(t for t, _ in terms)
+    acc = sum(sg * math.exp(t - mx) for t, sg in terms)
+    return math.log(0.5) + (N * M / 2) * math.log(2 * math.sinh(2 * K)) + mx + math.log(acc)
 
 
 def batch_means(x: np.ndarray, nbatch: int = 100) -> tuple[float, float]:

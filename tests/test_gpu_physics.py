@@ -10,13 +10,13 @@ from tests import cases
 pytestmark = pytest.mark.gpu
 
 
-def measure_abs_m(L, T, start, seed, sweeps, discard, every):
-    g = IsingLattice(L, L, seed).set_beta(1.0 / T)
+def measure_series(L, T, start, seed, sweeps, discard, every, rule=0):
+    g = IsingLattice(L, L, seed).set_beta(1.0 / T, rule)
     g.init_cold() if start == "cold" else g.init_random()
     g.sweep(discard)
-    ups, _ = g.measure((sweeps - discard) // every, every)  # device-side series
+    ups, Es = g.measure((sweeps - discard) // every, every)  # device-side series
     g.close()
-    return (2 * ups - L * L) / (L * L)
+    return (2 * ups - L * L) / (L * L), Es / (L * L)
 
 
 @pytest.mark.parametrize("T,start,expect", [(1.5, "cold", exact.onsager_m(1.5)), (3.0, "random", 0.0)])
@@ -26,10 +26,19 @@ def test_c2_onsager(T, start, expect, seed):
     # |<|m|> - M_Onsager| <= 0.003 (north_star).  T = 1.5 starts cold (reading R21 / the
     # band meta-stability the paper reports for L > 1024).
     L, sweeps = cases.C2[0], cases.C2[3]
-    m = measure_abs_m(L, T, start, seed, sweeps, 2000, 10)
+    m, e = measure_series(L, T, start, seed, sweeps, 2000, 10)
     mean, se = exact.batch_means(np.abs(m), 50)
     assert abs(mean - expect) <= 0.003, (mean, se)
     assert se < 0.001
+    # the same exact solution's energy per site (oracle/exact.onsager_energy)
+    assert abs(np.mean(e) - exact.onsager_energy(T)) <= 0.001
+
+
+def test_heatbath_equilibrium_matches_onsager():
+    # heat-bath dynamics has the same equilibrium: T = 2.0 on 2048^2
+    m, e = measure_series(2048, 2.0, "cold", 3, 12000, 2000, 10, rule=1)
+    assert abs(np.mean(np.abs(m)) - exact.onsager_m(2.0)) <= 0.003
+    assert abs(np.mean(e) - exact.onsager_energy(2.0)) <= 0.001
 
 
 def binder_point(L, T, seed, sweeps, every=1):

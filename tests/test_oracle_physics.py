@@ -53,6 +53,17 @@ def test_onsager_closed_form():
     assert exact.onsager_m(T) == pytest.approx(1 - 2 * u**2 - 8 * u**3, abs=50 * u**4)
 
 
+def test_onsager_energy_closed_form():
+    # u(Tc) = -sqrt 2; the infinite-lattice energy equals -d ln Z / d beta / N of Kaufman's
+    # finite-torus Z (pinned by enumeration above) at L = 64, where finite-size terms vanish
+    assert exact.onsager_energy(exact.TC) == pytest.approx(-math.sqrt(2.0), abs=1e-12)
+    for T in [1.5, 2.0, 3.0]:
+        b, h, L = 1.0 / T, 1e-5, 64
+        E = -(exact.kaufman_logZ(L, L, b + h) - exact.kaufman_logZ(L, L, b - h)) / (2 * h) / L**2
+        assert exact.onsager_energy(T) == pytest.approx(E, abs=1e-7)
+    assert exact.kaufman_logZ(4, 4, 0.3) == pytest.approx(math.log(exact.kaufman_Z(4, 4, 0.3)), rel=1e-12)
+
+
 @pytest.mark.parametrize("beta", [0.2, 0.4406868, 0.8])
 def test_metropolis_4x4_matches_exact_enumeration(beta):
     # Cold start (reading R21), 10^4 warm-up + 10^6 measured sweeps, 100 batch means,
@@ -94,11 +105,13 @@ def test_onsager_magnetization(T, warm, meas):
     L = 128
     lat = oracle.Lattice(L, L, seed=5).init_cold().set_beta(1.0 / T)
     lat.sweep(warm)
-    up, _ = lat.chain(meas)
+    up, E = lat.chain(meas)
     m = np.abs(2 * up - L * L) / (L * L)
     mean, se = exact.batch_means(m, 50)
     assert abs(mean - exact.onsager_m(T)) <= 0.003
     assert se < 0.001
+    e_mean, e_se = exact.batch_means(E / (L * L), 50)
+    assert abs(e_mean - exact.onsager_energy(T)) <= 0.002
 
 
 def _binder_curve(L, temps, warm, meas, seed):
