@@ -303,14 +303,34 @@ __device__ __forceinline__ void spin_until(const unsigned long long* flags, int 
     }
 }
 
-template <int RULE>
-__global__ void __launch_bounds__(128, ISING_MINB) k_halfsweep(const HalfSweepParams p) {
-  if (p.wait_flags) {  // rank-p2p: neighbours done with the previous phase
-    if (threadIdx.x == 0) spin_until(p.wait_flags, 2, p.wait_value);
-    __syncthreads();
-  }
-  // sweep index: absolute, or (CUDA graph replays) a device-resident base + the offset
-  const uint32_t t = p.t_dev ? *p.t_dev + p.t : p.t;
+// Loads.  COHERENT (the persistent kernel, where a plane written in one phase is read by
+// other SMs in the next phase of the same launch): L2-coherent ld.global.cg; otherwise the
+// read-only path for the source plane.
+template <bool COHERENT>
+__device__ __forceinline__ ulonglong2 ld_v2(const uint64_t* p) {
+  if (COHERENT) return __ldcg(reinterpret_cast<const ulonglong2*>(p));
+  return ld_nc_v2(p);
+}
+template <bool COHERENT>
+__device__ __forceinline__ uint64_t ld_1(const uint64_t* p) {
+  if (COHERENT) return __ldcg(reinterpret_cast<const unsigned long long*>(p));
+  return ld_nc(p);
+}
+template <bool COHERENT>
+__device__ __forceinline__ ulonglong2 ld_tgt(const uint64_t* p) {
+  if (COHERENT) return __ldcg(reinterpret_cast<const ulonglong2*>(p));
+  return *reinterpret_cast<const ulonglong2*>(p);
+}
+
+// All work items of one colour phase (the half-sweep proper).  OBS: also reduce the
+// observables of the state this (white) phase produces — every bond has exactly one white
+// end, whose four black neighbours are the N, C, S and side words loaded here, and every
+// black word is the C word of exactly one white word — so a measured chain needs no
+// separate pass over the lattice (Eq. 1; row a8).
+template <int RULE, bool OBS, bool COHERENT>
+__device__ __forceinline__ void halfsweep_items(const HalfSweepParams& p, const uint32_t t,
+                                                unsigned long long& obs_up,
+                                                unsigned long long& obs_anti) {
   const int64_t W = p.W;
   const int64_t chunks = W / kWords;
   const uint64_t* src = p.src + W;  // local row r (r = -1 .. R) at src + r * W
@@ -328,8 +348,8 @@ __global__ void __launch_bounds__(128, ISING_MINB) k_halfsweep(const HalfSweepPa
     uint64_t nv[kWords], cv[kWords];
 #pragma unroll
     for (int v = 0; v < kWords / 2; ++v) {
-      const ulonglong2 a = ld_nc_v2(src + (int64_t)(ra - 1) * W + wc + 2 * v);
-      const ulonglong2 b = ld_nc_v2(src + (int64_t)ra * W + wc + 2 * v);
+      const ulonglong2 a = ld_v2<COHERENT>(src + (int64_t)(ra - 1) * W + wc + 2 * v);
+      const ulonglong2 b = ld_v2<COHERENT>(src + (int64_t)ra * W + wc + 2 * v);
       nv[2 * v] = a.x;
       nv[2 * v + 1] = a.y;
       cv[2 * v] = b.x;
@@ -339,8 +359,8 @@ __global__ void __launch_bounds__(128, ISING_MINB) k_halfsweep(const HalfSweepPa
       uint64_t sv[kWords], tv[kWords];
 #pragma unroll
       for (int v = 0; v < kWords / 2; ++v) {
-        const ulonglong2 a = ld_nc_v2(src + (int64_t)(r + 1) * W + wc + 2 * v);
-        const ulonglong2 b = *reinterpret_cast<const ulonglong2*>(tgt + (int64_t)r * W + wc + 2 * v);
+        const ulonglong2 a = ld_v2<COHERENT>(src + (int64_t)(r + 1) * W + wc + 2 * v);
+        const ulonglong2 b = ld_tgt<COHERENT>(tgt + (int64_t)r * W + wc + 2 * v);
         sv[2 * v] = a.x;
         sv[2 * v + 1] = a.y;
         tv[2 * v] = b.x;
@@ -350,7 +370,7 @@ __global__ void __launch_bounds__(128, ISING_MINB) k_halfsweep(const HalfSweepPa
       // side word: the left word if (black and i even) or (white and i odd), else the
       // right one (Fig. 3 caption PAPER.md:208; reading R2)
       const bool west = ((gi & 1) == 0) == (p.colour == 0);
-      const uint64_t sw = ld_nc(src + (int64_t)r * W + (west ? wwest : weast));
+      const uint64_t sw = ld_1<COHERENT>(src + (int64_t)r * W + (west ? wwest : weast));
       uint64_t side[kWords];
 #pragma unroll
       for (int k = 0; k < kWords; ++k) {
@@ -363,6 +383,11 @@ __global__ void __launch_bounds__(128, ISING_MINB) k_halfsweep(const HalfSweepPa
       for (int k = 0; k < kWords; ++k) {
         const uint32_t ctr0 = (uint32_t)(4 * (wc + k));  // Philox counter word 1 = j / 4 (R6)
         tv[k] = update_word<RULE>(tv[k], nv[k], cv[k], sv[k], side[k], ctr0, (uint32_t)gi, t, p);
+        if (OBS) {
+          obs_up += __popcll(tv[k]) + __popcll(cv[k]);
+          obs_anti += __popcll(tv[k] ^ nv[k]) + __popcll(tv[k] ^ cv[k]) + __popcll(tv[k] ^ sv[k]) +
+                      __popcll(tv[k] ^ side[k]);
+        }
       }
 #pragma unroll
       for (int v = 0; v < kWords / 2; ++v) {
@@ -376,6 +401,29 @@ __global__ void __launch_bounds__(128, ISING_MINB) k_halfsweep(const HalfSweepPa
         nv[k] = cv[k];
         cv[k] = sv[k];
       }
+    }
+  }
+}
+
+template <int RULE, bool OBS = false>
+__global__ void __launch_bounds__(128, ISING_MINB) k_halfsweep(const HalfSweepParams p) {
+  if (p.wait_flags) {  // rank-p2p: neighbours done with the previous phase
+    if (threadIdx.x == 0) spin_until(p.wait_flags, 2, p.wait_value);
+    __syncthreads();
+  }
+  // sweep index: absolute, or (CUDA graph replays) a device-resident base + the offset
+  const uint32_t t = p.t_dev ? *p.t_dev + p.t : p.t;
+  unsigned long long obs_up = 0, obs_anti = 0;
+  halfsweep_items<RULE, OBS, false>(p, t, obs_up, obs_anti);
+  if (OBS) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      obs_up += __shfl_xor_sync(0xffffffffu, obs_up, off);
+      obs_anti += __shfl_xor_sync(0xffffffffu, obs_anti, off);
+    }
+    if ((threadIdx.x & 31) == 0 && (obs_up | obs_anti)) {
+      atomicAdd(&p.obs_out[0], obs_up);
+      atomicAdd(&p.obs_out[1], obs_anti);
     }
   }
   if (p.signal_up) {  // rank-p2p: the last block publishes "phase done" to both neighbours
@@ -436,6 +484,86 @@ cudaError_t launch_gather(cudaStream_t st, const GatherParams& p) {
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------- persistent sweeps
+// Small lattices are launch-bound (a 2048^2 half-sweep is ~1.5 us of work).  One
+// cooperative launch runs n whole sweeps: every block of the (co-resident) grid walks its
+// items of the black phase, meets the others at a grid barrier, walks the white phase, and
+// meets them again.  Loads are L2-coherent (a plane written in one phase is read by other
+// SMs in the next).  With obs_base, the white phase of every `every`-th sweep also reduces
+// the observables of the state it produces into slot (s / every - 1).
+__device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void grid_barrier(unsigned int* count, unsigned int* gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int g = ld_acquire_gpu(gen);
+    __threadfence();
+    if (atomicAdd(count, 1u) == gridDim.x - 1) {
+      atomicExch(count, 0u);
+      __threadfence();
+      atomicAdd(gen, 1u);
+    } else {
+      while (ld_acquire_gpu(gen) == g) {
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+constexpr int kPersistThreads = 512;  // one CTA per SM: fewer barrier arrivals
+template <int RULE, bool OBS>
+__global__ void __launch_bounds__(kPersistThreads, 1) k_sweeps_persistent(const PersistentParams P) {
+  for (uint32_t s = 1; s <= P.n; ++s) {
+    const uint32_t t = P.t0 + s;
+    unsigned long long up = 0, anti = 0;
+    halfsweep_items<RULE, false, true>(P.ph[0], t, up, anti);
+    grid_barrier(P.bar_count, P.bar_gen);
+    if (OBS && s % P.every == 0) {
+      halfsweep_items<RULE, true, true>(P.ph[1], t, up, anti);
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        up += __shfl_xor_sync(0xffffffffu, up, off);
+        anti += __shfl_xor_sync(0xffffffffu, anti, off);
+      }
+      if ((threadIdx.x & 31) == 0 && (up | anti)) {
+        unsigned long long* slot = P.obs_base + 2 * (size_t)(s / P.every - 1);
+        atomicAdd(&slot[0], up);
+        atomicAdd(&slot[1], anti);
+      }
+    } else {
+      halfsweep_items<RULE, false, true>(P.ph[1], t, up, anti);
+    }
+    grid_barrier(P.bar_count, P.bar_gen);
+  }
+}
+
+template <int RULE, bool OBS>
+static cudaError_t coop_launch(int grid, cudaStream_t st, const PersistentParams& P) {
+  void* args[] = {const_cast<PersistentParams*>(&P)};
+  return cudaLaunchCooperativeKernel((const void*)k_sweeps_persistent<RULE, OBS>, dim3(grid),
+                                     dim3(kPersistThreads), args, 0, st);
+}
+
+cudaError_t launch_persistent(int rule, int grid, cudaStream_t st, const PersistentParams& P) {
+  const bool obs = P.obs_base != nullptr;
+  switch (rule) {
+    case 0: return obs ? coop_launch<0, true>(grid, st, P) : coop_launch<0, false>(grid, st, P);
+    case 2: return obs ? coop_launch<2, true>(grid, st, P) : coop_launch<2, false>(grid, st, P);
+    case 3: return obs ? coop_launch<3, true>(grid, st, P) : coop_launch<3, false>(grid, st, P);
+    default: return obs ? coop_launch<1, true>(grid, st, P) : coop_launch<1, false>(grid, st, P);
+  }
+}
+
+cudaError_t persistent_occupancy(int* blocks_per_sm) {
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_sweeps_persistent<0, true>,
+                                                       kPersistThreads, 0);
+}
+
 // Philox-only throughput probe (ALU roofline denominator):
 // the same philox4x32_10 as the half-sweep, counter {x, row, t, colour} with the
 // same warp-uniform words, outputs XOR-folded so nothing but the fold is stored.
@@ -457,6 +585,17 @@ cudaError_t launch_philox_probe(int grid, cudaStream_t st, const PhiloxKeys& K,
 }
 
 cudaError_t launch_halfsweep(int rule, int grid, cudaStream_t st, const HalfSweepParams& p) {
+  if (p.obs_out) {  // measured white phase (Metropolis fast path or heat bath fast path)
+    if (rule == 0)
+      k_halfsweep<0, true><<<grid, 128, 0, st>>>(p);
+    else if (rule == 2)
+      k_halfsweep<2, true><<<grid, 128, 0, st>>>(p);
+    else if (rule == 3)
+      k_halfsweep<3, true><<<grid, 128, 0, st>>>(p);
+    else
+      k_halfsweep<1, true><<<grid, 128, 0, st>>>(p);
+    return cudaGetLastError();
+  }
   if (rule == 0)
     k_halfsweep<0><<<grid, 128, 0, st>>>(p);
   else if (rule == 2)

@@ -62,6 +62,20 @@ struct HalfSweepParams {
   unsigned long long* signal_dn;         // lower neighbour's from_up flag (peer memory)
   unsigned long long signal_value;
   unsigned int* done_counter;            // block counter for the last-block signal
+  // white phase of a measured sweep: add [up count, antiparallel bonds] of the resulting
+  // state into obs_out[0..1] (null: no measurement)
+  unsigned long long* obs_out;
+};
+
+// Persistent multi-sweep kernel for small lattices (one slab, one device).
+struct PersistentParams {
+  HalfSweepParams ph[2];          // black and white phase parameters
+  uint32_t t0;                    // runs sweeps t0 + 1 .. t0 + n
+  uint32_t n;
+  unsigned int* bar_count;        // grid barrier state (zero-initialised)
+  unsigned int* bar_gen;
+  unsigned long long* obs_base;   // measured chain: slot k = after sweep (k + 1) * every
+  uint32_t every;
 };
 
 // Rank-p2p synchronisation helpers (one thread each).
@@ -149,6 +163,8 @@ cudaError_t launch_basic_convert(int grid, cudaStream_t st, int8_t* black, int8_
 
 // Host-side launchers (defined in ising_kernels.cu).
 cudaError_t launch_sync(cudaStream_t st, const SyncParams& p);
+cudaError_t launch_persistent(int rule, int grid, cudaStream_t st, const PersistentParams& P);
+cudaError_t persistent_occupancy(int* blocks_per_sm);
 cudaError_t launch_set_u32(cudaStream_t st, uint32_t* dst, uint32_t v, int add);
 cudaError_t launch_gather(cudaStream_t st, const GatherParams& p);
 cudaError_t launch_halfsweep(int rule, int grid, cudaStream_t st, const HalfSweepParams& p);

@@ -156,6 +156,10 @@ struct ising_ctx {
   uint32_t* t_dev = nullptr;               // device-resident sweep base read by the kernels
   int64_t graph_launches = 0;              // kernel nodes per graph replay
   bool graphs_enabled = true;
+  bool persistent_enabled = false;         // opt-in (ISING_PERSISTENT=1): measured slower
+                                           // than graph replay on B200 (grid barrier ~3 us)
+  unsigned int* bar = nullptr;             // persistent kernel's grid barrier state
+  int persist_blocks_per_sm = 0;
   // basic byte-per-spin layout (ising_create_basic; §3.1)
   bool basic = false;
   int8_t* bplane[2] = {nullptr, nullptr};
@@ -303,6 +307,7 @@ void destroy_ctx(ising_ctx* h) {
   for (int c = 0; c < 2; ++c)
     if (h->bplane[c]) cudaFree(h->bplane[c]);
   if (h->t_dev) cudaFree(h->t_dev);
+  if (h->bar) cudaFree(h->bar);
   delete h;
 }
 
@@ -323,8 +328,17 @@ void halfsweep_geometry(const ising_ctx* h, const Device& d, int64_t rows, int* 
   *grid = (int)std::min<int64_t>((*items + 127) / 128, int64_t(1) << 30);
 }
 
+// kernel variant: 0 = Metropolis with both thresholds < 2^32 (the fast path),
+// 2 = Metropolis generic (tiny beta), 3 = heat bath with all thresholds < 2^32 (the fast
+// path), 1 = heat bath generic
+int kernel_variant(const ising_ctx* h) {
+  if (h->rule == ISING_RULE_METROPOLIS) return (h->acc.keep3 & h->acc.keep4) ? 0 : 2;
+  return (h->acc.always_mask == 0) ? 3 : 1;
+}
+
 int run_halfsweep(ising_ctx* h, Slab& s, int c, int r_begin, int r_end, uint64_t* halo_up,
-                     uint64_t* halo_dn, uint32_t t, bool t_from_dev = false) {
+                     uint64_t* halo_dn, uint32_t t, bool t_from_dev = false,
+                     unsigned long long* obs = nullptr) {
   if (r_end <= r_begin) return ISING_OK;
   Device& d = h->devs[s.devi];
   HalfSweepParams p{};
@@ -341,6 +355,7 @@ int run_halfsweep(ising_ctx* h, Slab& s, int c, int r_begin, int r_end, uint64_t
   halfsweep_geometry(h, d, r_end - r_begin, &p.H, &p.items, &grid);
   p.t = t;
   p.t_dev = t_from_dev ? h->t_dev : nullptr;
+  p.obs_out = obs;
   p.colour = (uint32_t)c;
   p.keys = h->keys;
   p.acc = h->acc;
@@ -356,12 +371,7 @@ int run_halfsweep(ising_ctx* h, Slab& s, int c, int r_begin, int r_end, uint64_t
   }
   const bool prof = h->profiling && s.devi == 0;
   if (prof) CU(cudaEventRecord(h->prof_events[2 * h->kernel_launches], d.stream));
-  // kernel variant: 0 = Metropolis with both thresholds < 2^32 (the fast path),
-  // 2 = Metropolis generic (tiny beta), 1 = heat bath
-  // 3 = heat bath with all thresholds < 2^32 (the fast path), 1 = heat bath generic
-  int variant = (h->acc.always_mask == 0) ? 3 : 1;
-  if (h->rule == ISING_RULE_METROPOLIS) variant = (h->acc.keep3 & h->acc.keep4) ? 0 : 2;
-  CU(launch_halfsweep(variant, grid, d.stream, p));
+  CU(launch_halfsweep(kernel_variant(h), grid, d.stream, p));
   if (prof) {
     CU(cudaEventRecord(h->prof_events[2 * h->kernel_launches + 1], d.stream));
     ++h->kernel_launches;
@@ -380,7 +390,8 @@ int sync_all(ising_ctx* h) {
 }
 
 // One colour phase, LOCAL mode.
-int phase_local(ising_ctx* h, int c, uint32_t t, bool t_from_dev = false) {
+int phase_local(ising_ctx* h, int c, uint32_t t, bool t_from_dev = false,
+                const std::vector<unsigned long long*>* obs = nullptr) {
   const int n = (int)h->slabs.size();
   const bool multi_dev = h->devs.size() > 1;
   if (multi_dev) {
@@ -406,7 +417,7 @@ int phase_local(ising_ctx* h, int c, uint32_t t, bool t_from_dev = false) {
     // local row 0 -> upper slab's bottom halo (padded row R+1); local row R-1 -> lower
     // slab's top halo (padded row 0).
     TRY(run_halfsweep(h, s, c, 0, (int)s.R, up.plane[c] + (up.R + 1) * h->W, dn.plane[c], t,
-                      t_from_dev));
+                      t_from_dev, (obs && c == 1) ? (*obs)[s.devi] : nullptr));
   }
   if (multi_dev) {
     for (auto& d : h->devs) {
@@ -611,6 +622,8 @@ int create_local(ising_t* out, int64_t N, int64_t M, uint64_t seed, int n_slabs,
   if (env) h->rows_per_item_override = atoi(env);
   const char* genv = getenv("ISING_GRAPHS");
   if (genv && genv[0] == '0') h->graphs_enabled = false;
+  const char* penv = getenv("ISING_PERSISTENT");
+  if (penv && penv[0] == '1') h->persistent_enabled = true;
   *out = h;
   return ISING_OK;
 }
@@ -660,15 +673,76 @@ int h2d_rows(ising_ctx* h, int8_t* dst, const int8_t* in, int64_t g, int64_t n, 
   return ISING_OK;
 }
 
-// Enqueue sweeps t+1 .. t+n on the handle's streams (no synchronisation); t += n.
-int enqueue_sweeps(ising_ctx* h, int64_t n) {
+// Persistent multi-sweep launch (small single-slab lattices): sweeps t+1 .. t+n in one
+// cooperative kernel; with obs_base, slot k receives the observables after sweep
+// t + (k+1) * every.
+constexpr int64_t kPersistMaxSpins = int64_t(1) << 24;
+
+bool persistent_eligible(const ising_ctx* h) {
+  return h->persistent_enabled && !h->rank_mode && !h->basic && h->devs.size() == 1 &&
+         h->slabs.size() == 1 && !h->profiling && h->N * h->M <= kPersistMaxSpins;
+}
+
+int run_persistent(ising_ctx* h, int64_t n, unsigned long long* obs_base, int64_t every) {
+  Device& d = h->devs[0];
+  Slab& s = h->slabs[0];
+  CU(cudaSetDevice(d.dev));
+  if (!h->bar) {
+    CU(cudaMalloc(&h->bar, 2 * sizeof(unsigned int)));
+    CU(cudaMemsetAsync(h->bar, 0, 2 * sizeof(unsigned int), d.stream));
+  }
+  if (h->persist_blocks_per_sm <= 0) {
+    CU(persistent_occupancy(&h->persist_blocks_per_sm));
+    if (h->persist_blocks_per_sm < 1) h->persist_blocks_per_sm = 1;
+  }
+  const int grid = d.sms * h->persist_blocks_per_sm;
+  PersistentParams P{};
+  for (int c = 0; c < 2; ++c) {
+    HalfSweepParams& p = P.ph[c];
+    p.tgt = s.plane[c];
+    p.src = s.plane[1 - c];
+    p.halo_up = s.plane[c] + (s.R + 1) * h->W;  // one slab: its own halo rows
+    p.halo_dn = s.plane[c];
+    p.W = h->W;
+    p.row0 = s.row0;
+    p.R = (int32_t)s.R;
+    p.r_begin = 0;
+    p.r_end = (int32_t)s.R;
+    // H = 1 unless the grid has more threads than chunk-rows
+    const int64_t chunks = h->W / kWordsPerItem;
+    int hh = 1;
+    while (hh < 32 && chunks * ((s.R + 2 * hh - 1) / (2 * hh)) >= (int64_t)grid * 512) hh *= 2;
+    p.H = hh;
+    p.items = chunks * ((s.R + hh - 1) / hh);
+    p.colour = (uint32_t)c;
+    p.keys = h->keys;
+    p.acc = h->acc;
+  }
+  P.t0 = (uint32_t)h->t;
+  P.n = (uint32_t)n;
+  P.bar_count = h->bar;
+  P.bar_gen = h->bar + 1;
+  P.obs_base = obs_base;
+  P.every = (uint32_t)std::max<int64_t>(every, 1);
+  CU(launch_persistent(kernel_variant(h), grid, d.stream, P));
+  ++h->launch_count;
+  h->t += (uint64_t)n;
+  return ISING_OK;
+}
+
+// Enqueue sweeps t+1 .. t+n on the handle's streams (no synchronisation); t += n.  With
+// obs (LOCAL mode), the white phase of sweep t+n also reduces the observables of the state
+// it produces into obs[device][0..1] (fused; no extra pass).
+int enqueue_sweeps(ising_ctx* h, int64_t n, const std::vector<unsigned long long*>* obs = nullptr) {
+  if (n > 0 && persistent_eligible(h)) return run_persistent(h, n, obs ? (*obs)[0] : nullptr, n);
   int64_t k0 = 1;
-  if (graph_eligible(h) && n >= kGraphSweeps) {
+  const int64_t n_graph = obs ? n - 1 : n;  // the measured sweep is launched directly
+  if (graph_eligible(h) && n_graph >= kGraphSweeps) {
     if (!h->gexec) TRY(build_graph(h));
     Device& d = h->devs[0];
     CU(launch_set_u32(d.stream, h->t_dev, (uint32_t)h->t, 0));
     ++h->launch_count;
-    const int64_t reps = n / kGraphSweeps;
+    const int64_t reps = n_graph / kGraphSweeps;
     for (int64_t r = 0; r < reps; ++r) {
       CU(cudaGraphLaunch(h->gexec, d.stream));
       h->launch_count += h->graph_launches;
@@ -683,7 +757,7 @@ int enqueue_sweeps(ising_ctx* h, int64_t n) {
       else if (h->rank_mode && h->world > 1)
         TRY(phase_rank(h, c, t));
       else
-        TRY(phase_local(h, c, t));
+        TRY(phase_local(h, c, t, false, k == n ? obs : nullptr));
     }
   }
   h->t += (uint64_t)n;
@@ -1345,10 +1419,13 @@ int ising_sweep_measure(ising_t h, int64_t n_samples, int64_t every, int64_t* up
   }
   h->kernel_launches = 0;
   std::vector<unsigned long long*> slot(base.size());
-  for (int64_t k = 0; k < n_samples; ++k) {
-    TRY(enqueue_sweeps(h, every));
-    for (size_t d = 0; d < base.size(); ++d) slot[d] = base[d] + 2 * k;
-    TRY(enqueue_observables(h, slot));
+  if (n_samples > 0 && persistent_eligible(h)) {
+    TRY(run_persistent(h, n_samples * every, base[0], every));  // the whole chain, one launch
+  } else {
+    for (int64_t k = 0; k < n_samples; ++k) {
+      for (size_t d = 0; d < base.size(); ++d) slot[d] = base[d] + 2 * k;
+      TRY(enqueue_sweeps(h, every, &slot));  // observables fused into the last white phase
+    }
   }
   for (auto& d : h->devs) {
     CU(cudaSetDevice(d.dev));

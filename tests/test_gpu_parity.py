@@ -258,3 +258,22 @@ def test_full_size_sampled_rows_after_one_sweep(N, M):
     g.set_beta(0.0).sweep(1)
     assert g.observables() == (N * M - up0, E0)
     g.close()
+
+
+def test_persistent_kernel_path(monkeypatch):
+    # opt-in persistent multi-sweep kernel (ISING_PERSISTENT=1): same lattices and series
+    monkeypatch.setenv("ISING_PERSISTENT", "1")
+    N, M = 128, 128
+    g = gpu_lattice(N, M, 6, "random", 0.4406868)
+    o = oracle_lattice(N, M, 6, "random", 0.4406868)
+    g.sweep(37)
+    o.sweep(37)
+    assert_same(g, o, "persistent sweeps")
+    ups, Es = g.measure(25, 3)
+    ou, oE = o.chain(75)
+    assert np.array_equal(ups, ou[2::3]) and np.array_equal(Es, oE[2::3])
+    g.set_beta(0.4406868, ising.RULE_HEATBATH)
+    o.set_beta(0.4406868, oracle.RULE_HEATBATH)
+    g.sweep(5)
+    o.sweep(5)
+    assert_same(g, o, "persistent heat bath")

@@ -16,3 +16,14 @@ for N in [64, 512, 2048, 4096]:
     print(f"ISING_GRAPHS={os.environ.get('ISING_GRAPHS', '1')} L={N}: device {N*N*2048/(ms*1e6):8.1f} flips/ns, "
           f"wall {N*N*2048/(wall*1e9):8.1f} flips/ns, {1e3*ms/2048:.2f} us/sweep")
     lat.close()
+
+# measured chain (observables fused into the white phase) on C2: every = 1 and 10
+for every in [1, 10]:
+    lat = IsingLattice(2048, 2048, 1).set_beta(0.4406868).init_random()
+    lat.sweep(64)
+    t0 = time.perf_counter()
+    lat.measure(2048 // every, every)
+    wall = time.perf_counter() - t0
+    print(f"measure every={every}: device {2048*2048*2048/(lat.last_sweep_ms()*1e6):8.1f} flips/ns, "
+          f"wall {2048*2048*2048/(wall*1e9):8.1f} flips/ns")
+    lat.close()
