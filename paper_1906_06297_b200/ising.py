@@ -309,11 +309,28 @@ class IsingLattice:
         if device is None:
             device = int(os.environ.get("LOCAL_RANK", rank))
         if transport == "p2p":
-            h = ising_create_rank_p2p(L_rows, L_cols, seed, rank, world, device)
-            blobs = [None] * world
-            dist.all_gather_object(blobs, ising_ipc_handle(h))
-            ising_ipc_connect(h, b"".join(blobs))
-        elif transport == "nccl":
+            # every rank must agree: if CUDA IPC / peer mapping fails anywhere, all ranks
+            # fall back to the NCCL transport together (both are GPU paths)
+            h, err = None, None
+            try:
+                h = ising_create_rank_p2p(L_rows, L_cols, seed, rank, world, device)
+                blobs = [None] * world
+                dist.all_gather_object(blobs, ising_ipc_handle(h))
+                ising_ipc_connect(h, b"".join(blobs))
+            except IsingError as e:
+                err = e
+            ok = [err is None]
+            oks = [None] * world
+            dist.all_gather_object(oks, ok[0])
+            if all(oks):
+                return cls(L_rows, L_cols, seed, _handle=h)
+            if h is not None:
+                ising_destroy(h)
+            import warnings
+
+            warnings.warn(f"rank-p2p transport unavailable ({err or 'on another rank'}); using NCCL")
+            transport = "nccl"
+        if transport == "nccl":
             obj = [ising_nccl_unique_id() if (rank == 0 and world > 1) else None]
             if world > 1:
                 dist.broadcast_object_list(obj, src=0)
