@@ -51,23 +51,6 @@ __device__ __forceinline__ uint64_t ld_nc(const uint64_t* p) {
 
 constexpr uint32_t kLane0 = 0x11111111u;  // bit 0 of every nibble of a 32-bit half
 
-// Per-half (8 lanes) classification of the aligned-neighbour count a = s ? n : 4 - n
-// (s = spin bit, n = neighbour sum).  B = a + 3 in 3..7 per lane:
-//   s = 1: B = n + 3;  s = 0: B = n ^ 7 = 7 - n.
-// ge3 (a >= 3) <=> B in {6, 7} <=> bits 1 and 2 set; is4 (a = 4) <=> B = 7.
-struct Class8 {
-  uint32_t ge3, is4;  // lane bit at 4k
-};
-
-__device__ __forceinline__ Class8 classify8(uint32_t s, uint32_t n) {
-  const uint32_t B = (n + 3u * s) ^ (7u * s) ^ 0x77777777u;
-  const uint32_t g = B & (B << 1) & 0x44444444u;
-  Class8 c;
-  c.ge3 = g >> 2;
-  c.is4 = (g & (B << 2)) >> 2;
-  return c;
-}
-
 // One 64-bit target word: 16 spins of plane row `row` (global), plane columns
 // 4*ctr0 .. 4*ctr0 + 15.  n, c, s: source words above / same / below; side: the
 // spliced side word.  Metropolis acceptance:
@@ -194,7 +177,8 @@ __device__ __forceinline__ void hb_step(uint32_t& acc, uint32_t r, const uint32_
 }
 
 __device__ __forceinline__ uint32_t hb_accept8(uint32_t s, uint32_t n, uint32_t nc) {
-  const uint32_t B = (n + 3u * s) ^ (7u * s) ^ 0x77777777u;  // a + 3 per lane
+  // a + 3 per lane (a = s ? n : 4 - n): s = 1 -> n + 3; s = 0 -> n ^ 7 = 7 - n
+  const uint32_t B = (n + 3u * s) ^ (7u * s) ^ 0x77777777u;
   const uint32_t x = B + nc;
   return s ^ ((~x >> 3) & kLane0);
 }
