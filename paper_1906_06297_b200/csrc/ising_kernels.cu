@@ -339,12 +339,16 @@ __device__ __forceinline__ void halfsweep_items(const HalfSweepParams& p, const 
       cv[2 * v] = b.x;
       cv[2 * v + 1] = b.y;
     }
-    for (int r = ra; r < rb; ++r) {
+    // row pointers advanced by W per row (no per-row 64-bit index arithmetic)
+    const uint64_t* sp = src + (int64_t)(ra + 1) * W + wc;  // source row r + 1
+    const uint64_t* swp = src + (int64_t)ra * W;             // source row r (side words)
+    uint64_t* tp = tgt + (int64_t)ra * W + wc;               // target row r
+    for (int r = ra; r < rb; ++r, sp += W, swp += W, tp += W) {
       uint64_t sv[kWords], tv[kWords];
 #pragma unroll
       for (int v = 0; v < kWords / 2; ++v) {
-        const ulonglong2 a = ld_v2<COHERENT>(src + (int64_t)(r + 1) * W + wc + 2 * v);
-        const ulonglong2 b = ld_tgt<COHERENT>(tgt + (int64_t)r * W + wc + 2 * v);
+        const ulonglong2 a = ld_v2<COHERENT>(sp + 2 * v);
+        const ulonglong2 b = ld_tgt<COHERENT>(tp + 2 * v);
         sv[2 * v] = a.x;
         sv[2 * v + 1] = a.y;
         tv[2 * v] = b.x;
@@ -354,7 +358,7 @@ __device__ __forceinline__ void halfsweep_items(const HalfSweepParams& p, const 
       // side word: the left word if (black and i even) or (white and i odd), else the
       // right one (Fig. 3 caption PAPER.md:208; reading R2)
       const bool west = ((gi & 1) == 0) == (p.colour == 0);
-      const uint64_t sw = ld_1<COHERENT>(src + (int64_t)r * W + (west ? wwest : weast));
+      const uint64_t sw = ld_1<COHERENT>(swp + (west ? wwest : weast));
       uint64_t side[kWords];
 #pragma unroll
       for (int k = 0; k < kWords; ++k) {
@@ -376,7 +380,7 @@ __device__ __forceinline__ void halfsweep_items(const HalfSweepParams& p, const 
 #pragma unroll
       for (int v = 0; v < kWords / 2; ++v) {
         const ulonglong2 o = make_ulonglong2(tv[2 * v], tv[2 * v + 1]);
-        *reinterpret_cast<ulonglong2*>(tgt + (int64_t)r * W + wc + 2 * v) = o;
+        *reinterpret_cast<ulonglong2*>(tp + 2 * v) = o;
         if (r == 0 && p.halo_up) *reinterpret_cast<ulonglong2*>(p.halo_up + wc + 2 * v) = o;
         if (r == p.R - 1 && p.halo_dn) *reinterpret_cast<ulonglong2*>(p.halo_dn + wc + 2 * v) = o;
       }
