@@ -414,7 +414,7 @@ def run_ours(args):
                 "unit": "flips/ns" if alu_bound else "GB/s",
                 "frac": flips_per_ns_kernel / alu_peak if alu_bound else hbm_gbs / hbm_peak,
                 "traffic": traffic,
-                "kernel": "k_basic_halfsweep<0>" if basic else "k_halfsweep<0>",
+                "kernel": "k_basic_halfsweep<0>" if basic else ("k_halfsweep_staged<0>" if (M // 32) % 256 == 0 else "k_halfsweep<0>"),
                 "alu_roof_flips_per_ns": alu_peak,
                 "hbm_roof_flips_per_ns": hbm_roof_flips,
                 "avg_launch_ms": avg_launch_ms,

@@ -472,6 +472,162 @@ cudaError_t launch_gather(cudaStream_t st, const GatherParams& p) {
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------- TMA-staged variant
+// The north_star's "shared-memory or TMA staging of the neighbour-colour rows": a block
+// owns 128 chunks (256 words) of a band of up to kStageRows rows; one elected thread
+// issues one cp.async.bulk (TMA bulk copy, completes on an mbarrier) per source row of
+// the band plus its two halo rows, the two words beyond the block's span come from plain
+// loads, and the threads read N / C / S / side words from shared memory.  Measured
+// against the register-rolling kernel in profiles/r01_ncu_halfsweep.md (371.6 vs 394.6 us
+// per C3 half-sweep: the shared-memory reads replace the per-row global loads and their
+// address arithmetic); used whenever W is a multiple of 256 words (ISING_STAGED=0 opts out).
+#ifndef ISING_STAGE_ROWS
+#define ISING_STAGE_ROWS 16
+#endif
+constexpr int kStageRows = ISING_STAGE_ROWS;
+constexpr int kStageWords = 256;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+template <int RULE, bool OBS = false>
+__global__ void __launch_bounds__(128, ISING_MINB) k_halfsweep_staged(const HalfSweepParams p) {
+  if (p.wait_flags) {  // rank-p2p: neighbours done with the previous phase
+    if (threadIdx.x == 0) spin_until(p.wait_flags, 2, p.wait_value);
+    __syncthreads();
+  }
+  __shared__ alignas(128) uint64_t tile[kStageRows + 2][kStageWords];
+  __shared__ uint64_t edge[kStageRows + 2][2];
+  __shared__ alignas(8) uint64_t mbar;
+  const int64_t W = p.W;
+  const int64_t bpr = W / kStageWords;  // blocks per band
+  const int band = (int)(blockIdx.x / bpr);
+  const int64_t w0 = (int64_t)(blockIdx.x - (int64_t)band * bpr) * kStageWords;
+  const int ra = p.r_begin + band * kStageRows;
+  const int rb = min(ra + kStageRows, p.r_end);
+  const int nrows = rb - ra;
+  const uint64_t* src = p.src + W;  // local row r at src + r * W
+  uint64_t* tgt = p.tgt + W;
+  const uint32_t bar = smem_u32(&mbar);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t bytes = (uint32_t)(nrows + 2) * kStageWords * 8;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+    for (int rr = 0; rr < nrows + 2; ++rr) {
+      const uint64_t* g = src + (int64_t)(ra - 1 + rr) * W + w0;
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+          ::"r"(smem_u32(&tile[rr][0])), "l"(g), "r"((uint32_t)(kStageWords * 8)), "r"(bar)
+          : "memory");
+    }
+  }
+  // the word left of the span (west side of the first thread) and right of it (east side
+  // of the last thread) for the band's rows, with the periodic wrap
+  if (threadIdx.x < 2 * nrows) {
+    const int rr = threadIdx.x >> 1;
+    const int64_t col = (threadIdx.x & 1) ? ((w0 + kStageWords == W) ? 0 : w0 + kStageWords)
+                                          : ((w0 == 0) ? W - 1 : w0 - 1);
+    edge[rr + 1][threadIdx.x & 1] = ld_nc(src + (int64_t)(ra + rr) * W + col);
+  }
+  __syncthreads();
+  {
+    uint32_t done = 0;
+    while (!done)
+      asm volatile(
+          "{\n\t.reg .pred q;\n\t"
+          "mbarrier.try_wait.parity.shared::cta.b64 q, [%1], 0;\n\t"
+          "selp.u32 %0, 1, 0, q;\n\t}"
+          : "=r"(done)
+          : "r"(bar)
+          : "memory");
+  }
+  const uint32_t t = p.t_dev ? *p.t_dev + p.t : p.t;
+  const int tid = threadIdx.x;
+  const int64_t wc = w0 + 2 * tid;
+  unsigned long long obs_up = 0, obs_anti = 0;
+  for (int rr = 0; rr < nrows; ++rr) {
+    const int r = ra + rr;
+    const int64_t gi = p.row0 + r;
+    const bool west = ((gi & 1) == 0) == (p.colour == 0);
+    const uint64_t n0 = tile[rr][2 * tid], n1 = tile[rr][2 * tid + 1];
+    const uint64_t c0 = tile[rr + 1][2 * tid], c1 = tile[rr + 1][2 * tid + 1];
+    const uint64_t s0 = tile[rr + 2][2 * tid], s1 = tile[rr + 2][2 * tid + 1];
+    uint64_t side0, side1;
+    if (west) {
+      const uint64_t wl = tid == 0 ? edge[rr + 1][0] : tile[rr + 1][2 * tid - 1];
+      side0 = (c0 << 4) | (wl >> 60);
+      side1 = (c1 << 4) | (c0 >> 60);
+    } else {
+      const uint64_t er = tid == 127 ? edge[rr + 1][1] : tile[rr + 1][2 * tid + 2];
+      side0 = (c0 >> 4) | (c1 << 60);
+      side1 = (c1 >> 4) | (er << 60);
+    }
+    uint64_t* tp = tgt + (int64_t)r * W + wc;
+    ulonglong2 tv = *reinterpret_cast<const ulonglong2*>(tp);
+    const uint32_t ctr0 = (uint32_t)(4 * wc);
+    tv.x = update_word<RULE>(tv.x, n0, c0, s0, side0, ctr0, (uint32_t)gi, t, p);
+    tv.y = update_word<RULE>(tv.y, n1, c1, s1, side1, ctr0 + 4, (uint32_t)gi, t, p);
+    *reinterpret_cast<ulonglong2*>(tp) = tv;
+    if (r == 0 && p.halo_up) *reinterpret_cast<ulonglong2*>(p.halo_up + wc) = tv;
+    if (r == p.R - 1 && p.halo_dn) *reinterpret_cast<ulonglong2*>(p.halo_dn + wc) = tv;
+    if (OBS) {  // same fused observables as k_halfsweep (white phase of a measured sweep)
+      obs_up += __popcll(tv.x) + __popcll(tv.y) + __popcll(c0) + __popcll(c1);
+      obs_anti += __popcll(tv.x ^ n0) + __popcll(tv.x ^ c0) + __popcll(tv.x ^ s0) +
+                  __popcll(tv.x ^ side0) + __popcll(tv.y ^ n1) + __popcll(tv.y ^ c1) +
+                  __popcll(tv.y ^ s1) + __popcll(tv.y ^ side1);
+    }
+  }
+  if (OBS) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      obs_up += __shfl_xor_sync(0xffffffffu, obs_up, off);
+      obs_anti += __shfl_xor_sync(0xffffffffu, obs_anti, off);
+    }
+    if ((threadIdx.x & 31) == 0 && (obs_up | obs_anti)) {
+      atomicAdd(&p.obs_out[0], obs_up);
+      atomicAdd(&p.obs_out[1], obs_anti);
+    }
+  }
+  if (p.signal_up) {  // rank-p2p: the last block publishes "phase done" to both neighbours
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned int prev = atomicAdd(p.done_counter, 1u);
+      if (prev == gridDim.x - 1) {
+        *p.done_counter = 0;
+        __threadfence_system();
+        st_release_sys(p.signal_up, p.signal_value);
+        st_release_sys(p.signal_dn, p.signal_value);
+      }
+    }
+  }
+}
+
+cudaError_t launch_halfsweep_staged(int rule, cudaStream_t st, const HalfSweepParams& p) {
+  const int64_t rows = p.r_end - p.r_begin;
+  const int64_t grid = (p.W / kStageWords) * ((rows + kStageRows - 1) / kStageRows);
+  const bool obs = p.obs_out != nullptr;
+  if (rule == 0)
+    obs ? k_halfsweep_staged<0, true><<<(unsigned)grid, 128, 0, st>>>(p)
+        : k_halfsweep_staged<0><<<(unsigned)grid, 128, 0, st>>>(p);
+  else if (rule == 2)
+    obs ? k_halfsweep_staged<2, true><<<(unsigned)grid, 128, 0, st>>>(p)
+        : k_halfsweep_staged<2><<<(unsigned)grid, 128, 0, st>>>(p);
+  else if (rule == 3)
+    obs ? k_halfsweep_staged<3, true><<<(unsigned)grid, 128, 0, st>>>(p)
+        : k_halfsweep_staged<3><<<(unsigned)grid, 128, 0, st>>>(p);
+  else
+    obs ? k_halfsweep_staged<1, true><<<(unsigned)grid, 128, 0, st>>>(p)
+        : k_halfsweep_staged<1><<<(unsigned)grid, 128, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------- persistent sweeps
 // Small lattices are launch-bound (a 2048^2 half-sweep is ~1.5 us of work).  One
 // cooperative launch runs n whole sweeps: every block of the (co-resident) grid walks its

@@ -163,6 +163,7 @@ cudaError_t launch_basic_convert(int grid, cudaStream_t st, int8_t* black, int8_
 
 // Host-side launchers (defined in ising_kernels.cu).
 cudaError_t launch_sync(cudaStream_t st, const SyncParams& p);
+cudaError_t launch_halfsweep_staged(int rule, cudaStream_t st, const HalfSweepParams& p);
 cudaError_t launch_persistent(int rule, int grid, cudaStream_t st, const PersistentParams& P);
 cudaError_t persistent_occupancy(int* blocks_per_sm);
 cudaError_t launch_set_u32(cudaStream_t st, uint32_t* dst, uint32_t v, int add);

@@ -158,6 +158,7 @@ struct ising_ctx {
   bool graphs_enabled = true;
   bool persistent_enabled = false;         // opt-in (ISING_PERSISTENT=1): measured slower
                                            // than graph replay on B200 (grid barrier ~3 us)
+  bool staged = true;                      // TMA-staged half-sweep (ISING_STAGED=0: off)
   unsigned int* bar = nullptr;             // persistent kernel's grid barrier state
   int persist_blocks_per_sm = 0;
   // basic byte-per-spin layout (ising_create_basic; §3.1)
@@ -371,7 +372,10 @@ int run_halfsweep(ising_ctx* h, Slab& s, int c, int r_begin, int r_end, uint64_t
   }
   const bool prof = h->profiling && s.devi == 0;
   if (prof) CU(cudaEventRecord(h->prof_events[2 * h->kernel_launches], d.stream));
-  CU(launch_halfsweep(kernel_variant(h), grid, d.stream, p));
+  if (h->staged && h->W % 256 == 0)
+    CU(launch_halfsweep_staged(kernel_variant(h), d.stream, p));
+  else
+    CU(launch_halfsweep(kernel_variant(h), grid, d.stream, p));
   if (prof) {
     CU(cudaEventRecord(h->prof_events[2 * h->kernel_launches + 1], d.stream));
     ++h->kernel_launches;
@@ -622,6 +626,8 @@ int create_local(ising_t* out, int64_t N, int64_t M, uint64_t seed, int n_slabs,
   if (env) h->rows_per_item_override = atoi(env);
   const char* genv = getenv("ISING_GRAPHS");
   if (genv && genv[0] == '0') h->graphs_enabled = false;
+  const char* senv = getenv("ISING_STAGED");
+  if (senv && senv[0] == '0') h->staged = false;
   const char* penv = getenv("ISING_PERSISTENT");
   if (penv && penv[0] == '1') h->persistent_enabled = true;
   *out = h;

@@ -277,3 +277,32 @@ def test_persistent_kernel_path(monkeypatch):
     g.sweep(5)
     o.sweep(5)
     assert_same(g, o, "persistent heat bath")
+
+
+def test_tma_staged_kernel_path():
+    # widths that are a multiple of 256 words use the TMA-staged half-sweep (cp.async.bulk
+    # + mbarrier into shared memory): ragged last band (40 = 16 + 16 + 8 rows), two slabs,
+    # heat bath, measured chain
+    for N, M, slabs in [(40, 8192, None), (64, 16384, [0, 0]), (34, 8192, None)]:
+        g = gpu_lattice(N, M, 2, "random", 0.4406868, devices=slabs)
+        o = oracle_lattice(N, M, 2, "random", 0.4406868)
+        for n in [1, 3]:
+            g.sweep(n)
+            o.sweep(n)
+            assert_same(g, o, f"staged {N}x{M} t={o.t}")
+        g.set_beta(0.3, ising.RULE_HEATBATH)
+        o.set_beta(0.3, oracle.RULE_HEATBATH)
+        ups, Es = g.measure(3, 2)
+        ou, oE = o.chain(6)
+        assert np.array_equal(ups, ou[1::2]) and np.array_equal(Es, oE[1::2])
+        assert_same(g, o, f"staged heat bath {N}x{M}")
+
+
+def test_register_rolling_path_on_wide_lattice(monkeypatch):
+    # ISING_STAGED=0 keeps the register-rolling kernel on widths the staged one would take
+    monkeypatch.setenv("ISING_STAGED", "0")
+    g = gpu_lattice(40, 8192, 3, "random", 0.4406868)
+    o = oracle_lattice(40, 8192, 3, "random", 0.4406868)
+    g.sweep(2)
+    o.sweep(2)
+    assert_same(g, o, "register rolling 40x8192")
