@@ -177,7 +177,8 @@ int ising_last_sweep_ms(ising_t h, double* device_ms);
 /* Per-launch timing of the half-sweep kernels of the last ising_sweep when
  * profiling is enabled (ising_set_profiling(h, 1)): *kernel_ms = summed CUDA-event
  * duration of the half-sweep launches on the first device's stream, *launches = how
- * many.  Profiling adds one event pair per launch. */
+ * many (at most the first 4096 launches of the call are timed).  Profiling adds one
+ * event pair per timed launch and disables graph replay. */
 int ising_set_profiling(ising_t h, int enable);
 int ising_kernel_stats(ising_t h, double* kernel_ms, int64_t* launches);
 

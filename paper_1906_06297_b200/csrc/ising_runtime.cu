@@ -81,7 +81,8 @@ constexpr size_t kStagingBytes = size_t(64) << 20;  // pack/unpack staging chunk
 #define ISING_VPT 1
 #endif
 constexpr int64_t kWordsPerItem = 2 * ISING_VPT;  // must match the kernel's kWords
-constexpr size_t kSyncBytes = 4096;                  // rank-p2p flags + gather area
+constexpr size_t kSyncBytes = 4096;
+constexpr int64_t kMaxProfiledLaunches = 4096;  // profiling times the first launches of a call                  // rank-p2p flags + gather area
 constexpr uint32_t kIpcMagic = 0x49534e47u;           // "ISNG"
 
 struct IpcBlob {  // ising_ipc_handle payload (<= ISING_IPC_BLOB_BYTES)
@@ -370,7 +371,7 @@ int run_halfsweep(ising_ctx* h, Slab& s, int c, int r_begin, int r_end, uint64_t
     p.signal_value = h->phase + 1;
     p.done_counter = h->done_counter;
   }
-  const bool prof = h->profiling && s.devi == 0;
+  const bool prof = h->profiling && s.devi == 0 && h->kernel_launches < kMaxProfiledLaunches;
   if (prof) CU(cudaEventRecord(h->prof_events[2 * h->kernel_launches], d.stream));
   if (h->staged && h->W % 256 == 0)
     CU(launch_halfsweep_staged(kernel_variant(h), d.stream, p));
@@ -827,7 +828,7 @@ int basic_enqueue_sweeps(ising_ctx* h, int64_t n) {
       for (int a = 0; a < 5; ++a) p.thr[a] = h->acc.thr[a];
       p.always_mask = h->acc.always_mask;
       p.keys = h->keys;
-      const bool prof = h->profiling;
+      const bool prof = h->profiling && h->kernel_launches < kMaxProfiledLaunches;
       if (prof) CU(cudaEventRecord(h->prof_events[2 * h->kernel_launches], d.stream));
       CU(launch_basic_halfsweep(rule, grid, d.stream, p));
       if (prof) {
@@ -1216,7 +1217,7 @@ int ising_sweep(ising_t h, int64_t n) {
   if (h->t + (uint64_t)n > 0xffffffffull) return ISING_ERR_RANGE;
   if (h->profiling) {
     const size_t per_phase = std::max<size_t>(3, h->slabs.size());
-    const size_t need = (size_t)n * 2 * 2 * per_phase;
+    const size_t need = std::min<size_t>((size_t)n * 2 * 2 * per_phase, 2 * kMaxProfiledLaunches);
     if (!h->devs.empty()) CU(cudaSetDevice(h->devs[0].dev));
     while (h->prof_events.size() < need) {
       cudaEvent_t e;
