@@ -1,0 +1,44 @@
+/* Plain-C use of the library (no Python, no PyTorch): the calls the north_star lists.
+ *   ising_c_example L_rows L_cols seed beta sweeps   ->  prints "up E t"
+ * Built by __graft_entry__.build(); tests/test_gpu_capi.py runs it against the oracle. */
+#include <stdio.h>
+#include <stdlib.h>
+
+#include "ising.h"
+
+#define CHECK(call)                                                                   \
+  do {                                                                                \
+    int st_ = (call);                                                                 \
+    if (st_ != ISING_OK) {                                                            \
+      fprintf(stderr, "%s -> %s: %s\n", #call, ising_strerror(st_), ising_last_error()); \
+      return 1;                                                                       \
+    }                                                                                 \
+  } while (0)
+
+int main(int argc, char** argv) {
+  if (argc != 6) {
+    fprintf(stderr, "usage: %s L_rows L_cols seed beta sweeps\n", argv[0]);
+    return 2;
+  }
+  const int64_t N = atoll(argv[1]), M = atoll(argv[2]);
+  const uint64_t seed = strtoull(argv[3], NULL, 10);
+  const double beta = atof(argv[4]);
+  const int64_t sweeps = atoll(argv[5]);
+  ising_t h = NULL;
+  CHECK(ising_create(&h, N, M, seed, 1));
+  CHECK(ising_set_beta(h, beta));
+  CHECK(ising_init_random(h));
+  CHECK(ising_sweep(h, sweeps));
+  int64_t up = 0, E = 0;
+  CHECK(ising_observables(h, &up, &E));
+  int8_t* lat = (int8_t*)malloc((size_t)(N * M));
+  CHECK(ising_read_lattice(h, lat, N * M));
+  uint64_t t = 0;
+  CHECK(ising_get_sweep(h, &t));
+  long long sum = 0;
+  for (int64_t k = 0; k < N * M; ++k) sum += lat[k];
+  printf("%lld %lld %llu %lld\n", (long long)up, (long long)E, (unsigned long long)t, sum);
+  free(lat);
+  CHECK(ising_destroy(h));
+  return 0;
+}

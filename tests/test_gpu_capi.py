@@ -1,0 +1,25 @@
+"""The C ABI from a plain C program (examples/ising_c_example.c, built by
+__graft_entry__.build()): no Python or PyTorch on the path, results equal the oracle."""
+import os
+import subprocess
+
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+EXE = os.path.join(ROOT, "examples", "ising_c_example")
+
+
+@pytest.mark.parametrize("N,M,seed,beta,sweeps", [(64, 64, 1, 0.4406868, 100), (130, 192, 7, 0.3, 65)])
+def test_c_program_matches_oracle(N, M, seed, beta, sweeps):
+    if not os.path.exists(EXE):
+        pytest.fail("examples/ising_c_example missing: run __graft_entry__.build()")
+    out = subprocess.run([EXE, str(N), str(M), str(seed), repr(beta), str(sweeps)],
+                         capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stderr
+    up, E, t, total = (int(x) for x in out.stdout.split())
+    o = oracle.Lattice(N, M, seed).init_random().set_beta(beta).sweep(sweeps)
+    assert (up, E) == o.observables()
+    assert t == sweeps and total == int(o.full().sum())
