@@ -410,8 +410,9 @@ __global__ void __launch_bounds__(128, ISING_MINB) k_halfsweep(const HalfSweepPa
       obs_anti += __shfl_xor_sync(0xffffffffu, obs_anti, off);
     }
     if ((threadIdx.x & 31) == 0 && (obs_up | obs_anti)) {
-      atomicAdd(&p.obs_out[0], obs_up);
-      atomicAdd(&p.obs_out[1], obs_anti);
+      unsigned long long* o = p.obs_out + (p.slot_dev ? 2 * (size_t)*p.slot_dev : 0);
+      atomicAdd(&o[0], obs_up);
+      atomicAdd(&o[1], obs_anti);
     }
   }
   if (p.signal_up) {  // rank-p2p: the last block publishes "phase done" to both neighbours
@@ -590,8 +591,9 @@ __global__ void __launch_bounds__(128, ISING_MINB) k_halfsweep_staged(const Half
       obs_anti += __shfl_xor_sync(0xffffffffu, obs_anti, off);
     }
     if ((threadIdx.x & 31) == 0 && (obs_up | obs_anti)) {
-      atomicAdd(&p.obs_out[0], obs_up);
-      atomicAdd(&p.obs_out[1], obs_anti);
+      unsigned long long* o = p.obs_out + (p.slot_dev ? 2 * (size_t)*p.slot_dev : 0);
+      atomicAdd(&o[0], obs_up);
+      atomicAdd(&o[1], obs_anti);
     }
   }
   if (p.signal_up) {  // rank-p2p: the last block publishes "phase done" to both neighbours

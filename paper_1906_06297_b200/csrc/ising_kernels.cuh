@@ -65,6 +65,7 @@ struct HalfSweepParams {
   // white phase of a measured sweep: add [up count, antiparallel bonds] of the resulting
   // state into obs_out[0..1] (null: no measurement)
   unsigned long long* obs_out;
+  const uint32_t* slot_dev;  // graph replays: device-resident sample index added to obs_out
 };
 
 // Persistent multi-sweep kernel for small lattices (one slab, one device).

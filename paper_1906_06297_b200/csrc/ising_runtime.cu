@@ -156,6 +156,9 @@ struct ising_ctx {
   cudaGraphExec_t gexec = nullptr;
   uint32_t* t_dev = nullptr;               // device-resident sweep base read by the kernels
   int64_t graph_launches = 0;              // kernel nodes per graph replay
+  cudaGraphExec_t gexec_meas = nullptr;    // measured-chain graph (ising_sweep_measure)
+  int64_t meas_every = 0, meas_samples = 0, meas_graph_launches = 0;
+  unsigned long long* meas_base = nullptr;
   bool graphs_enabled = true;
   bool persistent_enabled = false;         // opt-in (ISING_PERSISTENT=1): measured slower
                                            // than graph replay on B200 (grid barrier ~3 us)
@@ -309,6 +312,7 @@ void destroy_ctx(ising_ctx* h) {
   for (int c = 0; c < 2; ++c)
     if (h->bplane[c]) cudaFree(h->bplane[c]);
   if (h->t_dev) cudaFree(h->t_dev);
+  if (h->gexec_meas) cudaGraphExecDestroy(h->gexec_meas);
   if (h->bar) cudaFree(h->bar);
   delete h;
 }
@@ -340,7 +344,7 @@ int kernel_variant(const ising_ctx* h) {
 
 int run_halfsweep(ising_ctx* h, Slab& s, int c, int r_begin, int r_end, uint64_t* halo_up,
                      uint64_t* halo_dn, uint32_t t, bool t_from_dev = false,
-                     unsigned long long* obs = nullptr) {
+                     unsigned long long* obs = nullptr, bool slot_from_dev = false) {
   if (r_end <= r_begin) return ISING_OK;
   Device& d = h->devs[s.devi];
   HalfSweepParams p{};
@@ -358,6 +362,7 @@ int run_halfsweep(ising_ctx* h, Slab& s, int c, int r_begin, int r_end, uint64_t
   p.t = t;
   p.t_dev = t_from_dev ? h->t_dev : nullptr;
   p.obs_out = obs;
+  p.slot_dev = (obs && slot_from_dev) ? h->t_dev + 1 : nullptr;
   p.colour = (uint32_t)c;
   p.keys = h->keys;
   p.acc = h->acc;
@@ -396,7 +401,7 @@ int sync_all(ising_ctx* h) {
 
 // One colour phase, LOCAL mode.
 int phase_local(ising_ctx* h, int c, uint32_t t, bool t_from_dev = false,
-                const std::vector<unsigned long long*>* obs = nullptr) {
+                const std::vector<unsigned long long*>* obs = nullptr, bool slot_from_dev = false) {
   const int n = (int)h->slabs.size();
   const bool multi_dev = h->devs.size() > 1;
   if (multi_dev) {
@@ -422,7 +427,7 @@ int phase_local(ising_ctx* h, int c, uint32_t t, bool t_from_dev = false,
     // local row 0 -> upper slab's bottom halo (padded row R+1); local row R-1 -> lower
     // slab's top halo (padded row 0).
     TRY(run_halfsweep(h, s, c, 0, (int)s.R, up.plane[c] + (up.R + 1) * h->W, dn.plane[c], t,
-                      t_from_dev, (obs && c == 1) ? (*obs)[s.devi] : nullptr));
+                      t_from_dev, (obs && c == 1) ? (*obs)[s.devi] : nullptr, slot_from_dev));
   }
   if (multi_dev) {
     for (auto& d : h->devs) {
@@ -537,7 +542,7 @@ bool graph_eligible(const ising_ctx* h) {
 int build_graph(ising_ctx* h) {
   Device& d = h->devs[0];
   CU(cudaSetDevice(d.dev));
-  if (!h->t_dev) CU(cudaMalloc(&h->t_dev, sizeof(uint32_t)));
+  if (!h->t_dev) CU(cudaMalloc(&h->t_dev, 2 * sizeof(uint32_t)));  // [sweep base, sample base]
   if (h->gexec) {
     CU(cudaGraphExecDestroy(h->gexec));
     h->gexec = nullptr;
@@ -558,6 +563,46 @@ int build_graph(ising_ctx* h) {
   CU(e);
   h->graph_launches = h->launch_count - before + 1;
   h->launch_count = before;
+  return ISING_OK;
+}
+
+// Measured-chain graph: S = max(1, kGraphSweeps / every) samples of `every` sweeps each,
+// the white phase of each sample's last sweep reducing its observables into slot
+// (sample base + k) of `base`; the last nodes advance the sweep and sample bases.
+int build_measure_graph(ising_ctx* h, int64_t every, unsigned long long* base) {
+  Device& d = h->devs[0];
+  CU(cudaSetDevice(d.dev));
+  if (!h->t_dev) CU(cudaMalloc(&h->t_dev, 2 * sizeof(uint32_t)));
+  if (h->gexec_meas) {
+    CU(cudaGraphExecDestroy(h->gexec_meas));
+    h->gexec_meas = nullptr;
+  }
+  const int64_t S = std::max<int64_t>(1, kGraphSweeps / every);
+  const int64_t before = h->launch_count;
+  cudaGraph_t g = nullptr;
+  CU(cudaStreamBeginCapture(d.stream, cudaStreamCaptureModeThreadLocal));
+  int st = ISING_OK;
+  for (int64_t k = 0; k < S && st == ISING_OK; ++k) {
+    std::vector<unsigned long long*> slot(1, base + 2 * k);
+    for (int64_t sw = 1; sw <= every && st == ISING_OK; ++sw)
+      for (int c = 0; c < 2 && st == ISING_OK; ++c)
+        st = phase_local(h, c, (uint32_t)(k * every + sw), true, sw == every ? &slot : nullptr, true);
+  }
+  cudaError_t e = launch_set_u32(d.stream, h->t_dev, (uint32_t)(S * every), 1);
+  cudaError_t e1 = launch_set_u32(d.stream, h->t_dev + 1, (uint32_t)S, 1);
+  cudaError_t e2 = cudaStreamEndCapture(d.stream, &g);
+  if (st != ISING_OK) return st;
+  CU(e);
+  CU(e1);
+  CU(e2);
+  e = cudaGraphInstantiate(&h->gexec_meas, g, 0);
+  cudaGraphDestroy(g);
+  CU(e);
+  h->meas_graph_launches = h->launch_count - before + 2;
+  h->launch_count = before;
+  h->meas_every = every;
+  h->meas_base = base;
+  h->meas_samples = S;
   return ISING_OK;
 }
 
@@ -1107,6 +1152,10 @@ int ising_set_rule(ising_t h, int rule) {
     cudaGraphExecDestroy(h->gexec);
     h->gexec = nullptr;
   }
+  if (h->gexec_meas) {
+    cudaGraphExecDestroy(h->gexec_meas);
+    h->gexec_meas = nullptr;
+  }
   if (h->beta_set) return ising_set_beta(h, h->beta);
   return ISING_OK;
 }
@@ -1117,6 +1166,10 @@ int ising_set_beta(ising_t h, double beta) {
   if (h->gexec) {
     cudaGraphExecDestroy(h->gexec);
     h->gexec = nullptr;
+  }
+  if (h->gexec_meas) {
+    cudaGraphExecDestroy(h->gexec_meas);
+    h->gexec_meas = nullptr;
   }
   compute_thresholds(beta, h->rule, h->T);
   h->acc.always_mask = 0;
@@ -1429,7 +1482,24 @@ int ising_sweep_measure(ising_t h, int64_t n_samples, int64_t every, int64_t* up
   if (n_samples > 0 && persistent_eligible(h)) {
     TRY(run_persistent(h, n_samples * every, base[0], every));  // the whole chain, one launch
   } else {
-    for (int64_t k = 0; k < n_samples; ++k) {
+    int64_t k0 = 0;
+    const int64_t S = std::max<int64_t>(1, kGraphSweeps / every);
+    if (graph_eligible(h) && every <= kGraphSweeps && n_samples >= S) {
+      if (!h->gexec_meas || h->meas_every != every || h->meas_base != base[0])
+        TRY(build_measure_graph(h, every, base[0]));
+      Device& d = h->devs[0];
+      CU(launch_set_u32(d.stream, h->t_dev, (uint32_t)h->t, 0));
+      CU(launch_set_u32(d.stream, h->t_dev + 1, 0u, 0));
+      h->launch_count += 2;
+      const int64_t reps = n_samples / S;
+      for (int64_t r = 0; r < reps; ++r) {
+        CU(cudaGraphLaunch(h->gexec_meas, d.stream));
+        h->launch_count += h->meas_graph_launches;
+      }
+      h->t += (uint64_t)(reps * S * every);
+      k0 = reps * S;
+    }
+    for (int64_t k = k0; k < n_samples; ++k) {
       for (size_t d = 0; d < base.size(); ++d) slot[d] = base[d] + 2 * k;
       TRY(enqueue_sweeps(h, every, &slot));  // observables fused into the last white phase
     }

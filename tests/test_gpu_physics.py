@@ -65,10 +65,14 @@ def test_measured_chain_matches_oracle_series():
     # ising_sweep_measure's device-side series equals the oracle chain sample by sample
     import oracle
 
-    for N, M, every, slabs in [(64, 64, 1, None), (128, 192, 7, None), (96, 128, 3, [0, 0, 0])]:
+    # (small lattices replay measured-chain graphs of 64 // every samples; the plans mix
+    # replays and remainders, and a second call reuses the graph)
+    for N, M, every, slabs, ns in [(64, 64, 1, None, 40), (64, 64, 1, None, 200),
+                                   (128, 192, 7, None, 40), (96, 128, 3, [0, 0, 0], 40)]:
         g = IsingLattice(N, M, 4, devices=slabs).set_beta(0.4406868).init_random()
         o = oracle.Lattice(N, M, 4).set_beta(0.4406868).init_random()
-        ups, Es = g.measure(40, every)
-        ou, oE = o.chain(40 * every)
-        assert np.array_equal(ups, ou[every - 1::every]) and np.array_equal(Es, oE[every - 1::every])
-        assert g.t == o.t == 40 * every
+        for _ in range(2):
+            ups, Es = g.measure(ns, every)
+            ou, oE = o.chain(ns * every)
+            assert np.array_equal(ups, ou[every - 1::every]) and np.array_equal(Es, oE[every - 1::every])
+            assert g.t == o.t
