@@ -171,9 +171,27 @@ def cpu_baseline(cols: int) -> dict:
     rate, cores, dt = oracle_rate(rows, cols, 1)
     sweeps = max(1, min(256, int(12.0 / max(dt, 1e-3))))
     rate, cores, dt = oracle_rate(rows, cols, sweeps)
+    import oracle
+
+    # the same oracle on one thread (per-core rate), on a quarter of the rows
+    r1, _, dt1 = oracle_rate(rows // 4, cols, 1, threads=1)
+    oracle.set_threads(cores)
     return {"value": rate, "unit": "flips/ns", "cores": cores, "kind": "oracle",
+            "per_core_value": r1, "cpu_model": cpu_model(),
             "sample": f"{rows}x{cols} torus (C3 row width), beta={BETA}, random start seed {SEED}, "
-                      f"{sweeps} sweeps, {dt:.1f} s, OpenMP over rows of a colour phase"}
+                      f"{sweeps} sweeps, {dt:.1f} s, OpenMP over rows of a colour phase; "
+                      f"per-core: {rows // 4}x{cols}, 1 sweep, 1 thread, {dt1:.1f} s"}
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def run_reference(args):
