@@ -12,10 +12,16 @@
 //     slab's halo row (same device, or a peer device over NVLink P2P), and each
 //     phase waits on the neighbours' previous phase (RAW on the halo it reads, WAR
 //     on the halo it writes).
+//   RANK-P2P (ising_create_rank_p2p, the default of bench.py --gpus N): one process
+//     per GPU; the neighbours' planes and flag words are mapped through CUDA IPC, the
+//     half-sweep kernel stores its boundary rows into the neighbours' halo rows over
+//     NVLink, waits for / raises phase flags in peer memory (prologue / last block).
 //   RANK (ising_create_rank): one process per GPU; per phase the two boundary
 //     rows are updated first, then ncclSend/ncclRecv move them on a comm stream
 //     while the interior rows update (the classic halo/bulk overlap the paper cites,
 //     PAPER.md:224).
+// Small single-device lattices replay CUDA graphs (plain and measured chains); the basic
+// byte-per-spin layout (ising_create_basic, §3.1) has its own kernels.
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -81,8 +87,8 @@ constexpr size_t kStagingBytes = size_t(64) << 20;  // pack/unpack staging chunk
 #define ISING_VPT 1
 #endif
 constexpr int64_t kWordsPerItem = 2 * ISING_VPT;  // must match the kernel's kWords
-constexpr size_t kSyncBytes = 4096;
-constexpr int64_t kMaxProfiledLaunches = 4096;  // profiling times the first launches of a call                  // rank-p2p flags + gather area
+constexpr size_t kSyncBytes = 4096;                   // rank-p2p flags + gather area
+constexpr int64_t kMaxProfiledLaunches = 4096;        // profiling times the first launches
 constexpr uint32_t kIpcMagic = 0x49534e47u;           // "ISNG"
 
 struct IpcBlob {  // ising_ipc_handle payload (<= ISING_IPC_BLOB_BYTES)
