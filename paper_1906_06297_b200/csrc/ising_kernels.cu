@@ -155,6 +155,22 @@ __device__ __forceinline__ uint64_t update_word<2>(uint64_t tgt, uint64_t n, uin
   return update_word_metropolis<2>(tgt, n, c, s, side, ctr0, row, t, p);
 }
 
+// RULE 4: Metropolis with both thresholds in {0, 2^32} (beta = inf: zero-temperature
+// quench; beta = 0): the acceptance no longer depends on the draw, and with a counter-
+// based generator skipping a draw changes nothing else, so no Philox is evaluated.
+// nc = [r >= T3] + [r >= T4] is the per-launch constant p.acc.nc_const.
+template <>
+__device__ __forceinline__ uint64_t update_word<4>(uint64_t tgt, uint64_t n, uint64_t c, uint64_t s,
+                                                   uint64_t side, uint32_t ctr0, uint32_t row, uint32_t t,
+                                                   const HalfSweepParams& p) {
+  const uint32_t sum_lo = (uint32_t)n + (uint32_t)c + (uint32_t)s + (uint32_t)side;
+  const uint32_t sum_hi =
+      (uint32_t)(n >> 32) + (uint32_t)(c >> 32) + (uint32_t)(s >> 32) + (uint32_t)(side >> 32);
+  const uint32_t lo = accept8((uint32_t)tgt, sum_lo, p.acc.nc_const);
+  const uint32_t hi = accept8((uint32_t)(tgt >> 32), sum_hi, p.acc.nc_const);
+  return ((uint64_t)hi << 32) | lo;
+}
+
 // Heat bath, fast path (all five thresholds < 2^32, i.e. any finite beta < ~4.6): the
 // Horner accumulator counts nc = #{m : r >= T[m]} per lane on the carry chain (one madc
 // and four addc per lane), and since T is non-increasing in a, r < T[a] <=> a + nc <= 4.
@@ -615,7 +631,10 @@ cudaError_t launch_halfsweep_staged(int rule, cudaStream_t st, const HalfSweepPa
   const int64_t rows = p.r_end - p.r_begin;
   const int64_t grid = (p.W / kStageWords) * ((rows + kStageRows - 1) / kStageRows);
   const bool obs = p.obs_out != nullptr;
-  if (rule == 0)
+  if (rule == 4)
+    obs ? k_halfsweep_staged<4, true><<<(unsigned)grid, 128, 0, st>>>(p)
+        : k_halfsweep_staged<4><<<(unsigned)grid, 128, 0, st>>>(p);
+  else if (rule == 0)
     obs ? k_halfsweep_staged<0, true><<<(unsigned)grid, 128, 0, st>>>(p)
         : k_halfsweep_staged<0><<<(unsigned)grid, 128, 0, st>>>(p);
   else if (rule == 2)
@@ -732,7 +751,9 @@ cudaError_t launch_philox_probe(int grid, cudaStream_t st, const PhiloxKeys& K,
 
 cudaError_t launch_halfsweep(int rule, int grid, cudaStream_t st, const HalfSweepParams& p) {
   if (p.obs_out) {  // measured white phase (Metropolis fast path or heat bath fast path)
-    if (rule == 0)
+    if (rule == 4)
+      k_halfsweep<4, true><<<grid, 128, 0, st>>>(p);
+    else if (rule == 0)
       k_halfsweep<0, true><<<grid, 128, 0, st>>>(p);
     else if (rule == 2)
       k_halfsweep<2, true><<<grid, 128, 0, st>>>(p);
@@ -740,6 +761,10 @@ cudaError_t launch_halfsweep(int rule, int grid, cudaStream_t st, const HalfSwee
       k_halfsweep<3, true><<<grid, 128, 0, st>>>(p);
     else
       k_halfsweep<1, true><<<grid, 128, 0, st>>>(p);
+    return cudaGetLastError();
+  }
+  if (rule == 4) {
+    k_halfsweep<4><<<grid, 128, 0, st>>>(p);
     return cudaGetLastError();
   }
   if (rule == 0)

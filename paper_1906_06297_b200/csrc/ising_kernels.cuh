@@ -33,6 +33,7 @@ struct Accept {
   uint32_t thr[5];
   uint32_t always_mask;
   uint32_t keep3, keep4;  // Metropolis: 0 if T[a=3] / T[a=4] is 2^32, else ~0
+  uint32_t nc_const;      // RULE 4: [r >= T3] + [r >= T4] per lane (draw-independent)
 };
 
 struct HalfSweepParams {

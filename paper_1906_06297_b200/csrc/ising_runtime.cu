@@ -169,6 +169,7 @@ struct ising_ctx {
   bool persistent_enabled = false;         // opt-in (ISING_PERSISTENT=1): measured slower
                                            // than graph replay on B200 (grid barrier ~3 us)
   bool staged = true;                      // TMA-staged half-sweep (ISING_STAGED=0: off)
+  bool draw_free_enabled = true;           // beta in {0, inf}: skip Philox (ISING_DRAW_FREE=0)
   unsigned int* bar = nullptr;             // persistent kernel's grid barrier state
   int persist_blocks_per_sm = 0;
   // basic byte-per-spin layout (ising_create_basic; §3.1)
@@ -344,7 +345,12 @@ void halfsweep_geometry(const ising_ctx* h, const Device& d, int64_t rows, int* 
 // 2 = Metropolis generic (tiny beta), 3 = heat bath with all thresholds < 2^32 (the fast
 // path), 1 = heat bath generic
 int kernel_variant(const ising_ctx* h) {
-  if (h->rule == ISING_RULE_METROPOLIS) return (h->acc.keep3 & h->acc.keep4) ? 0 : 2;
+  if (h->rule == ISING_RULE_METROPOLIS) {
+    const bool t3_fixed = h->T[3] == 0 || h->T[3] == (uint64_t(1) << 32);
+    const bool t4_fixed = h->T[4] == 0 || h->T[4] == (uint64_t(1) << 32);
+    if (t3_fixed && t4_fixed && h->draw_free_enabled) return 4;  // no draw needed
+    return (h->acc.keep3 & h->acc.keep4) ? 0 : 2;
+  }
   return (h->acc.always_mask == 0) ? 3 : 1;
 }
 
@@ -678,6 +684,8 @@ int create_local(ising_t* out, int64_t N, int64_t M, uint64_t seed, int n_slabs,
   if (env) h->rows_per_item_override = atoi(env);
   const char* genv = getenv("ISING_GRAPHS");
   if (genv && genv[0] == '0') h->graphs_enabled = false;
+  const char* denv = getenv("ISING_DRAW_FREE");
+  if (denv && denv[0] == '0') h->draw_free_enabled = false;
   const char* senv = getenv("ISING_STAGED");
   if (senv && senv[0] == '0') h->staged = false;
   const char* penv = getenv("ISING_PERSISTENT");
@@ -1180,6 +1188,7 @@ int ising_set_beta(ising_t h, double beta) {
   compute_thresholds(beta, h->rule, h->T);
   h->acc.always_mask = 0;
   h->acc.keep3 = h->acc.keep4 = 0xffffffffu;
+  h->acc.nc_const = 0;
   for (int a = 0; a < 5; ++a) {
     if (h->T[a] >= (uint64_t(1) << 32)) {
       h->acc.always_mask |= 1u << a;
@@ -1190,6 +1199,8 @@ int ising_set_beta(ising_t h, double beta) {
       h->acc.thr[a] = (uint32_t)h->T[a];
     }
   }
+  // draw-free Metropolis (beta = 0 or inf): T = 0 contributes one "no flip" per class
+  h->acc.nc_const = (h->T[3] == 0 ? 0x11111111u : 0u) + (h->T[4] == 0 ? 0x11111111u : 0u);
   h->beta_set = true;
   return ISING_OK;
 }

@@ -18,7 +18,8 @@ C5_ROWS_PER_GPU, C5_COLS = 131072, 1048576
 # parity matrix: W = 2 (both side words wrap inside one chunk),
 # odd chunk count and non power of two rows (130 x 192), non-square.
 PARITY_SHAPES = [(64, 64), (66, 64), (64, 128), (130, 192), (256, 256), (2, 64)]
-PARITY_BETAS = [0.0, 0.2, BETA_TC, 0.8, math.inf]
+# 4e-11: T3 = 2^32 ("always") while T4 = 2^32 - 1, the generic kernel with mixed keep masks
+PARITY_BETAS = [0.0, 0.2, BETA_TC, 0.8, math.inf, 4e-11]
 PARITY_SEEDS = [1, 2]
 
 # (rows, cols, slabs): R = 2 (every row a boundary row), 2 slabs (up = down peer)

@@ -8,7 +8,8 @@ from paper_1906_06297_b200.ising import IsingLattice  # noqa: E402
 
 N = M = 32768
 lat = IsingLattice(N, M, 1).init_random()
-for name, beta, rule in [("metropolis fast", 0.4406868, 0), ("metropolis generic (beta=0)", 0.0, 0),
+for name, beta, rule in [("metropolis fast", 0.4406868, 0), ("metropolis generic (beta=4e-11)", 4e-11, 0),
+                         ("metropolis draw-free (beta=inf)", math.inf, 0), ("metropolis draw-free (beta=0)", 0.0, 0),
                          ("heat bath fast", 0.4406868, 1), ("heat bath generic (beta=inf)", math.inf, 1)]:
     lat.set_beta(beta, rule)
     lat.sweep(4)
