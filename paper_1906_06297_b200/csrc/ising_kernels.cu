@@ -8,6 +8,7 @@
 //   k_pack / k_unpack  +-1 byte full lattice <-> packed planes (row a9).
 //
 // All arithmetic is integer.  Nothing here is shared with oracle/.
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include "ising_kernels.cuh"
@@ -171,25 +172,51 @@ __device__ __forceinline__ uint64_t update_word<4>(uint64_t tgt, uint64_t n, uin
   return ((uint64_t)hi << 32) | lo;
 }
 
-// Heat bath, fast path (all five thresholds < 2^32, i.e. any finite beta < ~4.6): the
-// Horner accumulator counts nc = #{m : r >= T[m]} per lane on the carry chain (one madc
-// and four addc per lane), and since T is non-increasing in a, r < T[a] <=> a + nc <= 4.
-// With B = a + 3 from classify's SWAR form, x = B + nc <= 12 and flip <=> bit 3 of x clear.
-template <int K>
+// Heat bath, fast path.  The Horner accumulator counts nc = #{m : r >= T[m]} per lane on
+// the carry chain (one madc and an addc per further class), and since T is non-increasing
+// in a, r < T[a] <=> a + nc <= 4.  With B = a + 3 from classify's SWAR form, x = B + nc <= 12
+// and flip <=> bit 3 of x clear.  NA = number of "always" classes (T = 2^32, a prefix of the
+// non-increasing T: none for beta < ~2.77, a = 0 up to ~5.5, a = 0, 1 beyond; T[2] = 2^31
+// always): [r >= 2^32] = 0 for those, so their compares are simply left out.
+template <int NA>
 __device__ __forceinline__ void hb_step(uint32_t& acc, uint32_t r, const uint32_t* T) {
-  asm("{\n\t.reg .u32 d;\n\t"
-      "sub.cc.u32 d, %1, %2;\n\t"
-      "madc.lo.u32 %0, %0, 16, 0;\n\t"
-      "sub.cc.u32 d, %1, %3;\n\t"
-      "addc.u32 %0, %0, 0;\n\t"
-      "sub.cc.u32 d, %1, %4;\n\t"
-      "addc.u32 %0, %0, 0;\n\t"
-      "sub.cc.u32 d, %1, %5;\n\t"
-      "addc.u32 %0, %0, 0;\n\t"
-      "sub.cc.u32 d, %1, %6;\n\t"
-      "addc.u32 %0, %0, 0;\n\t}"
-      : "+r"(acc)
-      : "r"(r), "r"(T[0]), "r"(T[1]), "r"(T[2]), "r"(T[3]), "r"(T[4]));
+  static_assert(NA >= 0 && NA <= 2, "T[2] = 2^31 is never 'always'");
+  if constexpr (NA == 0)
+    asm("{\n\t.reg .u32 d;\n\t"
+        "sub.cc.u32 d, %1, %2;\n\t"
+        "madc.lo.u32 %0, %0, 16, 0;\n\t"
+        "sub.cc.u32 d, %1, %3;\n\t"
+        "addc.u32 %0, %0, 0;\n\t"
+        "sub.cc.u32 d, %1, %4;\n\t"
+        "addc.u32 %0, %0, 0;\n\t"
+        "sub.cc.u32 d, %1, %5;\n\t"
+        "addc.u32 %0, %0, 0;\n\t"
+        "sub.cc.u32 d, %1, %6;\n\t"
+        "addc.u32 %0, %0, 0;\n\t}"
+        : "+r"(acc)
+        : "r"(r), "r"(T[0]), "r"(T[1]), "r"(T[2]), "r"(T[3]), "r"(T[4]));
+  else if constexpr (NA == 1)
+    asm("{\n\t.reg .u32 d;\n\t"
+        "sub.cc.u32 d, %1, %2;\n\t"
+        "madc.lo.u32 %0, %0, 16, 0;\n\t"
+        "sub.cc.u32 d, %1, %3;\n\t"
+        "addc.u32 %0, %0, 0;\n\t"
+        "sub.cc.u32 d, %1, %4;\n\t"
+        "addc.u32 %0, %0, 0;\n\t"
+        "sub.cc.u32 d, %1, %5;\n\t"
+        "addc.u32 %0, %0, 0;\n\t}"
+        : "+r"(acc)
+        : "r"(r), "r"(T[1]), "r"(T[2]), "r"(T[3]), "r"(T[4]));
+  else
+    asm("{\n\t.reg .u32 d;\n\t"
+        "sub.cc.u32 d, %1, %2;\n\t"
+        "madc.lo.u32 %0, %0, 16, 0;\n\t"
+        "sub.cc.u32 d, %1, %3;\n\t"
+        "addc.u32 %0, %0, 0;\n\t"
+        "sub.cc.u32 d, %1, %4;\n\t"
+        "addc.u32 %0, %0, 0;\n\t}"
+        : "+r"(acc)
+        : "r"(r), "r"(T[2]), "r"(T[3]), "r"(T[4]));
 }
 
 __device__ __forceinline__ uint32_t hb_accept8(uint32_t s, uint32_t n, uint32_t nc) {
@@ -199,10 +226,11 @@ __device__ __forceinline__ uint32_t hb_accept8(uint32_t s, uint32_t n, uint32_t 
   return s ^ ((~x >> 3) & kLane0);
 }
 
-template <>
-__device__ __forceinline__ uint64_t update_word<3>(uint64_t tgt, uint64_t n, uint64_t c, uint64_t s,
-                                                   uint64_t side, uint32_t ctr0, uint32_t row, uint32_t t,
-                                                   const HalfSweepParams& p) {
+template <int NA>
+__device__ __forceinline__ uint64_t update_word_heatbath(uint64_t tgt, uint64_t n, uint64_t c,
+                                                         uint64_t s, uint64_t side, uint32_t ctr0,
+                                                         uint32_t row, uint32_t t,
+                                                         const HalfSweepParams& p) {
   const uint32_t sum_lo = (uint32_t)n + (uint32_t)c + (uint32_t)s + (uint32_t)side;
   const uint32_t sum_hi =
       (uint32_t)(n >> 32) + (uint32_t)(c >> 32) + (uint32_t)(s >> 32) + (uint32_t)(side >> 32);
@@ -210,32 +238,44 @@ __device__ __forceinline__ uint64_t update_word<3>(uint64_t tgt, uint64_t n, uin
   uint32_t lo = 0, hi = 0;
   {
     const uint4 r1 = philox4x32_10(t, ctr0 + 1, p.colour, row, p.keys);
-    hb_step<7>(lo, r1.w, T);
-    hb_step<6>(lo, r1.z, T);
-    hb_step<5>(lo, r1.y, T);
-    hb_step<4>(lo, r1.x, T);
+    hb_step<NA>(lo, r1.w, T);
+    hb_step<NA>(lo, r1.z, T);
+    hb_step<NA>(lo, r1.y, T);
+    hb_step<NA>(lo, r1.x, T);
     const uint4 r0 = philox4x32_10(t, ctr0 + 0, p.colour, row, p.keys);
-    hb_step<3>(lo, r0.w, T);
-    hb_step<2>(lo, r0.z, T);
-    hb_step<1>(lo, r0.y, T);
-    hb_step<0>(lo, r0.x, T);
+    hb_step<NA>(lo, r0.w, T);
+    hb_step<NA>(lo, r0.z, T);
+    hb_step<NA>(lo, r0.y, T);
+    hb_step<NA>(lo, r0.x, T);
   }
   {
     const uint4 r3 = philox4x32_10(t, ctr0 + 3, p.colour, row, p.keys);
-    hb_step<15>(hi, r3.w, T);
-    hb_step<14>(hi, r3.z, T);
-    hb_step<13>(hi, r3.y, T);
-    hb_step<12>(hi, r3.x, T);
+    hb_step<NA>(hi, r3.w, T);
+    hb_step<NA>(hi, r3.z, T);
+    hb_step<NA>(hi, r3.y, T);
+    hb_step<NA>(hi, r3.x, T);
     const uint4 r2 = philox4x32_10(t, ctr0 + 2, p.colour, row, p.keys);
-    hb_step<11>(hi, r2.w, T);
-    hb_step<10>(hi, r2.z, T);
-    hb_step<9>(hi, r2.y, T);
-    hb_step<8>(hi, r2.x, T);
+    hb_step<NA>(hi, r2.w, T);
+    hb_step<NA>(hi, r2.z, T);
+    hb_step<NA>(hi, r2.y, T);
+    hb_step<NA>(hi, r2.x, T);
   }
   const uint32_t flo = hb_accept8((uint32_t)tgt, sum_lo, lo);
   const uint32_t fhi = hb_accept8((uint32_t)(tgt >> 32), sum_hi, hi);
   return ((uint64_t)fhi << 32) | flo;
 }
+
+#define ISING_HB_RULE(RULE, NA)                                                                  \
+  template <>                                                                                   \
+  __device__ __forceinline__ uint64_t update_word<RULE>(                                        \
+      uint64_t tgt, uint64_t n, uint64_t c, uint64_t s, uint64_t side, uint32_t ctr0,           \
+      uint32_t row, uint32_t t, const HalfSweepParams& p) {                                     \
+    return update_word_heatbath<NA>(tgt, n, c, s, side, ctr0, row, t, p);                       \
+  }
+ISING_HB_RULE(3, 0)  // RULE 3: every T < 2^32
+ISING_HB_RULE(5, 1)  // RULE 5: T[0] = 2^32
+ISING_HB_RULE(6, 2)  // RULE 6: T[0] = T[1] = 2^32
+#undef ISING_HB_RULE
 
 // Heat bath, generic (some threshold is 2^32): flip iff r < T[a] for every class.
 // T is non-increasing in a, so "r < T[a]" <=> a < #{m : r < T[m]}.
@@ -267,6 +307,27 @@ __device__ __forceinline__ uint64_t update_word<1>(uint64_t tgt, uint64_t n, uin
     }
   }
   return tgt ^ flip;
+}
+
+// Host-side rule dispatch shared by every launcher: f(integral_constant<int, RULE>,
+// bool_constant<OBS>).  An unknown rule is an error, never a silent fallback.
+template <typename F>
+static cudaError_t dispatch_rule(int rule, bool obs, F&& f) {
+#define ISING_RULE_CASE(R)                                                       \
+  case R:                                                                        \
+    return obs ? f(std::integral_constant<int, R>{}, std::true_type{})           \
+               : f(std::integral_constant<int, R>{}, std::false_type{});
+  switch (rule) {
+    ISING_RULE_CASE(0)
+    ISING_RULE_CASE(1)
+    ISING_RULE_CASE(2)
+    ISING_RULE_CASE(3)
+    ISING_RULE_CASE(4)
+    ISING_RULE_CASE(5)
+    ISING_RULE_CASE(6)
+  }
+#undef ISING_RULE_CASE
+  return cudaErrorInvalidValue;
 }
 
 // One colour phase of one slab.  Work item = (band of H rows, 128-bit chunk
@@ -629,24 +690,11 @@ __global__ void __launch_bounds__(128, ISING_MINB) k_halfsweep_staged(const Half
 
 cudaError_t launch_halfsweep_staged(int rule, cudaStream_t st, const HalfSweepParams& p) {
   const int64_t rows = p.r_end - p.r_begin;
-  const int64_t grid = (p.W / kStageWords) * ((rows + kStageRows - 1) / kStageRows);
-  const bool obs = p.obs_out != nullptr;
-  if (rule == 4)
-    obs ? k_halfsweep_staged<4, true><<<(unsigned)grid, 128, 0, st>>>(p)
-        : k_halfsweep_staged<4><<<(unsigned)grid, 128, 0, st>>>(p);
-  else if (rule == 0)
-    obs ? k_halfsweep_staged<0, true><<<(unsigned)grid, 128, 0, st>>>(p)
-        : k_halfsweep_staged<0><<<(unsigned)grid, 128, 0, st>>>(p);
-  else if (rule == 2)
-    obs ? k_halfsweep_staged<2, true><<<(unsigned)grid, 128, 0, st>>>(p)
-        : k_halfsweep_staged<2><<<(unsigned)grid, 128, 0, st>>>(p);
-  else if (rule == 3)
-    obs ? k_halfsweep_staged<3, true><<<(unsigned)grid, 128, 0, st>>>(p)
-        : k_halfsweep_staged<3><<<(unsigned)grid, 128, 0, st>>>(p);
-  else
-    obs ? k_halfsweep_staged<1, true><<<(unsigned)grid, 128, 0, st>>>(p)
-        : k_halfsweep_staged<1><<<(unsigned)grid, 128, 0, st>>>(p);
-  return cudaGetLastError();
+  const unsigned grid = (unsigned)((p.W / kStageWords) * ((rows + kStageRows - 1) / kStageRows));
+  return dispatch_rule(rule, p.obs_out != nullptr, [&](auto R, auto O) {
+    k_halfsweep_staged<decltype(R)::value, decltype(O)::value><<<grid, 128, 0, st>>>(p);
+    return cudaGetLastError();
+  });
 }
 
 // ------------------------------------------------------- persistent sweeps
@@ -715,13 +763,9 @@ static cudaError_t coop_launch(int grid, cudaStream_t st, const PersistentParams
 }
 
 cudaError_t launch_persistent(int rule, int grid, cudaStream_t st, const PersistentParams& P) {
-  const bool obs = P.obs_base != nullptr;
-  switch (rule) {
-    case 0: return obs ? coop_launch<0, true>(grid, st, P) : coop_launch<0, false>(grid, st, P);
-    case 2: return obs ? coop_launch<2, true>(grid, st, P) : coop_launch<2, false>(grid, st, P);
-    case 3: return obs ? coop_launch<3, true>(grid, st, P) : coop_launch<3, false>(grid, st, P);
-    default: return obs ? coop_launch<1, true>(grid, st, P) : coop_launch<1, false>(grid, st, P);
-  }
+  return dispatch_rule(rule, P.obs_base != nullptr, [&](auto R, auto O) {
+    return coop_launch<decltype(R)::value, decltype(O)::value>(grid, st, P);
+  });
 }
 
 cudaError_t persistent_occupancy(int* blocks_per_sm) {
@@ -750,32 +794,10 @@ cudaError_t launch_philox_probe(int grid, cudaStream_t st, const PhiloxKeys& K,
 }
 
 cudaError_t launch_halfsweep(int rule, int grid, cudaStream_t st, const HalfSweepParams& p) {
-  if (p.obs_out) {  // measured white phase (Metropolis fast path or heat bath fast path)
-    if (rule == 4)
-      k_halfsweep<4, true><<<grid, 128, 0, st>>>(p);
-    else if (rule == 0)
-      k_halfsweep<0, true><<<grid, 128, 0, st>>>(p);
-    else if (rule == 2)
-      k_halfsweep<2, true><<<grid, 128, 0, st>>>(p);
-    else if (rule == 3)
-      k_halfsweep<3, true><<<grid, 128, 0, st>>>(p);
-    else
-      k_halfsweep<1, true><<<grid, 128, 0, st>>>(p);
+  return dispatch_rule(rule, p.obs_out != nullptr, [&](auto R, auto O) {
+    k_halfsweep<decltype(R)::value, decltype(O)::value><<<grid, 128, 0, st>>>(p);
     return cudaGetLastError();
-  }
-  if (rule == 4) {
-    k_halfsweep<4><<<grid, 128, 0, st>>>(p);
-    return cudaGetLastError();
-  }
-  if (rule == 0)
-    k_halfsweep<0><<<grid, 128, 0, st>>>(p);
-  else if (rule == 2)
-    k_halfsweep<2><<<grid, 128, 0, st>>>(p);
-  else if (rule == 3)
-    k_halfsweep<3><<<grid, 128, 0, st>>>(p);
-  else
-    k_halfsweep<1><<<grid, 128, 0, st>>>(p);
-  return cudaGetLastError();
+  });
 }
 
 cudaError_t halfsweep_occupancy(int* blocks_per_sm) {

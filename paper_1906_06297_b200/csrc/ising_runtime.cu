@@ -342,8 +342,8 @@ void halfsweep_geometry(const ising_ctx* h, const Device& d, int64_t rows, int* 
 }
 
 // kernel variant: 0 = Metropolis with both thresholds < 2^32 (the fast path),
-// 2 = Metropolis generic (tiny beta), 3 = heat bath with all thresholds < 2^32 (the fast
-// path), 1 = heat bath generic
+// 2 = Metropolis generic (tiny beta), 4 = Metropolis draw-free (T3, T4 in {0, 2^32});
+// heat bath 3 / 5 / 6 = fast path with 0 / 1 / 2 "always" classes (T = 2^32), 1 = generic
 int kernel_variant(const ising_ctx* h) {
   if (h->rule == ISING_RULE_METROPOLIS) {
     const bool t3_fixed = h->T[3] == 0 || h->T[3] == (uint64_t(1) << 32);
@@ -351,7 +351,12 @@ int kernel_variant(const ising_ctx* h) {
     if (t3_fixed && t4_fixed && h->draw_free_enabled) return 4;  // no draw needed
     return (h->acc.keep3 & h->acc.keep4) ? 0 : 2;
   }
-  return (h->acc.always_mask == 0) ? 3 : 1;
+  switch (h->acc.always_mask) {  // the "always" classes form a prefix of the non-increasing T
+    case 0: return 3;
+    case 1: return 5;
+    case 3: return 6;
+    default: return 1;  // not reachable from compute_thresholds; kept exact anyway
+  }
 }
 
 int run_halfsweep(ising_ctx* h, Slab& s, int c, int r_begin, int r_end, uint64_t* halo_up,

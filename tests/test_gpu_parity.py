@@ -89,7 +89,9 @@ def test_virtual_slabs_match_oracle(N, M, nslab):
 
 
 def test_heatbath_parity():
-    for N, M, beta in [(64, 64, 0.4406868), (66, 128, 0.2), (32, 64, math.inf), (32, 64, 0.0)]:
+    # beta 3.0: T[0] = 2^32 (variant 5); 6.0 and inf: T[0] = T[1] = 2^32 (variant 6)
+    for N, M, beta in [(64, 64, 0.4406868), (66, 128, 0.2), (32, 64, math.inf), (32, 64, 0.0),
+                       (64, 128, 3.0), (66, 64, 6.0), (32, 64, 2.5)]:
         g = gpu_lattice(N, M, 5, "random", beta, ising.RULE_HEATBATH)
         o = oracle_lattice(N, M, 5, "random", beta, oracle.RULE_HEATBATH)
         assert g.thresholds() == [int(x) for x in o_thresholds(beta, oracle.RULE_HEATBATH)]
@@ -277,6 +279,15 @@ def test_persistent_kernel_path(monkeypatch):
     g.sweep(5)
     o.sweep(5)
     assert_same(g, o, "persistent heat bath")
+    # every kernel variant through the persistent dispatcher: draw-free Metropolis (beta
+    # inf), generic Metropolis (tiny beta), heat bath with 1 and 2 "always" classes
+    for beta, rule in [(math.inf, ising.RULE_METROPOLIS), (4e-11, ising.RULE_METROPOLIS),
+                       (3.0, ising.RULE_HEATBATH), (6.0, ising.RULE_HEATBATH)]:
+        g.set_beta(beta, rule)
+        o.set_beta(beta, rule)
+        g.sweep(3)
+        o.sweep(3)
+        assert_same(g, o, f"persistent beta={beta} rule={rule}")
 
 
 def test_tma_staged_kernel_path():
@@ -296,6 +307,12 @@ def test_tma_staged_kernel_path():
         ou, oE = o.chain(6)
         assert np.array_equal(ups, ou[1::2]) and np.array_equal(Es, oE[1::2])
         assert_same(g, o, f"staged heat bath {N}x{M}")
+        for beta in [3.0, math.inf]:  # heat bath variants 5 and 6 in the staged kernel
+            g.set_beta(beta, ising.RULE_HEATBATH)
+            o.set_beta(beta, oracle.RULE_HEATBATH)
+            g.sweep(2)
+            o.sweep(2)
+            assert_same(g, o, f"staged heat bath {N}x{M} beta={beta}")
 
 
 def test_register_rolling_path_on_wide_lattice(monkeypatch):

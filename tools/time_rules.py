@@ -1,4 +1,4 @@
-"""C3 flips/ns for each kernel variant: Metropolis (fast / generic) and heat bath (fast / generic)."""
+"""C3 flips/ns for each kernel variant: Metropolis (fast / generic) and heat bath (0 / 1 / 2 "always" classes)."""
 import math
 import os
 import sys
@@ -10,7 +10,8 @@ N = M = 32768
 lat = IsingLattice(N, M, 1).init_random()
 for name, beta, rule in [("metropolis fast", 0.4406868, 0), ("metropolis generic (beta=4e-11)", 4e-11, 0),
                          ("metropolis draw-free (beta=inf)", math.inf, 0), ("metropolis draw-free (beta=0)", 0.0, 0),
-                         ("heat bath fast", 0.4406868, 1), ("heat bath generic (beta=inf)", math.inf, 1)]:
+                         ("heat bath fast", 0.4406868, 1), ("heat bath T0=2^32 (beta=3)", 3.0, 1),
+                         ("heat bath T0=T1=2^32 (beta=inf)", math.inf, 1)]:
     lat.set_beta(beta, rule)
     lat.sweep(4)
     lat.sweep(16)
