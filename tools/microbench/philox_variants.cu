@@ -3,6 +3,8 @@
 //   wide : hi/lo via one IMAD.WIDE.U32 (FMA-heavy pipe, 4 cycles per warp)
 //   dfma : hi via DFMA.RZ on the FP64 pipe (2^52 magic), lo via IMAD
 //   mix  : per round, product 0 via IMAD.WIDE and product 1 via DFMA + IMAD
+//   hi/lo: hi via mul.hi.u32 (IMAD.HI, one FMA-heavy pass) and lo via an IMAD that ptxas
+//          cannot fuse with it (c * (M - 1) + c), so the pair is not an IMAD.WIDE
 // Each thread runs 4 independent blocks per iteration (the half-sweep's ILP).
 #include <cstdio>
 #include <cstdint>
@@ -45,6 +47,29 @@ __device__ __forceinline__ uint4 philox_flow(uint32_t c0, uint32_t c1, uint32_t 
 template <int V>
 __device__ __forceinline__ uint4 philox(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, const Keys& K,
                                         double mp0, double cc0, double mp1, double cc1) {
+  if (V >= 6) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+      uint32_t hi0, lo0, hi1, lo1;
+      if (V == 6) {
+        hi0 = __umulhi(c0, M0); lo0 = c0 * M0; hi1 = __umulhi(c2, M1); lo1 = c2 * M1;
+      } else if (V == 7) {
+        asm("mul.hi.u32 %0, %1, %2;" : "=r"(hi0) : "r"(c0), "n"(M0));
+        asm("mad.lo.u32 %0, %1, %2, %1;" : "=r"(lo0) : "r"(c0), "n"(M0 - 1));
+        asm("mul.hi.u32 %0, %1, %2;" : "=r"(hi1) : "r"(c2), "n"(M1));
+        asm("mad.lo.u32 %0, %1, %2, %1;" : "=r"(lo1) : "r"(c2), "n"(M1 - 1));
+      } else {
+        asm("mul.hi.u32 %0, %1, %2;" : "=r"(hi0) : "r"(c0), "n"(M0));
+        asm volatile("mul.lo.u32 %0, %1, %2;" : "=r"(lo0) : "r"(c0), "n"(M0));
+        asm("mul.hi.u32 %0, %1, %2;" : "=r"(hi1) : "r"(c2), "n"(M1));
+        asm volatile("mul.lo.u32 %0, %1, %2;" : "=r"(lo1) : "r"(c2), "n"(M1));
+      }
+      const uint32_t n0 = hi1 ^ c1 ^ K.k0[r];
+      const uint32_t n2 = hi0 ^ c3 ^ K.k1[r];
+      c1 = lo1; c3 = lo0; c0 = n0; c2 = n2;
+    }
+    return make_uint4(c0, c1, c2, c3);
+  }
   if (V == 3) return philox_flow(c0, c1, c2, c3, K, mp0, cc0, mp1, cc1);
   if (V == 4) return philox<0>(c0, c1, c2, c3, K, mp0, cc0, mp1, cc1);
   if (V == 5) {
@@ -119,11 +144,11 @@ int main() {
   const double cc1 = 4503599627370496.0 - 1048576.0 * (double)M1;
   const int grid = sms * 16, threads = 128;
   const uint32_t iters = 256;
-  uint32_t* out[6];
-  for (int v = 0; v < 6; ++v) CK(cudaMalloc(&out[v], sizeof(uint32_t) * grid * threads));
+  uint32_t* out[9];
+  for (int v = 0; v < 9; ++v) CK(cudaMalloc(&out[v], sizeof(uint32_t) * grid * threads));
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
-  const char* names[6] = {"wide", "dfma", "mix", "flow", "wide+flow", "wide(param M)"};
-  for (int v = 0; v < 6; ++v) {
+  const char* names[9] = {"wide", "dfma", "mix", "flow", "wide+flow", "wide(param M)", "umulhi+mul", "hi+mad(M-1)", "hi+lo asm"};
+  for (int v = 0; v < 9; ++v) {
     float best = 1e30f;
     for (int rep = 0; rep < 5; ++rep) {
       cudaEventRecord(a);
@@ -133,6 +158,9 @@ int main() {
       if (v == 3) k_philox<3><<<grid, threads>>>(K, iters, 7, 3, mp0, cc0, mp1, cc1, out[v]);
       if (v == 4) k_philox<4><<<grid, threads>>>(K, iters, 7, 3, mp0, cc0, mp1, cc1, out[v]);
       if (v == 5) k_philox<5><<<grid, threads>>>(K, iters, 7, 3, mp0, cc0, mp1, cc1, out[v]);
+      if (v == 6) k_philox<6><<<grid, threads>>>(K, iters, 7, 3, mp0, cc0, mp1, cc1, out[v]);
+      if (v == 7) k_philox<7><<<grid, threads>>>(K, iters, 7, 3, mp0, cc0, mp1, cc1, out[v]);
+      if (v == 8) k_philox<8><<<grid, threads>>>(K, iters, 7, 3, mp0, cc0, mp1, cc1, out[v]);
       cudaEventRecord(b); CK(cudaEventSynchronize(b)); CK(cudaGetLastError());
       float ms; cudaEventElapsedTime(&ms, a, b); if (rep && ms < best) best = ms;
     }
@@ -140,11 +168,11 @@ int main() {
     printf("philox %-5s: %.3f ms  %.0f draws/ns\n", names[v], best, draws / (best * 1e6));
   }
   // correctness: all variants fold to the same values
-  uint32_t* h = new uint32_t[6 * grid * threads];
-  for (int v = 0; v < 6; ++v) CK(cudaMemcpy(h + v * grid * threads, out[v], 4 * grid * threads, cudaMemcpyDeviceToHost));
+  uint32_t* h = new uint32_t[9 * grid * threads];
+  for (int v = 0; v < 9; ++v) CK(cudaMemcpy(h + v * grid * threads, out[v], 4 * grid * threads, cudaMemcpyDeviceToHost));
   int bad = 0;
   for (int i = 0; i < grid * threads; ++i)
-    for (int v = 1; v < 6; ++v) bad += (h[i] != h[v * grid * threads + i]);
+    for (int v = 1; v < 9; ++v) bad += (h[i] != h[v * grid * threads + i]);
   printf("variants agree: %s (%d mismatches)\n", bad ? "NO" : "yes", bad);
   double* dout; CK(cudaMalloc(&dout, sizeof(double) * grid * threads));
   for (int rep = 0; rep < 3; ++rep) {
