@@ -6,8 +6,10 @@
 A step is one full sweep (black + white half-sweep) of the whole lattice.  N = 1 runs
 BASELINE.json configs[2] (C3: 32768 x 32768, beta = 0.4406868, random start, seed 1).
 N > 1 (launched by torch.distributed.run, one process per GPU) weak-scales C3: each
-rank owns a 32768 x 32768 slab of an (N*32768) x 32768 lattice and exchanges halo rows
-with ncclSend/ncclRecv ("scaling": "weak").  --config c4 strong-scales 131072^2,
+rank owns a 32768 x 32768 slab of an (N*32768) x 32768 lattice; the half-sweep kernel
+stores its boundary rows into the neighbours' halo rows through CUDA-IPC peer pointers and
+signals them with flags in peer memory (rank-p2p; ncclSend/ncclRecv if peer mapping is
+unavailable — config.transport says which) ("scaling": "weak").  --config c4 strong-scales 131072^2,
 --config c5 weak-scales 131072 x 1048576 per GPU.
 
 value: flips/ns over the K timed sweeps, device-timed with CUDA events on the launching
@@ -421,6 +423,7 @@ def run_ours(args):
                 "seed": SEED,
                 "start": "random",
                 "parallelism": f"slab{n}",
+                "transport": getattr(lat, "transport", "single") if n > 1 else "single",
                 "layout": "basic byte/spin (PAPER.md §3.1)" if basic else "multi-spin 4 bit/spin (PAPER.md §3.3)",
                 "l2": f"inputs larger than L2: packed planes {N * M // 2 / 2**20:.0f} MiB per "
                       f"{'GPU' if n == 1 else 'lattice'} vs 126 MB L2; no flush",

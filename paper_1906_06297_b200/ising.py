@@ -323,7 +323,9 @@ class IsingLattice:
             oks = [None] * world
             dist.all_gather_object(oks, ok[0])
             if all(oks):
-                return cls(L_rows, L_cols, seed, _handle=h)
+                lat = cls(L_rows, L_cols, seed, _handle=h)
+                lat.transport = "p2p"
+                return lat
             if h is not None:
                 ising_destroy(h)
             import warnings
@@ -337,7 +339,9 @@ class IsingLattice:
             h = ising_create_rank(L_rows, L_cols, seed, rank, world, device, obj[0])
         else:
             raise ValueError(f"unknown transport {transport!r}")
-        return cls(L_rows, L_cols, seed, _handle=h)
+        lat = cls(L_rows, L_cols, seed, _handle=h)
+        lat.transport = "nccl"
+        return lat
 
     def close(self):
         if getattr(self, "h", None):
