@@ -5,11 +5,17 @@
 // wrap, and the same draw contract / integer thresholds as the multi-spin path, so both
 // layouts are bit-identical to each other and to the oracle.
 //
-// B200 choices: a thread owns four consecutive plane sites (one Philox4x32-10 block, one
-// 32-bit load/store per row of target and source) instead of the listing's one thread per
-// spin with a pre-generated random array: same arithmetic per site,
-// no random-number array in HBM, 3 algorithmic bytes per attempted flip.
+// B200 choices (default kernel): a thread owns 16 consecutive plane sites (four Philox4x32-10
+// blocks, 128-bit loads / stores) of a band of rows, keeps the source rows above / at /
+// below in registers as it walks down, and evaluates the listing's stencil and acceptance
+// on four byte lanes per 32-bit word (SWAR) instead of site by site; no random-number array
+// in HBM (the paper pre-generates one): 3 algorithmic bytes per attempted
+// flip.  The listing-shaped kernel (a thread per four sites, per-site selects) is kept for
+// the layout / kernel-style comparison (ISING_BASIC_LISTING=1) and for widths whose plane
+// rows are not a whole number of 16-byte chunks (L_cols % 32 != 0).
 #include <cuda_runtime.h>
+
+#include <algorithm>
 
 #include "ising_kernels.cuh"
 
@@ -31,11 +37,13 @@ __device__ __forceinline__ uint4 philox_basic(uint32_t c0, uint32_t c1, uint32_t
   return make_uint4(c0, c1, c2, c3);
 }
 
+// ---- listing form (ISING_BASIC_LISTING=1): the Fig. 2 kernel site by site ----
 // One colour phase: lattice (target colour c) and op_lattice (the other colour), both
 // nx x ny int8.  Thread = plane sites (i, 4q .. 4q+3); x covers the quads of a row, y
-// strides over rows (no 64-bit division in the index math).
+// strides over rows (no 64-bit division in the index math).  rule 0 = Metropolis, else
+// heat bath.
 template <int RULE>
-__global__ void __launch_bounds__(256) k_basic_halfsweep(const BasicParams p) {
+__global__ void __launch_bounds__(256) k_basic_listing(const BasicParams p) {
   const int64_t quads = p.ny >> 2;
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= quads) return;
@@ -69,12 +77,12 @@ __global__ void __launch_bounds__(256) k_basic_halfsweep(const BasicParams p) {
       bool always;
       if (RULE == 0) {
         // Metropolis (PAPER.md:40-41, :155-156 with the integer compare of reading R5)
-        thr = (a == 4) ? p.thr[4] : p.thr[3];
-        always = (a <= 2) || ((p.always_mask >> a) & 1u);
+        thr = (a == 4) ? p.acc.thr[4] : p.acc.thr[3];
+        always = (a <= 2) || ((p.acc.always_mask >> a) & 1u);
       } else {
         // heat bath
-        thr = a == 0 ? p.thr[0] : a == 1 ? p.thr[1] : a == 2 ? p.thr[2] : a == 3 ? p.thr[3] : p.thr[4];
-        always = (p.always_mask >> a) & 1u;
+        thr = p.acc.thr[a];
+        always = (p.acc.always_mask >> a) & 1u;
       }
       if (always || rr[k] < thr) s[k] = (int8_t)-s[k];
     }
@@ -83,6 +91,143 @@ __global__ void __launch_bounds__(256) k_basic_halfsweep(const BasicParams p) {
     tv.z = s[2];
     tv.w = s[3];
     *reinterpret_cast<char4*>(p.lattice + i * p.ny + j0) = tv;
+  }
+}
+
+// ---- B200 form (default): byte-lane SWAR, 16 sites per thread, rows rolled in registers ----
+// Per 32-bit word = 4 byte lanes (plane sites j .. j+3, one Philox block, word k = j & 3 ->
+// byte k).  A +-1 byte has bit 1 set iff the spin is -1, so with t the target word,
+//   b2 = sum over the 4 neighbour words of ((nb ^ t) & 0x02020202)
+// is twice the number of anti-aligned neighbours b per lane (<= 8, no carries).  Both rules
+// reduce to "flip iff b >= nc", nc = #{compared classes m : r >= T[m]}: Metropolis compares
+// classes a = 3, 4 (a <= 2 flips), heat bath every class whose T is below 2^32 (r < T[a] <=>
+// a + nc <= 4 for the non-increasing T, a = 4 - b).  x = b2 + 16 - 2 nc lies in [6, 24] per
+// lane and bit 4 of x is the flip bit.  A flip negates the byte: t ^= 0xFE per flipped lane,
+// 0xFE f = (f << 8) - 2 f exactly (mod 2^32) for 0/1 lanes f.
+constexpr uint32_t kByte0 = 0x01010101u;
+constexpr uint32_t kByteDown = 0x02020202u;
+
+__device__ __forceinline__ void horner8(uint32_t& acc, uint32_t r, uint32_t T) {
+  asm("{\n\t.reg .u32 d;\n\t"
+      "sub.cc.u32 d, %1, %2;\n\t"
+      "madc.lo.u32 %0, %0, 256, 0;\n\t}"
+      : "+r"(acc)
+      : "r"(r), "r"(T));
+}
+
+__device__ __forceinline__ void add_carry(uint32_t& acc, uint32_t r, uint32_t T) {
+  asm("{\n\t.reg .u32 d;\n\t"
+      "sub.cc.u32 d, %1, %2;\n\t"
+      "addc.u32 %0, %0, 0;\n\t}"
+      : "+r"(acc)
+      : "r"(r), "r"(T));
+}
+
+// nc per byte lane for one Philox block (lanes 3 .. 0 in Horner order).
+template <int RULE>
+__device__ __forceinline__ uint32_t basic_nc(const uint4 r, const Accept& A) {
+  const uint32_t rr[4] = {r.w, r.z, r.y, r.x};
+  if constexpr (RULE == 4) {
+    return (A.nc_const & 0xFu) * kByte0;  // draw-free (T3, T4 in {0, 2^32})
+  } else if constexpr (RULE == 0 || RULE == 2) {
+    uint32_t a3 = 0, a4 = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      horner8(a3, rr[k], A.thr[3]);
+      horner8(a4, rr[k], A.thr[4]);
+    }
+    if constexpr (RULE == 0) return a3 + a4;
+    return (a3 & A.keep3) + (a4 & A.keep4);  // a class at 2^32 never blocks a flip
+  } else if constexpr (RULE == 3 || RULE == 5 || RULE == 6) {
+    constexpr int NA = RULE == 3 ? 0 : RULE == 5 ? 1 : 2;  // "always" prefix, left out
+    uint32_t acc = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      horner8(acc, rr[k], A.thr[NA]);
+#pragma unroll
+      for (int m = NA + 1; m < 5; ++m) add_carry(acc, rr[k], A.thr[m]);
+    }
+    return acc;
+  } else {  // RULE 1: heat bath with an arbitrary always-mask (not produced by the host)
+    uint32_t nc = 0;
+#pragma unroll
+    for (int m = 0; m < 5; ++m) {
+      uint32_t acc = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) horner8(acc, rr[k], A.thr[m]);
+      nc += ((A.always_mask >> m) & 1u) ? 0u : acc;
+    }
+    return nc;
+  }
+}
+
+__device__ __forceinline__ uint32_t basic_update(uint32_t t, uint32_t n, uint32_t c, uint32_t s,
+                                                 uint32_t side, uint32_t nc) {
+  const uint32_t b2 = ((n ^ t) & kByteDown) + ((c ^ t) & kByteDown) + ((s ^ t) & kByteDown) +
+                      ((side ^ t) & kByteDown);
+  const uint32_t x = b2 + 0x10101010u - (nc << 1);
+  const uint32_t f = (x >> 4) & kByte0;
+  return t ^ ((f << 8) - (f << 1));
+}
+
+__device__ __forceinline__ uint4 ld_u4_nc(const int8_t* p) {
+  return __ldg(reinterpret_cast<const uint4*>(p));
+}
+
+constexpr int kBasicRows = 16;  // rows per work item (source rows reused in registers)
+
+template <int RULE>
+__global__ void __launch_bounds__(128, 4) k_basic_halfsweep(const BasicParams p) {
+  const int64_t chunks = p.ny >> 4;  // 16-byte chunks per plane row
+  const int64_t bands = (p.nx + kBasicRows - 1) / kBasicRows;
+  const int64_t items = chunks * bands;
+  const int8_t* op = p.op_lattice;
+  for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < items;
+       it += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t band = it / chunks;
+    const int64_t q = it - band * chunks;
+    const int64_t j0 = 16 * q;
+    const int64_t i0 = band * kBasicRows;
+    const int64_t i1 = (i0 + kBasicRows < p.nx) ? i0 + kBasicRows : p.nx;
+    // "Set stencil indices with periodicity": rows wrap mod nx
+    uint4 up = ld_u4_nc(op + ((i0 > 0) ? i0 - 1 : p.nx - 1) * p.ny + j0);
+    uint4 mid = ld_u4_nc(op + i0 * p.ny + j0);
+    const int64_t je = (j0 + 16 < p.ny) ? j0 + 16 : 0;  // east edge byte's column
+    const int64_t jw = (j0 > 0) ? j0 - 1 : p.ny - 1;    // west edge byte's column
+    for (int64_t i = i0; i < i1; ++i) {
+      const uint4 dn = ld_u4_nc(op + ((i + 1 < p.nx) ? i + 1 : 0) * p.ny + j0);
+      // off-column neighbour: black odd rows and white even rows
+      // look east (j + 1), the others west (j - 1)
+      const bool east = (p.colour == 0) == ((i & 1) == 1);
+      const uint32_t edge = (uint8_t)__ldg(op + i * p.ny + (east ? je : jw));
+      uint4 side;
+      if (east) {
+        side.x = __funnelshift_r(mid.x, mid.y, 8);
+        side.y = __funnelshift_r(mid.y, mid.z, 8);
+        side.z = __funnelshift_r(mid.z, mid.w, 8);
+        side.w = __funnelshift_r(mid.w, edge, 8);
+      } else {
+        side.x = __funnelshift_l(edge << 24, mid.x, 8);
+        side.y = __funnelshift_l(mid.x, mid.y, 8);
+        side.z = __funnelshift_l(mid.y, mid.z, 8);
+        side.w = __funnelshift_l(mid.z, mid.w, 8);
+      }
+      int8_t* tp = p.lattice + i * p.ny + j0;
+      uint4 t = *reinterpret_cast<const uint4*>(tp);
+      const uint32_t ctr = (uint32_t)(j0 >> 2);  // Philox block of plane site j: j >> 2
+      const uint32_t row = (uint32_t)i;
+      t.x = basic_update(t.x, up.x, mid.x, dn.x, side.x,
+                         basic_nc<RULE>(philox_basic(p.t, ctr + 0, p.colour, row, p.keys), p.acc));
+      t.y = basic_update(t.y, up.y, mid.y, dn.y, side.y,
+                         basic_nc<RULE>(philox_basic(p.t, ctr + 1, p.colour, row, p.keys), p.acc));
+      t.z = basic_update(t.z, up.z, mid.z, dn.z, side.z,
+                         basic_nc<RULE>(philox_basic(p.t, ctr + 2, p.colour, row, p.keys), p.acc));
+      t.w = basic_update(t.w, up.w, mid.w, dn.w, side.w,
+                         basic_nc<RULE>(philox_basic(p.t, ctr + 3, p.colour, row, p.keys), p.acc));
+      *reinterpret_cast<uint4*>(tp) = t;
+      up = mid;
+      mid = dn;
+    }
   }
 }
 
@@ -157,14 +302,31 @@ __global__ void k_basic_convert(int8_t* black, int8_t* white, int8_t* full, int6
   }
 }
 
-cudaError_t launch_basic_halfsweep(int rule, int grid, cudaStream_t st, const BasicParams& p) {
-  (void)grid;
-  const int64_t quads = p.ny >> 2;
-  const dim3 g((unsigned)((quads + 255) / 256), (unsigned)(p.nx < 65535 ? p.nx : 65535));
-  if (rule == 0)
-    k_basic_halfsweep<0><<<g, 256, 0, st>>>(p);
-  else
-    k_basic_halfsweep<1><<<g, 256, 0, st>>>(p);
+cudaError_t launch_basic_halfsweep(int rule, int listing, int sms, cudaStream_t st,
+                                   const BasicParams& p) {
+  if (listing || (p.ny & 15) != 0) {  // the SWAR kernel needs whole 16-byte chunks
+    const int64_t quads = p.ny >> 2;
+    const dim3 g((unsigned)((quads + 255) / 256), (unsigned)(p.nx < 65535 ? p.nx : 65535));
+    const bool metropolis = rule == 0 || rule == 2 || rule == 4;
+    if (metropolis)
+      k_basic_listing<0><<<g, 256, 0, st>>>(p);
+    else
+      k_basic_listing<1><<<g, 256, 0, st>>>(p);
+    return cudaGetLastError();
+  }
+  const int64_t items = (p.ny >> 4) * ((p.nx + kBasicRows - 1) / kBasicRows);
+  const int64_t cap = (int64_t)sms * 4 * 64;  // grid-stride beyond 64 waves
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((items + 127) / 128, cap));
+  switch (rule) {
+    case 0: k_basic_halfsweep<0><<<grid, 128, 0, st>>>(p); break;
+    case 1: k_basic_halfsweep<1><<<grid, 128, 0, st>>>(p); break;
+    case 2: k_basic_halfsweep<2><<<grid, 128, 0, st>>>(p); break;
+    case 3: k_basic_halfsweep<3><<<grid, 128, 0, st>>>(p); break;
+    case 4: k_basic_halfsweep<4><<<grid, 128, 0, st>>>(p); break;
+    case 5: k_basic_halfsweep<5><<<grid, 128, 0, st>>>(p); break;
+    case 6: k_basic_halfsweep<6><<<grid, 128, 0, st>>>(p); break;
+    default: return cudaErrorInvalidValue;
+  }
   return cudaGetLastError();
 }
 

@@ -149,11 +149,13 @@ struct BasicParams {
   const int8_t* op_lattice;  // the other colour
   int64_t nx, ny;
   uint32_t t, colour;
-  uint32_t thr[5];
-  uint32_t always_mask;
+  Accept acc;  // same threshold table / variant flags as the multi-spin path
   PhiloxKeys keys;
 };
-cudaError_t launch_basic_halfsweep(int rule, int grid, cudaStream_t st, const BasicParams& p);
+// rule: kernel variant as for launch_halfsweep (0, 2, 4 Metropolis; 3, 5, 6, 1 heat bath).
+// listing != 0 selects the per-site kernel that mirrors the Fig. 2 listing line by line.
+cudaError_t launch_basic_halfsweep(int rule, int listing, int sms, cudaStream_t st,
+                                   const BasicParams& p);
 cudaError_t launch_basic_init(int grid, cudaStream_t st, int8_t* black, int8_t* white, int64_t nx,
                               int64_t ny, int cold, const PhiloxKeys& keys);
 cudaError_t launch_basic_observables(int grid, cudaStream_t st, const int8_t* black,

@@ -878,8 +878,9 @@ int basic_init(ising_ctx* h, int cold) {
 int basic_enqueue_sweeps(ising_ctx* h, int64_t n) {
   Device& d = h->devs[0];
   const int64_t ny = h->M / 2;
-  const int grid = basic_grid(d, h->N * (ny / 4));
-  const int rule = h->rule == ISING_RULE_METROPOLIS ? 0 : 1;
+  const int rule = kernel_variant(h);
+  const char* listing_env = getenv("ISING_BASIC_LISTING");
+  const int listing = (listing_env && listing_env[0] == '1') ? 1 : 0;
   for (int64_t k = 1; k <= n; ++k) {
     for (int c = 0; c < 2; ++c) {
       BasicParams p{};
@@ -889,12 +890,11 @@ int basic_enqueue_sweeps(ising_ctx* h, int64_t n) {
       p.ny = ny;
       p.t = (uint32_t)(h->t + (uint64_t)k);
       p.colour = (uint32_t)c;
-      for (int a = 0; a < 5; ++a) p.thr[a] = h->acc.thr[a];
-      p.always_mask = h->acc.always_mask;
+      p.acc = h->acc;
       p.keys = h->keys;
       const bool prof = h->profiling && h->kernel_launches < kMaxProfiledLaunches;
       if (prof) CU(cudaEventRecord(h->prof_events[2 * h->kernel_launches], d.stream));
-      CU(launch_basic_halfsweep(rule, grid, d.stream, p));
+      CU(launch_basic_halfsweep(rule, listing, d.sms, d.stream, p));
       if (prof) {
         CU(cudaEventRecord(h->prof_events[2 * h->kernel_launches + 1], d.stream));
         ++h->kernel_launches;
@@ -1052,10 +1052,14 @@ int ising_create_rank_p2p(ising_t* out, int64_t L_rows, int64_t L_cols, uint64_t
   h->slabs.push_back(s);
   st = alloc_slabs(h);
   if (st == ISING_OK) {
+    // zeroed on the handle's (non-blocking) stream and synchronised: a legacy-stream
+    // cudaMemset is not ordered before work on a non-blocking stream
+    cudaStream_t st0 = h->devs[0].stream;
     cudaError_t e = cudaMalloc(&h->sync, kSyncBytes);
-    if (e == cudaSuccess) e = cudaMemset(h->sync, 0, kSyncBytes);
+    if (e == cudaSuccess) e = cudaMemsetAsync(h->sync, 0, kSyncBytes, st0);
     if (e == cudaSuccess) e = cudaMalloc(&h->done_counter, sizeof(unsigned int));
-    if (e == cudaSuccess) e = cudaMemset(h->done_counter, 0, sizeof(unsigned int));
+    if (e == cudaSuccess) e = cudaMemsetAsync(h->done_counter, 0, sizeof(unsigned int), st0);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st0);
     if (e != cudaSuccess) st = fail_cuda(e, "rank-p2p sync buffers", __LINE__);
   }
   if (st != ISING_OK) {
@@ -1093,8 +1097,11 @@ int ising_create_basic(ising_t* out, int64_t L_rows, int64_t L_cols, uint64_t se
   if (st == ISING_OK) {
     const size_t bytes = (size_t)(L_rows * (L_cols / 2));
     for (int c = 0; c < 2 && st == ISING_OK; ++c) {
+      // same stream as every later kernel on these planes (k_basic_init must not race a
+      // legacy-stream memset)
       cudaError_t e = cudaMalloc(&h->bplane[c], bytes);
-      if (e == cudaSuccess) e = cudaMemset(h->bplane[c], 1, bytes);
+      if (e == cudaSuccess) e = cudaMemsetAsync(h->bplane[c], 1, bytes, h->devs[0].stream);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(h->devs[0].stream);
       if (e != cudaSuccess) st = fail_cuda(e, "basic planes", __LINE__);
     }
   }
