@@ -193,6 +193,13 @@ int ising_slab_info(ising_t h, int64_t* row0, int64_t* rows);
  * k = 0..4 (2^32 means "always").  Host-side; for tests and reports. */
 int ising_thresholds(ising_t h, uint64_t T[5]);
 
+/* Half-sweep kernel variant the next sweep runs (for tests and reports; the same numbering
+ * for packed and ising_create_basic handles): 0 Metropolis (both thresholds < 2^32), 2 Metropolis with a threshold at 2^32,
+ * 4 Metropolis draw-free (thresholds in {0, 2^32}: beta = 0 or inf); heat bath 3 / 5 / 6
+ * (0 / 1 / 2 leading thresholds at 2^32, five compares per site), 7 (symmetric thresholds
+ * T[0] + T[4] = T[1] + T[3] = 2^32 + 1 and T[2] = 2^31: two compares per site on |r|), 1 generic. */
+int ising_kernel_variant(ising_t h, int* variant);
+
 /* Number of kernel launches issued by this handle since creation. */
 int ising_launch_count(ising_t h, int64_t* launches);
 

@@ -148,6 +148,20 @@ __device__ __forceinline__ uint32_t basic_nc(const uint4 r, const Accept& A) {
       for (int m = NA + 1; m < 5; ++m) add_carry(acc, rr[k], A.thr[m]);
     }
     return acc;
+  } else if constexpr (RULE == 7) {
+    // symmetric heat bath (ising_kernels.cu, update_word<7>): the Metropolis compare pair on
+    // v = |r| (as int32), and nc = 5 - that count in lanes with r >= 2^31
+    uint32_t a3 = 0, a4 = 0, am = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t v = (uint32_t)abs((int32_t)rr[k]);
+      horner8(a3, v, A.thr[3]);
+      horner8(a4, v, A.thr[4]);
+      am = __funnelshift_l(rr[k], am, 8);  // r's msb -> bit 7 of the new byte
+    }
+    const uint32_t m = (am >> 7) & kByte0;
+    const uint32_t m255 = (m << 8) - m;
+    return ((a3 + a4) ^ m255) - (m255 & 0xFAFAFAFAu);  // m: (255 - c) - 250 = 5 - c
   } else {  // RULE 1: heat bath with an arbitrary always-mask (not produced by the host)
     uint32_t nc = 0;
 #pragma unroll
@@ -325,6 +339,7 @@ cudaError_t launch_basic_halfsweep(int rule, int listing, int sms, cudaStream_t 
     case 4: k_basic_halfsweep<4><<<grid, 128, 0, st>>>(p); break;
     case 5: k_basic_halfsweep<5><<<grid, 128, 0, st>>>(p); break;
     case 6: k_basic_halfsweep<6><<<grid, 128, 0, st>>>(p); break;
+    case 7: k_basic_halfsweep<7><<<grid, 128, 0, st>>>(p); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();

@@ -277,6 +277,67 @@ ISING_HB_RULE(5, 1)  // RULE 5: T[0] = 2^32
 ISING_HB_RULE(6, 2)  // RULE 6: T[0] = T[1] = 2^32
 #undef ISING_HB_RULE
 
+// Heat bath, symmetric fast path (RULE 7).  Applies when the host has verified T[2] = 2^31 and
+// T[0] + T[4] = T[1] + T[3] = 2^32 + 1 — what ceil(2^32 P) gives for P(e) + P(-e) = 1
+// unless 2^32 P(e) lands within rounding of an integer, in which case RULE 3 / 5 / 6 run.
+// With nc = #{m : r >= T[m]} and T non-increasing:
+//   r <  2^31: T[0] >= T[1] > 2^31 > r and r < T[2], so nc = [r >= T3] + [r >= T4];
+//   r >= 2^31: r >= T[2] >= T[3] >= T[4], and with v = 2^32 - r (|r| as int32, in [1, 2^31]),
+//              r >= T[0] <=> v <= 2^32 - T[0] <=> v < T[4] (likewise T[1] / T[3]), so
+//              nc = 3 + (1 - [v >= T4]) + (1 - [v >= T3]) = 5 - ([v >= T3] + [v >= T4]).
+// So every lane needs the Metropolis compare pair on v = |r| plus the msb of r: 6 integer
+// operations per lane instead of 5 compares and 5 inserts.
+__device__ __forceinline__ void hbs_step(uint32_t& a3, uint32_t& a4, uint32_t& am, uint32_t r,
+                                         uint32_t t3, uint32_t t4) {
+  nc_step(a3, a4, (uint32_t)abs((int32_t)r), t3, t4);
+  am = __funnelshift_l(r, am, 4);  // (am << 4) | (r >> 28): r's msb is bit 3 of the new nibble
+}
+
+// nc per lane from the compare pair count c (0..2) and the msb bit of the lane's nibble in am
+__device__ __forceinline__ uint32_t hbs_nc(uint32_t c, uint32_t am) {
+  const uint32_t m = (am >> 3) & kLane0;
+  const uint32_t m15 = (m << 4) - m;  // 0xF in lanes with r >= 2^31
+  return (c ^ m15) - (m15 & 0xAAAAAAAAu);  // m: (15 - c) - 10 = 5 - c; else c (no borrows)
+}
+
+template <>
+__device__ __forceinline__ uint64_t update_word<7>(uint64_t tgt, uint64_t n, uint64_t c, uint64_t s,
+                                                   uint64_t side, uint32_t ctr0, uint32_t row, uint32_t t,
+                                                   const HalfSweepParams& p) {
+  const uint32_t sum_lo = (uint32_t)n + (uint32_t)c + (uint32_t)s + (uint32_t)side;
+  const uint32_t sum_hi =
+      (uint32_t)(n >> 32) + (uint32_t)(c >> 32) + (uint32_t)(s >> 32) + (uint32_t)(side >> 32);
+  const uint32_t t3 = p.acc.thr[3], t4 = p.acc.thr[4];
+  uint32_t a3lo = 0, a4lo = 0, amlo = 0, a3hi = 0, a4hi = 0, amhi = 0;
+  {
+    const uint4 r1 = philox4x32_10(t, ctr0 + 1, p.colour, row, p.keys);
+    hbs_step(a3lo, a4lo, amlo, r1.w, t3, t4);
+    hbs_step(a3lo, a4lo, amlo, r1.z, t3, t4);
+    hbs_step(a3lo, a4lo, amlo, r1.y, t3, t4);
+    hbs_step(a3lo, a4lo, amlo, r1.x, t3, t4);
+    const uint4 r0 = philox4x32_10(t, ctr0 + 0, p.colour, row, p.keys);
+    hbs_step(a3lo, a4lo, amlo, r0.w, t3, t4);
+    hbs_step(a3lo, a4lo, amlo, r0.z, t3, t4);
+    hbs_step(a3lo, a4lo, amlo, r0.y, t3, t4);
+    hbs_step(a3lo, a4lo, amlo, r0.x, t3, t4);
+  }
+  {
+    const uint4 r3 = philox4x32_10(t, ctr0 + 3, p.colour, row, p.keys);
+    hbs_step(a3hi, a4hi, amhi, r3.w, t3, t4);
+    hbs_step(a3hi, a4hi, amhi, r3.z, t3, t4);
+    hbs_step(a3hi, a4hi, amhi, r3.y, t3, t4);
+    hbs_step(a3hi, a4hi, amhi, r3.x, t3, t4);
+    const uint4 r2 = philox4x32_10(t, ctr0 + 2, p.colour, row, p.keys);
+    hbs_step(a3hi, a4hi, amhi, r2.w, t3, t4);
+    hbs_step(a3hi, a4hi, amhi, r2.z, t3, t4);
+    hbs_step(a3hi, a4hi, amhi, r2.y, t3, t4);
+    hbs_step(a3hi, a4hi, amhi, r2.x, t3, t4);
+  }
+  const uint32_t flo = hb_accept8((uint32_t)tgt, sum_lo, hbs_nc(a3lo + a4lo, amlo));
+  const uint32_t fhi = hb_accept8((uint32_t)(tgt >> 32), sum_hi, hbs_nc(a3hi + a4hi, amhi));
+  return ((uint64_t)fhi << 32) | flo;
+}
+
 // Heat bath, generic (some threshold is 2^32): flip iff r < T[a] for every class.
 // T is non-increasing in a, so "r < T[a]" <=> a < #{m : r < T[m]}.
 template <>
@@ -325,6 +386,7 @@ static cudaError_t dispatch_rule(int rule, bool obs, F&& f) {
     ISING_RULE_CASE(4)
     ISING_RULE_CASE(5)
     ISING_RULE_CASE(6)
+    ISING_RULE_CASE(7)
   }
 #undef ISING_RULE_CASE
   return cudaErrorInvalidValue;

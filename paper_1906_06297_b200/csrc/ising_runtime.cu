@@ -100,6 +100,11 @@ struct IpcBlob {  // ising_ipc_handle payload (<= ISING_IPC_BLOB_BYTES)
 };
 static_assert(sizeof(IpcBlob) <= ISING_IPC_BLOB_BYTES, "IPC blob too large");
 
+static bool env_is_zero(const char* name) {
+  const char* v = getenv(name);
+  return v && v[0] == '0';
+}
+
 struct Device {
   int dev = -1;
   int sms = 0;
@@ -169,6 +174,8 @@ struct ising_ctx {
   bool persistent_enabled = false;         // opt-in (ISING_PERSISTENT=1): measured slower
                                            // than graph replay on B200 (grid barrier ~3 us)
   bool staged = true;                      // TMA-staged half-sweep (ISING_STAGED=0: off)
+  // heat-bath variant 7 (ISING_HB_SYMMETRIC=0: off, for every handle type)
+  bool symmetric_hb_enabled = !env_is_zero("ISING_HB_SYMMETRIC");
   bool draw_free_enabled = true;           // beta in {0, inf}: skip Philox (ISING_DRAW_FREE=0)
   unsigned int* bar = nullptr;             // persistent kernel's grid barrier state
   int persist_blocks_per_sm = 0;
@@ -343,7 +350,8 @@ void halfsweep_geometry(const ising_ctx* h, const Device& d, int64_t rows, int* 
 
 // kernel variant: 0 = Metropolis with both thresholds < 2^32 (the fast path),
 // 2 = Metropolis generic (tiny beta), 4 = Metropolis draw-free (T3, T4 in {0, 2^32});
-// heat bath 3 / 5 / 6 = fast path with 0 / 1 / 2 "always" classes (T = 2^32), 1 = generic
+// heat bath 3 / 5 / 6 = fast path with 0 / 1 / 2 "always" classes (T = 2^32), 1 = generic,
+// 7 = symmetric thresholds (T[0] + T[4] = T[1] + T[3] = 2^32 + 1, T[2] = 2^31)
 int kernel_variant(const ising_ctx* h) {
   if (h->rule == ISING_RULE_METROPOLIS) {
     const bool t3_fixed = h->T[3] == 0 || h->T[3] == (uint64_t(1) << 32);
@@ -351,6 +359,11 @@ int kernel_variant(const ising_ctx* h) {
     if (t3_fixed && t4_fixed && h->draw_free_enabled) return 4;  // no draw needed
     return (h->acc.keep3 & h->acc.keep4) ? 0 : 2;
   }
+  // symmetric thresholds (P(e) + P(-e) = 1 survived the rounding): the 2-compare kernel
+  const uint64_t two32p1 = (uint64_t(1) << 32) + 1;
+  if (h->symmetric_hb_enabled && h->T[2] == (uint64_t(1) << 31) && h->T[0] + h->T[4] == two32p1 &&
+      h->T[1] + h->T[3] == two32p1)
+    return 7;
   switch (h->acc.always_mask) {  // the "always" classes form a prefix of the non-increasing T
     case 0: return 3;
     case 1: return 5;
@@ -1604,6 +1617,12 @@ int ising_thresholds(ising_t h, uint64_t T[5]) {
 int ising_launch_count(ising_t h, int64_t* launches) {
   if (!h || !launches) return ISING_ERR_ARG;
   *launches = h->launch_count;
+  return ISING_OK;
+}
+
+int ising_kernel_variant(ising_t h, int* variant) {
+  if (!h || !variant) return ISING_ERR_ARG;
+  *variant = kernel_variant(h);
   return ISING_OK;
 }
 

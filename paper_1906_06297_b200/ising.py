@@ -59,6 +59,7 @@ SIGNATURES = {
     "ising_slab_info": (_INT, [_VP, _I64P, _I64P]),
     "ising_thresholds": (_INT, [_VP, _U64P]),
     "ising_launch_count": (_INT, [_VP, _I64P]),
+    "ising_kernel_variant": (_INT, [_VP, ctypes.POINTER(ctypes.c_int)]),
     "ising_probe_philox": (_INT, [_INT, _DBLP]),
     "ising_strerror": (ctypes.c_char_p, [_INT]),
     "ising_last_error": (ctypes.c_char_p, []),
@@ -261,6 +262,12 @@ def ising_thresholds(h: int) -> list[int]:
     return [int(x) for x in T]
 
 
+def ising_kernel_variant(h: int) -> int:
+    v = ctypes.c_int(0)
+    _check(load().ising_kernel_variant(h, ctypes.byref(v)), "ising_kernel_variant")
+    return v.value
+
+
 def ising_launch_count(h: int) -> int:
     n = _I64()
     _check(load().ising_launch_count(h, ctypes.byref(n)), "ising_launch_count")
@@ -423,3 +430,6 @@ class IsingLattice:
 
     def launch_count(self) -> int:
         return ising_launch_count(self.h)
+
+    def kernel_variant(self) -> int:
+        return ising_kernel_variant(self.h)

@@ -28,15 +28,21 @@ def test_basic_matches_oracle(N, M, beta, rule):
 
 @pytest.mark.parametrize("N,M", [(64, 64), (130, 192), (34, 1024)])
 @pytest.mark.parametrize("beta,rule", [(0.4406868, 0), (4e-11, 0), (math.inf, 0), (0.0, 0),
-                                       (0.4406868, 1), (3.0, 1), (6.0, 1), (math.inf, 1)])
-def test_basic_kernels_every_variant(N, M, beta, rule, monkeypatch):
+                                       (0.4406868, 1), (3.0, 1), (6.0, 1), (math.inf, 1),
+                                       (0.3377438395041983, 1)])
+@pytest.mark.parametrize("sym", ["1", "0"])
+def test_basic_kernels_every_variant(N, M, beta, rule, sym, monkeypatch):
     # the byte-lane SWAR kernel (default) and the listing-shaped kernel both equal the
     # oracle for every acceptance variant (Metropolis fast / generic / draw-free, heat bath
-    # with 0, 1, 2 "always" classes)
+    # symmetric (7) or with 0, 1, 2 "always" classes; 0.33774... has an asymmetric table)
+    monkeypatch.setenv("ISING_HB_SYMMETRIC", sym)
     o = oracle.Lattice(N, M, 4).set_beta(beta, rule).init_random().sweep(3)
     for listing in ["0", "1"]:
         monkeypatch.setenv("ISING_BASIC_LISTING", listing)
-        g = IsingLattice.basic(N, M, 4).set_beta(beta, rule).init_random().sweep(3)
+        g = IsingLattice.basic(N, M, 4).set_beta(beta, rule)
+        if rule == 1 and sym == "1" and beta in (0.4406868, 3.0, 6.0):
+            assert g.kernel_variant() == 7
+        g.init_random().sweep(3)
         assert np.array_equal(g.read_lattice(), o.full()), (listing, N, M, beta, rule)
         g.close()
 

@@ -88,17 +88,45 @@ def test_virtual_slabs_match_oracle(N, M, nslab):
         assert_same(g, o, f"{nslab} slabs t={o.t}")
 
 
-def test_heatbath_parity():
-    # beta 3.0: T[0] = 2^32 (variant 5); 6.0 and inf: T[0] = T[1] = 2^32 (variant 6)
-    for N, M, beta in [(64, 64, 0.4406868), (66, 128, 0.2), (32, 64, math.inf), (32, 64, 0.0),
-                       (64, 128, 3.0), (66, 64, 6.0), (32, 64, 2.5)]:
+# Heat-bath betas with the expected kernel variant (ising_kernel_variant): 7 = symmetric
+# thresholds (T[0] + T[4] = T[1] + T[3] = 2^32 + 1), the default whenever the rounded table
+# has that property; with ISING_HB_SYMMETRIC=0 the five-compare kernels: 3 (every T < 2^32),
+# 5 (T[0] = 2^32, beta 3), 6 (T[0] = T[1] = 2^32, beta 6, inf).  beta = 0 (all T = 2^31) and
+# the two betas below (found by search: ceil(2^32 P(e)) + ceil(2^32 P(-e)) = 2^32 for one
+# pair) are not symmetric, so they keep the five-compare kernels either way.
+HB_ASYM = [0.3377438395041983, 1.2800778283900398]
+HB_CASES = [((64, 64), 0.4406868, 7, 3), ((66, 128), 0.2, 7, 3), ((32, 64), math.inf, 6, 6),
+            ((32, 64), 0.0, 3, 3), ((64, 128), 3.0, 7, 5), ((66, 64), 6.0, 7, 6),
+            ((32, 64), 2.5, 7, 3), ((64, 64), HB_ASYM[0], 3, 3), ((64, 64), HB_ASYM[1], 3, 3)]
+
+
+@pytest.mark.parametrize("sym", ["1", "0"])
+def test_heatbath_parity(monkeypatch, sym):
+    monkeypatch.setenv("ISING_HB_SYMMETRIC", sym)
+    for (N, M), beta, v_sym, v_plain in HB_CASES:
         g = gpu_lattice(N, M, 5, "random", beta, ising.RULE_HEATBATH)
         o = oracle_lattice(N, M, 5, "random", beta, oracle.RULE_HEATBATH)
-        assert g.thresholds() == [int(x) for x in o_thresholds(beta, oracle.RULE_HEATBATH)]
+        T = [int(x) for x in o_thresholds(beta, oracle.RULE_HEATBATH)]
+        assert g.thresholds() == T
+        symmetric = T[2] == 2**31 and T[0] + T[4] == T[1] + T[3] == 2**32 + 1
+        assert symmetric == (v_sym == 7), (beta, T)
+        assert g.kernel_variant() == (v_sym if sym == "1" else v_plain), beta
         for n in [1, 10]:
             g.sweep(n)
             o.sweep(n)
-            assert_same(g, o, f"heat bath {N}x{M} beta={beta}")
+            assert_same(g, o, f"heat bath {N}x{M} beta={beta} variant={g.kernel_variant()}")
+
+
+def test_heatbath_symmetric_wide_and_measured():
+    # variant 7 in the TMA-staged kernel (W % 256 == 0), two virtual slabs, and the fused
+    # observables of a measured chain
+    g = gpu_lattice(34, 8192, 6, "random", 0.4406868, ising.RULE_HEATBATH, devices=[0, 0])
+    o = oracle_lattice(34, 8192, 6, "random", 0.4406868, oracle.RULE_HEATBATH)
+    assert g.kernel_variant() == 7
+    ups, Es = g.measure(4, 1)
+    ou, oE = o.chain(4)
+    assert np.array_equal(ups, ou) and np.array_equal(Es, oE)
+    assert_same(g, o, "symmetric heat bath 34x8192")
 
 
 def o_thresholds(beta, rule):

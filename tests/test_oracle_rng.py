@@ -107,3 +107,32 @@ def test_thresholds_special_cases():
         assert hb[0] > hb[1] > hb[2] > hb[3] > hb[4]
         m = [int(x) for x in oracle.thresholds(beta)]
         assert m[3] > m[4] > 0
+
+
+def test_heatbath_table_symmetry_and_its_rounding_exceptions():
+    # Heat bath: P(e) + P(-e) = 1, so with exact arithmetic
+    # ceil(2^32 P(e)) + ceil(2^32 P(-e)) = 2^32 + 1 (2^32 P is never an integer for beta > 0).
+    # The GPU's symmetric heat-bath kernel (variant 7) relies on that identity and the host
+    # checks it on the rounded table (reading R22: IEEE double via host libm, as here).  Two
+    # betas found by search break it in double precision only: the 60-digit table is
+    # symmetric, the double one is not, so those betas must take the five-compare kernel
+    # (tests/test_gpu_parity.py::HB_ASYM).
+    getcontext().prec = 60
+
+    def exact_table(beta):
+        out = []
+        for a in range(5):
+            p = (Decimal(-2 * (2 * a - 4)) * Decimal(beta)).exp()
+            out.append(_ceil_scaled_decimal(p / (1 + p)))
+        return out
+
+    def symmetric(T):
+        return T[2] == 2**31 and T[0] + T[4] == T[1] + T[3] == 2**32 + 1
+
+    for beta in [0.1, 0.2, 0.4406868, 0.8, 2.5, 3.0, 6.0]:
+        T = [int(x) for x in oracle.thresholds(beta, oracle.RULE_HEATBATH)]
+        assert symmetric(T) and T == exact_table(beta), beta
+    for beta in [0.3377438395041983, 1.2800778283900398]:
+        T = [int(x) for x in oracle.thresholds(beta, oracle.RULE_HEATBATH)]
+        assert not symmetric(T) and symmetric(exact_table(beta)), beta
+        assert T[0] + T[4] + T[1] + T[3] == 2**33 + 1  # exactly one pair rounded onto 2^32

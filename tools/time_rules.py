@@ -15,4 +15,4 @@ for name, beta, rule in [("metropolis fast", 0.4406868, 0), ("metropolis generic
     lat.set_beta(beta, rule)
     lat.sweep(4)
     lat.sweep(16)
-    print(f"{name:30s} {N * M * 16 / (lat.last_sweep_ms() * 1e6):8.1f} flips/ns")
+    print(f"{name:30s} {N * M * 16 / (lat.last_sweep_ms() * 1e6):8.1f} flips/ns  (variant {lat.kernel_variant()})")
