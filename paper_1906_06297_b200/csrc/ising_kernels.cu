@@ -940,51 +940,85 @@ __global__ void __launch_bounds__(256) k_observables(const ObsParams p) {
 }
 
 // ------------------------------------------------------------ pack / unpack
-// Full lattice (row-major +-1 bytes) <-> planes.  Site (i, J) has colour
-// c = (i + J) & 1 and plane column J / 2, i.e. J = 2 j + ((i + c) & 1).
+// Full lattice (row-major +-1 bytes) <-> planes.  Site (i, J) has colour c = (i + J) & 1 and
+// plane column J / 2 (reading R1), so full columns J0 .. J0 + 15 (J0 = 16 u) of row i are
+// plane columns 8u .. 8u + 7 — the 32-bit half-word u of each plane row — with byte 2j' + x
+// from colour (i + x) & 1.  One thread per 16 bytes: 128-bit full-row accesses and 32-bit
+// plane accesses, both coalesced across the warp.
+__device__ __forceinline__ void bytes_to_lanes(const uint4 v, uint32_t& even, uint32_t& odd,
+                                               unsigned int& bad) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  even = odd = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const uint32_t byte = (w[q] >> (8 * b)) & 0xFFu;  // full column J0 + 4q + b
+      bad |= (byte != 0x01u && byte != 0xFFu);
+      const int jj = 2 * q + (b >> 1);                  // plane column 8u + jj
+      const uint32_t up = byte == 0x01u ? 1u : 0u;
+      if (b & 1) odd |= up << (4 * jj);
+      else even |= up << (4 * jj);
+    }
+}
+
+__device__ __forceinline__ uint4 lanes_to_bytes(uint32_t even, uint32_t odd) {
+  uint32_t w[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    // bytes: (2q, even), (2q, odd), (2q + 1, even), (2q + 1, odd); 0/1 bits at 0, 8, 16, 24
+    const uint32_t f = ((even >> (8 * q)) & 1u) | (((odd >> (8 * q)) & 1u) << 8) |
+                       (((even >> (8 * q + 4)) & 1u) << 16) | (((odd >> (8 * q + 4)) & 1u) << 24);
+    w[q] = ~((f << 8) - (f << 1));  // per byte: f ? 0x01 : 0xFF (0xFE f = (f << 8) - 2 f)
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
 __global__ void k_pack(const PackParams p) {
   const int64_t rows = p.rb - p.ra;
-  const int64_t total = 2 * rows * p.W;
+  const int64_t halves = 2 * p.W;  // 32-bit half-words per plane row
+  const int64_t total = rows * halves;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  uint32_t* pl0 = reinterpret_cast<uint32_t*>(p.plane[0]);
+  uint32_t* pl1 = reinterpret_cast<uint32_t*>(p.plane[1]);
+  unsigned int bad = 0;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += stride) {
-    const int c = (int)(idx / (rows * p.W));
-    const int64_t rem = idx - (int64_t)c * rows * p.W;
-    const int64_t lr = rem / p.W;  // row within staging
-    const int64_t w = rem - lr * p.W;
-    const int64_t r = p.ra + lr;   // padded local row (-1 .. R)
+    const int64_t lr = idx / halves;  // row within staging
+    const int64_t u = idx - lr * halves;
+    const int64_t r = p.ra + lr;      // padded local row (-1 .. R)
     int64_t gi = (p.row0 + r) % p.N;
     if (gi < 0) gi += p.N;
-    const int x = (int)((gi + c) & 1);
-    const int8_t* rowp = p.full + lr * p.M;
-    uint64_t word = 0;
-    unsigned int bad = 0;
-#pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      const int8_t v = rowp[2 * (16 * w + k) + x];
-      bad |= (v != 1 && v != -1);
-      if (v == 1) word |= 1ull << (4 * k);
+    uint32_t even, odd;
+    bytes_to_lanes(*reinterpret_cast<const uint4*>(p.full + lr * p.M + 16 * u), even, odd, bad);
+    const int64_t o = (r + 1) * halves + u;
+    // even full columns have colour i & 1, odd ones the other
+    if (gi & 1) {
+      pl1[o] = even;
+      pl0[o] = odd;
+    } else {
+      pl0[o] = even;
+      pl1[o] = odd;
     }
-    if (bad) atomicOr(p.bad, 1u);
-    p.plane[c][(r + 1) * p.W + w] = word;
   }
+  if (bad) atomicOr(p.bad, 1u);
 }
 
 __global__ void k_unpack(const UnpackParams p) {
   const int64_t rows = p.rb - p.ra;
-  const int64_t total = 2 * rows * p.W;
+  const int64_t halves = 2 * p.W;
+  const int64_t total = rows * halves;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const uint32_t* pl0 = reinterpret_cast<const uint32_t*>(p.plane[0]);
+  const uint32_t* pl1 = reinterpret_cast<const uint32_t*>(p.plane[1]);
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += stride) {
-    const int c = (int)(idx / (rows * p.W));
-    const int64_t rem = idx - (int64_t)c * rows * p.W;
-    const int64_t lr = rem / p.W;
-    const int64_t w = rem - lr * p.W;
+    const int64_t lr = idx / halves;
+    const int64_t u = idx - lr * halves;
     const int64_t r = p.ra + lr;
-    const int64_t gi = p.row0 + r;
-    const int x = (int)((gi + c) & 1);
-    const uint64_t word = p.plane[c][(r + 1) * p.W + w];
-    int8_t* rowp = p.full + lr * p.M;
-#pragma unroll
-    for (int k = 0; k < 16; ++k) rowp[2 * (16 * w + k) + x] = ((word >> (4 * k)) & 1) ? 1 : -1;
+    const int64_t o = (r + 1) * halves + u;
+    const uint32_t a = pl0[o], b = pl1[o];
+    const bool odd_row = ((p.row0 + r) & 1) != 0;
+    *reinterpret_cast<uint4*>(p.full + lr * p.M + 16 * u) =
+        odd_row ? lanes_to_bytes(b, a) : lanes_to_bytes(a, b);
   }
 }
 

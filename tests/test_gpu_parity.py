@@ -211,11 +211,12 @@ def test_error_behaviour():
     with pytest.raises(ising.IsingError) as e:
         g.read_lattice(np.empty(64 * 64 - 1, dtype=np.int8))
     assert e.value.status == ising.ISING_ERR_RANGE
-    bad = np.ones((64, 64), dtype=np.int8)
-    bad[3, 3] = 0
-    with pytest.raises(ising.IsingError) as e:
-        g.write_lattice(bad)
-    assert e.value.status == ising.ISING_ERR_ARG
+    for (i, j), v in [((3, 3), 0), ((0, 0), 2), ((63, 63), -128), ((10, 17), 127), ((5, 48), -2)]:
+        bad = np.ones((64, 64), dtype=np.int8)
+        bad[i, j] = v  # anything but +-1, at even / odd columns and both corners
+        with pytest.raises(ising.IsingError) as e:
+            g.write_lattice(bad)
+        assert e.value.status == ising.ISING_ERR_ARG, (i, j, v)
     g.set_beta(0.3)
     g.write_lattice(np.ones((64, 64), dtype=np.int8), t=2**32 - 3)
     g.sweep(2)
@@ -223,6 +224,20 @@ def test_error_behaviour():
         g.sweep(1)
     assert e.value.status == ising.ISING_ERR_RANGE
     g.sweep(0)
+
+
+def test_write_read_round_trip_pattern():
+    # pack / unpack (row a9) on an arbitrary pattern: every byte position of the 16-byte
+    # chunks, both row parities, a width that is not a multiple of 128 columns
+    rng = np.random.default_rng(11)
+    for N, M in [(6, 64), (130, 192), (34, 8192)]:
+        full = rng.choice(np.array([-1, 1], dtype=np.int8), size=(N, M))
+        g = IsingLattice(N, M, 1).write_lattice(full)
+        assert np.array_equal(g.read_lattice(), full), (N, M)
+        up, E = g.observables()
+        assert up == int((full == 1).sum())
+        assert E == -int((full * np.roll(full, 1, 0)).sum() + (full * np.roll(full, 1, 1)).sum())
+        g.close()
 
 
 def test_random_start_golden():
