@@ -392,6 +392,22 @@ static cudaError_t dispatch_rule(int rule, bool obs, F&& f) {
   return cudaErrorInvalidValue;
 }
 
+// Observables of one target word t after its update (row a8, Eq. 1): up spins in t and in
+// the centre source word c, and bonds from t's 16 sites to their four neighbours that are
+// antiparallel.  Lanes use bit 0 of each nibble only, so the four neighbour XORs are packed
+// into the four bits of each nibble — X = (t * 15) ^ (n | c << 1 | s << 2 | side << 3) — and
+// one popcount counts all of them (likewise t | c << 1 for the up count): 2 popcounts per
+// word instead of 6.
+// Acc: 32-bit in the half-sweep kernels (per-thread counts stay far below 2^32 and 64-bit
+// adds would put an IMAD.X on the FMA pipe per add), 64-bit in k_observables.
+template <typename Acc>
+__device__ __forceinline__ void obs_word(uint64_t t, uint64_t n, uint64_t c, uint64_t s,
+                                         uint64_t side, Acc& up, Acc& anti) {
+  const uint64_t t15 = (t << 4) - t;
+  up += __popcll(t | (c << 1));
+  anti += __popcll(t15 ^ (n | (c << 1) | (s << 2) | (side << 3)));
+}
+
 // One colour phase of one slab.  Work item = (band of H rows, 128-bit chunk
 // column q); the thread walks down the band keeping the N/C/S source chunks in
 // registers, so each source word is read from memory once per band (plus one halo
@@ -452,8 +468,7 @@ __device__ __forceinline__ ulonglong2 ld_tgt(const uint64_t* p) {
 // separate pass over the lattice (Eq. 1; row a8).
 template <int RULE, bool OBS, bool COHERENT>
 __device__ __forceinline__ void halfsweep_items(const HalfSweepParams& p, const uint32_t t,
-                                                unsigned long long& obs_up,
-                                                unsigned long long& obs_anti) {
+                                                uint32_t& obs_up, uint32_t& obs_anti) {
   const int64_t W = p.W;
   const int64_t chunks = W / kWords;
   const uint64_t* src = p.src + W;  // local row r (r = -1 .. R) at src + r * W
@@ -511,9 +526,7 @@ __device__ __forceinline__ void halfsweep_items(const HalfSweepParams& p, const 
         const uint32_t ctr0 = (uint32_t)(4 * (wc + k));  // Philox counter word 1 = j / 4 (R6)
         tv[k] = update_word<RULE>(tv[k], nv[k], cv[k], sv[k], side[k], ctr0, (uint32_t)gi, t, p);
         if (OBS) {
-          obs_up += __popcll(tv[k]) + __popcll(cv[k]);
-          obs_anti += __popcll(tv[k] ^ nv[k]) + __popcll(tv[k] ^ cv[k]) + __popcll(tv[k] ^ sv[k]) +
-                      __popcll(tv[k] ^ side[k]);
+          obs_word(tv[k], nv[k], cv[k], sv[k], side[k], obs_up, obs_anti);
         }
       }
 #pragma unroll
@@ -540,7 +553,7 @@ __global__ void __launch_bounds__(128, ISING_MINB) k_halfsweep(const HalfSweepPa
   }
   // sweep index: absolute, or (CUDA graph replays) a device-resident base + the offset
   const uint32_t t = p.t_dev ? *p.t_dev + p.t : p.t;
-  unsigned long long obs_up = 0, obs_anti = 0;
+  uint32_t obs_up = 0, obs_anti = 0;
   halfsweep_items<RULE, OBS, false>(p, t, obs_up, obs_anti);
   if (OBS) {
 #pragma unroll
@@ -690,7 +703,7 @@ __global__ void __launch_bounds__(128, ISING_MINB) k_halfsweep_staged(const Half
   const uint32_t t = p.t_dev ? *p.t_dev + p.t : p.t;
   const int tid = threadIdx.x;
   const int64_t wc = w0 + 2 * tid;
-  unsigned long long obs_up = 0, obs_anti = 0;
+  uint32_t obs_up = 0, obs_anti = 0;
   for (int rr = 0; rr < nrows; ++rr) {
     const int r = ra + rr;
     const int64_t gi = p.row0 + r;
@@ -717,10 +730,8 @@ __global__ void __launch_bounds__(128, ISING_MINB) k_halfsweep_staged(const Half
     if (r == 0 && p.halo_up) *reinterpret_cast<ulonglong2*>(p.halo_up + wc) = tv;
     if (r == p.R - 1 && p.halo_dn) *reinterpret_cast<ulonglong2*>(p.halo_dn + wc) = tv;
     if (OBS) {  // same fused observables as k_halfsweep (white phase of a measured sweep)
-      obs_up += __popcll(tv.x) + __popcll(tv.y) + __popcll(c0) + __popcll(c1);
-      obs_anti += __popcll(tv.x ^ n0) + __popcll(tv.x ^ c0) + __popcll(tv.x ^ s0) +
-                  __popcll(tv.x ^ side0) + __popcll(tv.y ^ n1) + __popcll(tv.y ^ c1) +
-                  __popcll(tv.y ^ s1) + __popcll(tv.y ^ side1);
+      obs_word(tv.x, n0, c0, s0, side0, obs_up, obs_anti);
+      obs_word(tv.y, n1, c1, s1, side1, obs_up, obs_anti);
     }
   }
   if (OBS) {
@@ -795,7 +806,7 @@ template <int RULE, bool OBS>
 __global__ void __launch_bounds__(kPersistThreads, 1) k_sweeps_persistent(const PersistentParams P) {
   for (uint32_t s = 1; s <= P.n; ++s) {
     const uint32_t t = P.t0 + s;
-    unsigned long long up = 0, anti = 0;
+    uint32_t up = 0, anti = 0;
     halfsweep_items<RULE, false, true>(P.ph[0], t, up, anti);
     grid_barrier(P.bar_count, P.bar_gen);
     if (OBS && s % P.every == 0) {
@@ -924,8 +935,7 @@ __global__ void __launch_bounds__(256) k_observables(const ObsParams p) {
       const uint64_t ew = wh[r * p.W + (w + 1 == p.W ? 0 : w + 1)];
       side = (cw >> 4) | (ew << 60);
     }
-    up += __popcll(b) + __popcll(cw);
-    anti += __popcll(b ^ nw) + __popcll(b ^ cw) + __popcll(b ^ sw) + __popcll(b ^ side);
+    obs_word(b, nw, cw, sw, side, up, anti);
   }
   // warp reduction by shuffles, then one atomic per warp
 #pragma unroll
