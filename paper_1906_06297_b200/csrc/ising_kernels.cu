@@ -657,8 +657,19 @@ __global__ void __launch_bounds__(128, ISING_MINB) k_halfsweep_staged(const Half
   const int64_t bpr = W / kStageWords;  // blocks per band
   const int band = (int)(blockIdx.x / bpr);
   const int64_t w0 = (int64_t)(blockIdx.x - (int64_t)band * bpr) * kStageWords;
-  const int ra = p.r_begin + band * kStageRows;
-  const int rb = min(ra + kStageRows, p.r_end);
+  // bands of kStageRows rows; with a guided tail (tail_band8 > 0) the last bands are 8 and
+  // then 4 rows tall, so the partial last wave idles for a short block lifetime only
+  int ra, rb;
+  if (band < p.tail_band8 || p.tail_band8 == 0) {
+    ra = p.r_begin + band * kStageRows;
+    rb = min(ra + kStageRows, p.r_end);
+  } else if (band < p.tail_band4) {
+    ra = p.r_begin + p.tail_band8 * kStageRows + (band - p.tail_band8) * p.tail_h1;
+    rb = min(ra + p.tail_h1, p.r_begin + p.tail_row4);
+  } else {
+    ra = p.r_begin + p.tail_row4 + (band - p.tail_band4) * p.tail_h2;
+    rb = min(ra + p.tail_h2, p.r_end);
+  }
   const int nrows = rb - ra;
   const uint64_t* src = p.src + W;  // local row r at src + r * W
   uint64_t* tgt = p.tgt + W;
@@ -761,13 +772,38 @@ __global__ void __launch_bounds__(128, ISING_MINB) k_halfsweep_staged(const Half
   }
 }
 
-cudaError_t launch_halfsweep_staged(int rule, cudaStream_t st, const HalfSweepParams& p) {
+// slots = resident blocks (SMs x blocks per SM), 0: no guided tail.  The tail is one wave of
+// 8-row bands then one of 4-row bands, used when the 16-row grid is 3 to 64 waves long (a
+// partial last wave costs about half a block lifetime per slot: 3.6 % on C3).
+cudaError_t launch_halfsweep_staged(int rule, int64_t slots, cudaStream_t st, HalfSweepParams p) {
   const int64_t rows = p.r_end - p.r_begin;
-  const unsigned grid = (unsigned)((p.W / kStageWords) * ((rows + kStageRows - 1) / kStageRows));
+  const int64_t spans = p.W / kStageWords;
+  int64_t bands = (rows + kStageRows - 1) / kStageRows;
+  p.tail_band8 = p.tail_band4 = p.tail_row4 = 0;
+  const int64_t per_wave = slots / spans;  // bands per wave
+  // measured on C3 (profiles/r01_ncu_halfsweep.md): heights 8/4, 8/2, 4/2, 12/6 and one or
+  // two waves each all land within 0.3 % of each other
+  constexpr int h1 = 8, h2 = 4, w1 = 1, w2 = 1;
+  if (per_wave > 0 && bands * spans >= 3 * slots && bands * spans < 64 * slots) {
+    const int64_t row4 = rows - (int64_t)h2 * w2 * per_wave;
+    const int64_t row8 = ((row4 - (int64_t)h1 * w1 * per_wave) / kStageRows) * kStageRows;
+    const int64_t n8 = (row4 - row8 + h1 - 1) / h1;
+    p.tail_band8 = (int32_t)(row8 / kStageRows);
+    p.tail_band4 = (int32_t)(p.tail_band8 + n8);
+    p.tail_row4 = (int32_t)row4;
+    p.tail_h1 = h1;
+    p.tail_h2 = h2;
+    bands = p.tail_band4 + (rows - row4 + h2 - 1) / h2;
+  }
+  const unsigned grid = (unsigned)(spans * bands);
   return dispatch_rule(rule, p.obs_out != nullptr, [&](auto R, auto O) {
     k_halfsweep_staged<decltype(R)::value, decltype(O)::value><<<grid, 128, 0, st>>>(p);
     return cudaGetLastError();
   });
+}
+
+cudaError_t staged_occupancy(int* blocks_per_sm) {
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_halfsweep_staged<0>, 128, 0);
 }
 
 // ------------------------------------------------------- persistent sweeps

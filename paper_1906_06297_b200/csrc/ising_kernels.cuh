@@ -48,6 +48,10 @@ struct HalfSweepParams {
   int32_t r_end;          // one past the last local row to update
   int32_t H;              // rows per work item (register-rolling band)
   int64_t items;          // number of work items = (W / 2) * ceil((r_end - r_begin) / H)
+  int32_t tail_band8;     // staged kernel guided tail: first 8-row band (0: no tail)
+  int32_t tail_band4;     //   first 4-row band
+  int32_t tail_row4;      //   first row (relative to r_begin) of the 4-row bands
+  int32_t tail_h1, tail_h2;  // tail band heights (8, 4)
   uint32_t t;             // sweep index (>= 1), or the offset added to *t_dev
   const uint32_t* t_dev;  // graph replays: device-resident sweep base (null otherwise)
   uint32_t colour;        // 0 black, 1 white
@@ -167,7 +171,8 @@ cudaError_t launch_basic_convert(int grid, cudaStream_t st, int8_t* black, int8_
 
 // Host-side launchers (defined in ising_kernels.cu).
 cudaError_t launch_sync(cudaStream_t st, const SyncParams& p);
-cudaError_t launch_halfsweep_staged(int rule, cudaStream_t st, const HalfSweepParams& p);
+cudaError_t launch_halfsweep_staged(int rule, int64_t slots, cudaStream_t st, HalfSweepParams p);
+cudaError_t staged_occupancy(int* blocks_per_sm);
 cudaError_t launch_persistent(int rule, int grid, cudaStream_t st, const PersistentParams& P);
 cudaError_t persistent_occupancy(int* blocks_per_sm);
 cudaError_t launch_set_u32(cudaStream_t st, uint32_t* dst, uint32_t v, int add);

@@ -109,6 +109,7 @@ struct Device {
   int dev = -1;
   int sms = 0;
   int hs_blocks_per_sm = 0;  // occupancy of k_halfsweep<0>
+  int staged_blocks_per_sm = 0;  // occupancy of k_halfsweep_staged<0>
   cudaStream_t stream = nullptr;
   cudaStream_t comm = nullptr;
   cudaEvent_t ev_phase = nullptr;  // end of the latest phase on this device
@@ -174,6 +175,7 @@ struct ising_ctx {
   bool persistent_enabled = false;         // opt-in (ISING_PERSISTENT=1): measured slower
                                            // than graph replay on B200 (grid barrier ~3 us)
   bool staged = true;                      // TMA-staged half-sweep (ISING_STAGED=0: off)
+  bool guided_tail = !env_is_zero("ISING_TAIL");  // staged kernel: 8- / 4-row last waves
   // heat-bath variant 7 (ISING_HB_SYMMETRIC=0: off, for every handle type)
   bool symmetric_hb_enabled = !env_is_zero("ISING_HB_SYMMETRIC");
   bool draw_free_enabled = true;           // beta in {0, inf}: skip Philox (ISING_DRAW_FREE=0)
@@ -263,6 +265,8 @@ int setup_device(Device& d, int dev) {
   CU(cudaMalloc(&d.red, 4 * sizeof(unsigned long long)));
   CU(halfsweep_occupancy(&d.hs_blocks_per_sm));
   if (d.hs_blocks_per_sm < 1) d.hs_blocks_per_sm = 1;
+  CU(staged_occupancy(&d.staged_blocks_per_sm));
+  if (d.staged_blocks_per_sm < 1) d.staged_blocks_per_sm = 1;
   return ISING_OK;
 }
 
@@ -409,7 +413,8 @@ int run_halfsweep(ising_ctx* h, Slab& s, int c, int r_begin, int r_end, uint64_t
   const bool prof = h->profiling && s.devi == 0 && h->kernel_launches < kMaxProfiledLaunches;
   if (prof) CU(cudaEventRecord(h->prof_events[2 * h->kernel_launches], d.stream));
   if (h->staged && h->W % 256 == 0)
-    CU(launch_halfsweep_staged(kernel_variant(h), d.stream, p));
+    CU(launch_halfsweep_staged(kernel_variant(h),
+                               h->guided_tail ? (int64_t)d.sms * d.staged_blocks_per_sm : 0, d.stream, p));
   else
     CU(launch_halfsweep(kernel_variant(h), grid, d.stream, p));
   if (prof) {

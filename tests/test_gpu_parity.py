@@ -358,6 +358,26 @@ def test_tma_staged_kernel_path():
             assert_same(g, o, f"staged heat bath {N}x{M} beta={beta}")
 
 
+@pytest.mark.parametrize("tail", ["1", "0"])
+def test_staged_guided_tail(monkeypatch, tail):
+    # grids of 3 to 64 waves of 16-row tiles end with one wave of 8-row and one of 4-row
+    # bands (ISING_TAIL=0: plain 16-row bands).  7168 x 32768: 448 bands x 4 spans = 1792
+    # blocks >= 3 waves of 592 on a 148-SM B200; the 8-row region starts at row 4784.
+    monkeypatch.setenv("ISING_TAIL", tail)
+    N, M = 7168, 32768
+    g = gpu_lattice(N, M, 9, "random", 0.4406868)
+    o = oracle_lattice(N, M, 9, "random", 0.4406868)
+    g.sweep(1)
+    o.sweep(1)
+    assert_same(g, o, f"staged tail={tail} {N}x{M}")
+    g.set_beta(0.4406868, ising.RULE_HEATBATH)
+    o.set_beta(0.4406868, oracle.RULE_HEATBATH)
+    ups, Es = g.measure(1, 1)
+    ou, oE = o.chain(1)
+    assert np.array_equal(ups, ou) and np.array_equal(Es, oE)
+    assert_same(g, o, f"staged tail={tail} heat bath {N}x{M}")
+
+
 def test_register_rolling_path_on_wide_lattice(monkeypatch):
     # ISING_STAGED=0 keeps the register-rolling kernel on widths the staged one would take
     monkeypatch.setenv("ISING_STAGED", "0")
