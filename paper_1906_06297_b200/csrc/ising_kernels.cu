@@ -646,6 +646,14 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 
 template <int RULE, bool OBS = false>
 __global__ void __launch_bounds__(128, ISING_MINB) k_halfsweep_staged(const HalfSweepParams p) {
+  // Programmatic dependent launch (p.pdl: launched with programmatic stream serialisation):
+  // let the next kernel in the stream be scheduled as soon as every block of this one is
+  // resident, and wait here until the previous kernel has completed and its writes are
+  // visible — nothing before this line touches global memory.
+  if (p.pdl) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
   if (p.wait_flags) {  // rank-p2p: neighbours done with the previous phase
     if (threadIdx.x == 0) spin_until(p.wait_flags, 2, p.wait_value);
     __syncthreads();
@@ -797,8 +805,20 @@ cudaError_t launch_halfsweep_staged(int rule, int64_t slots, cudaStream_t st, Ha
   }
   const unsigned grid = (unsigned)(spans * bands);
   return dispatch_rule(rule, p.obs_out != nullptr, [&](auto R, auto O) {
-    k_halfsweep_staged<decltype(R)::value, decltype(O)::value><<<grid, 128, 0, st>>>(p);
-    return cudaGetLastError();
+    if (!p.pdl) {
+      k_halfsweep_staged<decltype(R)::value, decltype(O)::value><<<grid, 128, 0, st>>>(p);
+      return cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(128);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_halfsweep_staged<decltype(R)::value, decltype(O)::value>, p);
   });
 }
 

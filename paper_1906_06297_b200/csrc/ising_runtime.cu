@@ -176,6 +176,7 @@ struct ising_ctx {
                                            // than graph replay on B200 (grid barrier ~3 us)
   bool staged = true;                      // TMA-staged half-sweep (ISING_STAGED=0: off)
   bool guided_tail = !env_is_zero("ISING_TAIL");  // staged kernel: 8- / 4-row last waves
+  bool pdl = !env_is_zero("ISING_PDL");  // staged kernel: programmatic dependent launch
   // heat-bath variant 7 (ISING_HB_SYMMETRIC=0: off, for every handle type)
   bool symmetric_hb_enabled = !env_is_zero("ISING_HB_SYMMETRIC");
   bool draw_free_enabled = true;           // beta in {0, inf}: skip Philox (ISING_DRAW_FREE=0)
@@ -412,11 +413,13 @@ int run_halfsweep(ising_ctx* h, Slab& s, int c, int r_begin, int r_end, uint64_t
   }
   const bool prof = h->profiling && s.devi == 0 && h->kernel_launches < kMaxProfiledLaunches;
   if (prof) CU(cudaEventRecord(h->prof_events[2 * h->kernel_launches], d.stream));
-  if (h->staged && h->W % 256 == 0)
+  if (h->staged && h->W % 256 == 0) {
+    p.pdl = h->pdl ? 1 : 0;
     CU(launch_halfsweep_staged(kernel_variant(h),
                                h->guided_tail ? (int64_t)d.sms * d.staged_blocks_per_sm : 0, d.stream, p));
-  else
+  } else {
     CU(launch_halfsweep(kernel_variant(h), grid, d.stream, p));
+  }
   if (prof) {
     CU(cudaEventRecord(h->prof_events[2 * h->kernel_launches + 1], d.stream));
     ++h->kernel_launches;
