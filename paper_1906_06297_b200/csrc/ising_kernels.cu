@@ -408,6 +408,22 @@ __device__ __forceinline__ void obs_word(uint64_t t, uint64_t n, uint64_t c, uin
   anti += __popcll(t15 ^ (n | (c << 1) | (s << 2) | (side << 3)));
 }
 
+// Launch with programmatic stream serialisation (the kernel itself calls
+// griddepcontrol.launch_dependents / griddepcontrol.wait before touching global memory).
+template <typename K>
+static cudaError_t launch_pdl(K kernel, unsigned grid, cudaStream_t st, const HalfSweepParams& p) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(128);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, p);
+}
+
 // One colour phase of one slab.  Work item = (band of H rows, 128-bit chunk
 // column q); the thread walks down the band keeping the N/C/S source chunks in
 // registers, so each source word is read from memory once per band (plus one halo
@@ -547,6 +563,10 @@ __device__ __forceinline__ void halfsweep_items(const HalfSweepParams& p, const 
 
 template <int RULE, bool OBS = false>
 __global__ void __launch_bounds__(128, ISING_MINB) k_halfsweep(const HalfSweepParams p) {
+  if (p.pdl) {  // programmatic dependent launch, as in k_halfsweep_staged
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
   if (p.wait_flags) {  // rank-p2p: neighbours done with the previous phase
     if (threadIdx.x == 0) spin_until(p.wait_flags, 2, p.wait_value);
     __syncthreads();
@@ -809,16 +829,7 @@ cudaError_t launch_halfsweep_staged(int rule, int64_t slots, cudaStream_t st, Ha
       k_halfsweep_staged<decltype(R)::value, decltype(O)::value><<<grid, 128, 0, st>>>(p);
       return cudaGetLastError();
     }
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(128);
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k_halfsweep_staged<decltype(R)::value, decltype(O)::value>, p);
+    return launch_pdl(k_halfsweep_staged<decltype(R)::value, decltype(O)::value>, grid, st, p);
   });
 }
 
@@ -924,8 +935,11 @@ cudaError_t launch_philox_probe(int grid, cudaStream_t st, const PhiloxKeys& K,
 
 cudaError_t launch_halfsweep(int rule, int grid, cudaStream_t st, const HalfSweepParams& p) {
   return dispatch_rule(rule, p.obs_out != nullptr, [&](auto R, auto O) {
-    k_halfsweep<decltype(R)::value, decltype(O)::value><<<grid, 128, 0, st>>>(p);
-    return cudaGetLastError();
+    if (!p.pdl) {
+      k_halfsweep<decltype(R)::value, decltype(O)::value><<<grid, 128, 0, st>>>(p);
+      return cudaGetLastError();
+    }
+    return launch_pdl(k_halfsweep<decltype(R)::value, decltype(O)::value>, grid, st, p);
   });
 }
 
