@@ -52,6 +52,20 @@ __device__ __forceinline__ uint64_t ld_nc(const uint64_t* p) {
 
 constexpr uint32_t kLane0 = 0x11111111u;  // bit 0 of every nibble of a 32-bit half
 
+// Side-word splices (reading R10) as funnel shifts on the 32-bit halves (two
+// SHF per word, no IMAD.SHL on the FMA pipe): west = (C << 4) | (L >> 60) with L the word to
+// the left, east = (C >> 4) | (R << 60) with R the word to the right.
+__device__ __forceinline__ uint64_t splice_west(uint64_t c, uint64_t l) {
+  const uint32_t lo = __funnelshift_l((uint32_t)(l >> 32), (uint32_t)c, 4);
+  const uint32_t hi = __funnelshift_l((uint32_t)c, (uint32_t)(c >> 32), 4);
+  return ((uint64_t)hi << 32) | lo;
+}
+__device__ __forceinline__ uint64_t splice_east(uint64_t c, uint64_t r) {
+  const uint32_t lo = __funnelshift_r((uint32_t)c, (uint32_t)(c >> 32), 4);
+  const uint32_t hi = __funnelshift_r((uint32_t)(c >> 32), (uint32_t)r, 4);
+  return ((uint64_t)hi << 32) | lo;
+}
+
 // One 64-bit target word: 16 spins of plane row `row` (global), plane columns
 // 4*ctr0 .. 4*ctr0 + 15.  n, c, s: source words above / same / below; side: the
 // spliced side word.  Metropolis acceptance:
@@ -78,11 +92,27 @@ __device__ __forceinline__ void nc_step(uint32_t& a3, uint32_t& a4, uint32_t r, 
       : "r"(r), "r"(t3), "r"(t4));
 }
 
-// Flip decision for 8 lanes (one 32-bit half).  With a = aligned neighbours, b = 4 - a
-// (anti-aligned), cnt = [r < T_3] + [r < T_4] and T_4 <= T_3, Metropolis flips iff
-// a - 2 <= cnt, i.e. iff b - nc >= 0 with nc = 2 - cnt = a3 + a4 (the Horner
-// accumulators).  Per lane x = b + 8 - nc lies in [6, 12]; bit 3 of x is the flip bit.
-//   b = s ? 4 - n : n  =  (n ^ 15 s) - 11 s   (n = neighbour sum, s = spin bit)
+// Flip decision for 8 lanes (one 32-bit half).  With b = number of neighbours anti-aligned
+// with the spin, cnt = [r < T_3] + [r < T_4] and T_4 <= T_3, Metropolis flips iff
+// a - 2 <= cnt (a = 4 - b aligned), i.e. iff b - nc >= 0 with nc = 2 - cnt = a3 + a4 (the
+// Horner accumulators).  Per lane x = b + 8 - nc lies in [6, 12]; bit 3 of x is the flip bit.
+// b per lane is the sum of the four XORs of the spin with its neighbours (lanes hold 0/1 in
+// bit 0, sums <= 4: no carries) — four LOP3 and two adds on the ALU pipe, where the
+// s ? 4 - n : n form of the up-neighbour count took two IMADs on the FMA pipe.
+#ifndef ISING_ANTI_XOR
+#define ISING_ANTI_XOR 0
+#endif
+__device__ __forceinline__ uint32_t anti8(uint32_t t, uint32_t n, uint32_t c, uint32_t s,
+                                          uint32_t side) {
+  return (t ^ n) + (t ^ c) + (t ^ s) + (t ^ side);
+}
+
+__device__ __forceinline__ uint32_t flip8(uint32_t t, uint32_t b, uint32_t nc) {
+  const uint32_t x = b + 0x88888888u - nc;
+  return t ^ ((x >> 3) & kLane0);
+}
+
+// (the up-count form, kept for the heat-bath kernels)
 __device__ __forceinline__ uint32_t accept8(uint32_t s, uint32_t n, uint32_t nc) {
   const uint32_t x = (n ^ (s * 15u)) + (s * (uint32_t)-11 + 0x88888888u) - nc;
   return s ^ ((x >> 3) & kLane0);
@@ -95,11 +125,18 @@ __device__ __forceinline__ uint64_t update_word_metropolis(uint64_t tgt, uint64_
                                                            uint64_t s, uint64_t side, uint32_t ctr0,
                                                            uint32_t row, uint32_t t, const HalfSweepParams& p) {
   constexpr bool kSingle = RULE == 0;
-  // "three additions are sufficient to compute the neighbors sums":
-  // lanes hold 0/1 and sums <= 4, so the 64-bit adds split into independent halves.
+  // "three additions are sufficient to compute the neighbors sums": here the
+  // sums of the XORs with the target (anti-aligned neighbours); lanes hold 0/1 and sums <= 4,
+  // so the 64-bit adds split into independent 32-bit halves.
+#if ISING_ANTI_XOR
+  const uint32_t b_lo = anti8((uint32_t)tgt, (uint32_t)n, (uint32_t)c, (uint32_t)s, (uint32_t)side);
+  const uint32_t b_hi = anti8((uint32_t)(tgt >> 32), (uint32_t)(n >> 32), (uint32_t)(c >> 32),
+                              (uint32_t)(s >> 32), (uint32_t)(side >> 32));
+#else
   const uint32_t sum_lo = (uint32_t)n + (uint32_t)c + (uint32_t)s + (uint32_t)side;
   const uint32_t sum_hi =
       (uint32_t)(n >> 32) + (uint32_t)(c >> 32) + (uint32_t)(s >> 32) + (uint32_t)(side >> 32);
+#endif
   const uint32_t t3 = p.acc.thr[3], t4 = p.acc.thr[4];
   // lanes k = 4b + q; Horner order is lane 7 .. 0 (lo half) and 15 .. 8 (hi half)
   uint32_t a3lo = 0, a4lo = 0, a3hi = 0, a4hi = 0;
@@ -137,8 +174,13 @@ __device__ __forceinline__ uint64_t update_word_metropolis(uint64_t tgt, uint64_
     nclo = (a3lo & k3) + (a4lo & k4);
     nchi = (a3hi & k3) + (a4hi & k4);
   }
+#if ISING_ANTI_XOR
+  const uint32_t lo = flip8((uint32_t)tgt, b_lo, nclo);
+  const uint32_t hi = flip8((uint32_t)(tgt >> 32), b_hi, nchi);
+#else
   const uint32_t lo = accept8((uint32_t)tgt, sum_lo, nclo);
   const uint32_t hi = accept8((uint32_t)(tgt >> 32), sum_hi, nchi);
+#endif
   return ((uint64_t)hi << 32) | lo;
 }
 
@@ -533,9 +575,9 @@ __device__ __forceinline__ void halfsweep_items(const HalfSweepParams& p, const 
 #pragma unroll
       for (int k = 0; k < kWords; ++k) {
         if (west)
-          side[k] = (cv[k] << 4) | ((k == 0 ? sw : cv[k - 1]) >> 60);
+          side[k] = splice_west(cv[k], k == 0 ? sw : cv[k - 1]);
         else
-          side[k] = (cv[k] >> 4) | ((k == kWords - 1 ? sw : cv[k + 1]) << 60);
+          side[k] = splice_east(cv[k], k == kWords - 1 ? sw : cv[k + 1]);
       }
 #pragma unroll
       for (int k = 0; k < kWords; ++k) {
@@ -743,7 +785,8 @@ __global__ void __launch_bounds__(128, ISING_MINB) k_halfsweep_staged(const Half
   const int tid = threadIdx.x;
   const int64_t wc = w0 + 2 * tid;
   uint32_t obs_up = 0, obs_anti = 0;
-  for (int rr = 0; rr < nrows; ++rr) {
+  uint64_t* tp = tgt + (int64_t)ra * W + wc;  // target chunk of row r, advanced by W per row
+  for (int rr = 0; rr < nrows; ++rr, tp += W) {
     const int r = ra + rr;
     const int64_t gi = p.row0 + r;
     const bool west = ((gi & 1) == 0) == (p.colour == 0);
@@ -753,14 +796,13 @@ __global__ void __launch_bounds__(128, ISING_MINB) k_halfsweep_staged(const Half
     uint64_t side0, side1;
     if (west) {
       const uint64_t wl = tid == 0 ? edge[rr + 1][0] : tile[rr + 1][2 * tid - 1];
-      side0 = (c0 << 4) | (wl >> 60);
-      side1 = (c1 << 4) | (c0 >> 60);
+      side0 = splice_west(c0, wl);
+      side1 = splice_west(c1, c0);
     } else {
       const uint64_t er = tid == 127 ? edge[rr + 1][1] : tile[rr + 1][2 * tid + 2];
-      side0 = (c0 >> 4) | (c1 << 60);
-      side1 = (c1 >> 4) | (er << 60);
+      side0 = splice_east(c0, c1);
+      side1 = splice_east(c1, er);
     }
-    uint64_t* tp = tgt + (int64_t)r * W + wc;
     ulonglong2 tv = *reinterpret_cast<const ulonglong2*>(tp);
     const uint32_t ctr0 = (uint32_t)(4 * wc);
     tv.x = update_word<RULE>(tv.x, n0, c0, s0, side0, ctr0, (uint32_t)gi, t, p);
