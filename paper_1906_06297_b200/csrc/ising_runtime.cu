@@ -131,6 +131,18 @@ struct Slab {
 
 }  // namespace
 
+// One ising_sweep_measure_async call whose results are still in flight.
+struct PendingMeasure {
+  int64_t ticket = -1;  // -1: free slot
+  int64_t* up = nullptr;
+  int64_t* energy = nullptr;
+  int64_t n = 0;
+  bool ready = false;   // completed synchronously (fallback path): nothing to wait for
+  double ms = 0;
+  cudaEvent_t t0 = nullptr, t1 = nullptr, done = nullptr;
+};
+constexpr int kMaxPending = 8;
+
 struct ising_ctx {
   int64_t N = 0, M = 0, W = 0;
   uint64_t seed = 0;
@@ -185,6 +197,8 @@ struct ising_ctx {
   // basic byte-per-spin layout (ising_create_basic; §3.1)
   bool basic = false;
   int8_t* bplane[2] = {nullptr, nullptr};
+  PendingMeasure pending[kMaxPending];
+  int64_t next_ticket = 0;
 };
 
 namespace {
@@ -327,6 +341,9 @@ void destroy_ctx(ising_ctx* h) {
     if (d.comm) cudaStreamDestroy(d.comm);
   }
   for (cudaEvent_t e : h->prof_events) cudaEventDestroy(e);
+  for (auto& pm : h->pending)
+    for (cudaEvent_t e : {pm.t0, pm.t1, pm.done})
+      if (e) cudaEventDestroy(e);
   if (h->gexec) cudaGraphExecDestroy(h->gexec);
   for (int c = 0; c < 2; ++c)
     if (h->bplane[c]) cudaFree(h->bplane[c]);
@@ -1495,23 +1512,10 @@ int ising_observables(ising_t h, int64_t* up_count, int64_t* bond_energy) {
   return ISING_OK;
 }
 
-int ising_sweep_measure(ising_t h, int64_t n_samples, int64_t every, int64_t* up_counts,
-                        int64_t* bond_energies) {
-  if (!h || n_samples < 0 || every < 1 || (n_samples > 0 && (!up_counts || !bond_energies)))
-    return ISING_ERR_ARG;
-  if (!h->beta_set || !h->state_set) return ISING_ERR_STATE;
-  if (h->t + (uint64_t)(n_samples * every) > 0xffffffffull) return ISING_ERR_RANGE;
-  if ((h->rank_mode && h->world > 1) || h->basic) {
-    // rank mode: the observables need the cross-rank all-reduce per sample
-    double total = 0;
-    for (int64_t k = 0; k < n_samples; ++k) {
-      TRY(ising_sweep(h, every));
-      total += h->last_ms;
-      TRY(ising_observables(h, &up_counts[k], &bond_energies[k]));
-    }
-    h->last_ms = total;
-    return ISING_OK;
-  }
+// Enqueue n_samples x `every` sweeps with the observables of every sample's white phase
+// reduced into each device's meas buffer ([up, antiparallel] per sample), bracketed by the
+// devices' ev_t0 / ev_t1 events.  Single-process handles (not rank mode, not basic).
+static int measure_enqueue(ising_ctx* h, int64_t n_samples, int64_t every) {
   const size_t need = (size_t)std::max<int64_t>(n_samples, 1) * 2;
   std::vector<unsigned long long*> base;
   for (auto& d : h->devs) {
@@ -1558,6 +1562,28 @@ int ising_sweep_measure(ising_t h, int64_t n_samples, int64_t every, int64_t* up
     CU(cudaSetDevice(d.dev));
     CU(cudaEventRecord(d.ev_t1, d.stream));
   }
+  return ISING_OK;
+}
+
+int ising_sweep_measure(ising_t h, int64_t n_samples, int64_t every, int64_t* up_counts,
+                        int64_t* bond_energies) {
+  if (!h || n_samples < 0 || every < 1 || (n_samples > 0 && (!up_counts || !bond_energies)))
+    return ISING_ERR_ARG;
+  if (!h->beta_set || !h->state_set) return ISING_ERR_STATE;
+  if (h->t + (uint64_t)(n_samples * every) > 0xffffffffull) return ISING_ERR_RANGE;
+  if ((h->rank_mode && h->world > 1) || h->basic) {
+    // rank mode: the observables need the cross-rank all-reduce per sample
+    double total = 0;
+    for (int64_t k = 0; k < n_samples; ++k) {
+      TRY(ising_sweep(h, every));
+      total += h->last_ms;
+      TRY(ising_observables(h, &up_counts[k], &bond_energies[k]));
+    }
+    h->last_ms = total;
+    return ISING_OK;
+  }
+  TRY(measure_enqueue(h, n_samples, every));
+  const size_t need = (size_t)std::max<int64_t>(n_samples, 1) * 2;
   TRY(sync_all(h));
   double mx = 0;
   std::vector<unsigned long long> host(need);
@@ -1575,6 +1601,73 @@ int ising_sweep_measure(ising_t h, int64_t n_samples, int64_t every, int64_t* up
   }
   for (int64_t k = 0; k < n_samples; ++k) bond_energies[k] = 2 * bond_energies[k] - 2 * h->N * h->M;
   h->last_ms = mx;
+  return ISING_OK;
+}
+
+int ising_sweep_measure_async(ising_t h, int64_t n_samples, int64_t every, int64_t* up_counts,
+                              int64_t* bond_energies, int64_t* ticket) {
+  if (!h || !ticket || n_samples < 0 || every < 1 ||
+      (n_samples > 0 && (!up_counts || !bond_energies)))
+    return ISING_ERR_ARG;
+  if (!h->beta_set || !h->state_set) return ISING_ERR_STATE;
+  if (h->t + (uint64_t)(n_samples * every) > 0xffffffffull) return ISING_ERR_RANGE;
+  PendingMeasure* pm = nullptr;
+  for (auto& q : h->pending)
+    if (q.ticket < 0) {
+      pm = &q;
+      break;
+    }
+  if (!pm) {
+    g_last_error = "ising_sweep_measure_async: more than 8 calls pending";
+    return ISING_ERR_STATE;
+  }
+  pm->up = up_counts;
+  pm->energy = bond_energies;
+  pm->n = n_samples;
+  pm->ready = false;
+  if ((h->rank_mode && h->world > 1) || h->basic || h->devs.size() > 1 || n_samples == 0) {
+    // cross-device reductions: the synchronous path, complete on return
+    TRY(ising_sweep_measure(h, n_samples, every, up_counts, bond_energies));
+    pm->ready = true;
+    pm->ms = h->last_ms;
+  } else {
+    Device& d = h->devs[0];
+    CU(cudaSetDevice(d.dev));
+    for (cudaEvent_t* e : {&pm->t0, &pm->t1, &pm->done})
+      if (!*e) CU(cudaEventCreate(e));
+    CU(cudaEventRecord(pm->t0, d.stream));
+    TRY(measure_enqueue(h, n_samples, every));
+    CU(cudaEventRecord(pm->t1, d.stream));
+    // the two columns of [up, antiparallel] pairs straight into the caller's arrays
+    CU(cudaMemcpy2DAsync(up_counts, sizeof(int64_t), d.meas, 2 * sizeof(unsigned long long),
+                         sizeof(int64_t), (size_t)n_samples, cudaMemcpyDeviceToHost, d.stream));
+    CU(cudaMemcpy2DAsync(bond_energies, sizeof(int64_t), d.meas + 1,
+                         2 * sizeof(unsigned long long), sizeof(int64_t), (size_t)n_samples,
+                         cudaMemcpyDeviceToHost, d.stream));
+    CU(cudaEventRecord(pm->done, d.stream));
+  }
+  pm->ticket = h->next_ticket++;
+  *ticket = pm->ticket;
+  return ISING_OK;
+}
+
+int ising_measure_wait(ising_t h, int64_t ticket) {
+  if (!h) return ISING_ERR_ARG;
+  PendingMeasure* pm = nullptr;
+  for (auto& q : h->pending)
+    if (q.ticket >= 0 && q.ticket == ticket) pm = &q;
+  if (!pm) return ISING_ERR_ARG;
+  if (!pm->ready) {
+    CU(cudaSetDevice(h->devs[0].dev));
+    CU(cudaEventSynchronize(pm->done));
+    for (int64_t k = 0; k < pm->n; ++k)  // antiparallel bonds -> bond energy (Eq. 1, R11)
+      pm->energy[k] = 2 * pm->energy[k] - 2 * h->N * h->M;
+    float ms = 0;
+    CU(cudaEventElapsedTime(&ms, pm->t0, pm->t1));
+    pm->ms = ms;
+  }
+  h->last_ms = pm->ms;
+  pm->ticket = -1;
   return ISING_OK;
 }
 

@@ -52,6 +52,8 @@ SIGNATURES = {
     "ising_observables": (_INT, [_VP, _I64P, _I64P]),
     "ising_read_rows": (_INT, [_VP, _I64, _I64, _VP, _I64]),
     "ising_sweep_measure": (_INT, [_VP, _I64, _I64, _I64P, _I64P]),
+    "ising_sweep_measure_async": (_INT, [_VP, _I64, _I64, _I64P, _I64P, _I64P]),
+    "ising_measure_wait": (_INT, [_VP, _I64]),
     "ising_last_sweep_ms": (_INT, [_VP, _DBLP]),
     "ising_set_profiling": (_INT, [_VP, _INT]),
     "ising_kernel_stats": (_INT, [_VP, _DBLP, _I64P]),
@@ -228,6 +230,29 @@ def ising_sweep_measure(h: int, n_samples: int, every: int) -> tuple[np.ndarray,
     return ups, Es
 
 
+def _i64_out(a: np.ndarray, n: int, name: str) -> np.ndarray:
+    if a.dtype != np.int64 or not a.flags["C_CONTIGUOUS"] or a.size < n:
+        raise ValueError(f"{name}: need a C-contiguous int64 array of at least {n} entries")
+    return a
+
+
+def ising_sweep_measure_async(h: int, n_samples: int, every: int, ups: np.ndarray,
+                              Es: np.ndarray) -> int:
+    """Enqueue a measured chain; `ups` / `Es` (caller-owned, ideally pinned, e.g. numpy views
+    of torch pinned tensors) are valid after ising_measure_wait(h, ticket)."""
+    _i64_out(ups, n_samples, "ups")
+    _i64_out(Es, n_samples, "Es")
+    ticket = ctypes.c_int64(0)
+    _check(load().ising_sweep_measure_async(h, int(n_samples), int(every),
+                                            ups.ctypes.data_as(_I64P), Es.ctypes.data_as(_I64P),
+                                            ctypes.byref(ticket)), "ising_sweep_measure_async")
+    return ticket.value
+
+
+def ising_measure_wait(h: int, ticket: int) -> None:
+    _check(load().ising_measure_wait(h, int(ticket)), "ising_measure_wait")
+
+
 def ising_last_sweep_ms(h: int) -> float:
     v = _DBL()
     _check(load().ising_last_sweep_ms(h, ctypes.byref(v)), "ising_last_sweep_ms")
@@ -392,6 +417,14 @@ class IsingLattice:
     def measure(self, n_samples: int, every: int = 1) -> tuple[np.ndarray, np.ndarray]:
         """(up_count, bond_energy) after every `every` sweeps, n_samples times."""
         return ising_sweep_measure(self.h, n_samples, every)
+
+    def measure_async(self, n_samples: int, every: int, ups: np.ndarray, Es: np.ndarray) -> int:
+        """Enqueue `n_samples` x `every` sweeps with observables into ups / Es; returns a
+        ticket for measure_wait (the arrays are undefined until then)."""
+        return ising_sweep_measure_async(self.h, n_samples, every, ups, Es)
+
+    def measure_wait(self, ticket: int) -> None:
+        ising_measure_wait(self.h, ticket)
 
     def read_lattice(self, out=None) -> np.ndarray:
         if out is None:

@@ -4,6 +4,7 @@ import numpy as np
 import pytest
 
 from oracle import exact
+from paper_1906_06297_b200 import ising
 from paper_1906_06297_b200.ising import IsingLattice
 from tests import cases
 
@@ -76,3 +77,59 @@ def test_measured_chain_matches_oracle_series():
             ou, oE = o.chain(ns * every)
             assert np.array_equal(ups, ou[every - 1::every]) and np.array_equal(Es, oE[every - 1::every])
             assert g.t == o.t
+
+
+def test_async_measured_chain_matches_oracle_series():
+    # ising_sweep_measure_async: pipelined calls (enqueue k + 1, then wait for k) give the
+    # oracle's series sample by sample, into pinned host memory; interleaved plain sweeps
+    # keep stream order; graph-replayed and direct paths; slabs on one device; a basic-layout
+    # handle takes the synchronous fallback
+    import oracle
+    import torch
+
+    for N, M, every, slabs, ns, calls in [(64, 64, 1, None, 5, 12), (128, 192, 3, [0, 0], 4, 6),
+                                          (34, 8192, 1, None, 1, 9), (64, 64, 1, None, 70, 2)]:
+        g = IsingLattice(N, M, 6, devices=slabs).set_beta(0.4406868).init_random()
+        o = oracle.Lattice(N, M, 6).set_beta(0.4406868).init_random()
+        ups = torch.zeros((calls, ns), dtype=torch.int64).pin_memory().numpy()
+        Es = torch.zeros((calls, ns), dtype=torch.int64).pin_memory().numpy()
+        tickets = []
+        for k in range(calls):
+            if k == calls // 2:
+                g.sweep(2)  # a plain sweep between async calls (stream-ordered)
+            tickets.append(g.measure_async(ns, every, ups[k], Es[k]))
+            if k >= 1:
+                g.measure_wait(tickets[k - 1])
+        g.measure_wait(tickets[-1])
+        for k in range(calls):
+            if k == calls // 2:
+                o.sweep(2)
+            ou, oE = o.chain(ns * every)
+            assert np.array_equal(ups[k], ou[every - 1::every]), (N, M, k)
+            assert np.array_equal(Es[k], oE[every - 1::every]), (N, M, k)
+        assert g.t == o.t
+        assert np.array_equal(g.read_lattice(), o.full())
+        g.close()
+    b = IsingLattice.basic(64, 64, 6).set_beta(0.3).init_random()
+    ob = oracle.Lattice(64, 64, 6).set_beta(0.3).init_random()
+    u = np.zeros(3, dtype=np.int64)
+    e = np.zeros(3, dtype=np.int64)
+    b.measure_wait(b.measure_async(3, 2, u, e))
+    ou, oE = ob.chain(6)
+    assert np.array_equal(u, ou[1::2]) and np.array_equal(e, oE[1::2])
+
+
+def test_async_measure_errors():
+    g = IsingLattice(64, 64, 1).set_beta(0.3).init_random()
+    bufs = [(np.zeros(1, dtype=np.int64), np.zeros(1, dtype=np.int64)) for _ in range(9)]
+    tickets = [g.measure_async(1, 1, u, e) for u, e in bufs[:8]]
+    with pytest.raises(ising.IsingError) as err:  # a ninth pending call
+        g.measure_async(1, 1, *bufs[8])
+    assert err.value.status == ising.ISING_ERR_STATE
+    for t in tickets:
+        g.measure_wait(t)
+    with pytest.raises(ising.IsingError) as err:  # already waited for / unknown
+        g.measure_wait(tickets[0])
+    assert err.value.status == ising.ISING_ERR_ARG
+    with pytest.raises(ValueError):
+        g.measure_async(2, 1, np.zeros(1, dtype=np.int64), np.zeros(2, dtype=np.int64))
