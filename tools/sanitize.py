@@ -1,7 +1,7 @@
 """Small workloads for compute-sanitizer (memcheck / racecheck / synccheck / initcheck): C1,
 virtual slabs with R = 2, heat bath (0 / 1 / 2 "always" classes), draw-free, the TMA-staged
 kernel (shared memory + mbarrier, ragged band), both basic-layout kernels, measured chain,
-graph replay."""
+graph replay, the asynchronous measured chain, and (SANITIZE_BIG=1) the guided tail."""
 import os
 import sys
 
@@ -38,3 +38,14 @@ print("basic listing", b.observables())
 w = IsingLattice(64, 128, 5).write_lattice(np.ones((64, 128), dtype=np.int8), t=3).set_beta(0.0)
 w.sweep(1)
 print("write", w.observables(), w.read_rows(10, 2).sum())
+a = IsingLattice(64, 64, 7).set_beta(0.4406868).init_random()  # asynchronous measured chain
+bufs = [np.zeros(3, dtype=np.int64) for _ in range(4)]
+t1 = a.measure_async(3, 1, bufs[0], bufs[1])
+t2 = a.measure_async(3, 1, bufs[2], bufs[3])
+a.measure_wait(t1)
+a.measure_wait(t2)
+print("async", bufs[1].tolist(), bufs[3].tolist(), "variant", h.kernel_variant())
+if os.environ.get("SANITIZE_BIG"):  # >= 3 waves: the staged kernel's guided tail (memcheck)
+    big = IsingLattice(7168, 32768, 9).set_beta(0.4406868).init_random()
+    big.sweep(1)
+    print("tail", big.observables())
