@@ -716,10 +716,6 @@ __global__ void __launch_bounds__(128, ISING_MINB) k_halfsweep_staged(const Half
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
   }
-  if (p.wait_flags) {  // rank-p2p: neighbours done with the previous phase
-    if (threadIdx.x == 0) spin_until(p.wait_flags, 2, p.wait_value);
-    __syncthreads();
-  }
   __shared__ alignas(128) uint64_t tile[kStageRows + 2][kStageWords];
   __shared__ uint64_t edge[kStageRows + 2][2];
   __shared__ alignas(8) uint64_t mbar;
@@ -741,6 +737,14 @@ __global__ void __launch_bounds__(128, ISING_MINB) k_halfsweep_staged(const Half
     rb = min(ra + p.tail_h2, p.r_end);
   }
   const int nrows = rb - ra;
+  // rank-p2p: only the bands at the slab edges depend on the neighbours — they read the halo
+  // rows the neighbours stored in the previous phase and store rows 0 / R - 1 into halo rows
+  // the neighbours read in it — so only their blocks wait for both neighbours to finish that
+  // phase; interior blocks touch this slab's own rows only (ordered by the stream)
+  if (p.wait_flags && (ra == 0 || rb == p.R)) {
+    if (threadIdx.x == 0) spin_until(p.wait_flags, 2, p.wait_value);
+    __syncthreads();
+  }
   const uint64_t* src = p.src + W;  // local row r at src + r * W
   uint64_t* tgt = p.tgt + W;
   const uint32_t bar = smem_u32(&mbar);

@@ -65,7 +65,9 @@ def _worker(rank, world, port, N, M, seed, beta, plan, transport, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,N,M", [(2, 64, 128), (4, 128, 64), (2, 4, 64)])
+# (x, 8192) widths run the TMA-staged kernel, whose interior bands skip the neighbour wait
+@pytest.mark.parametrize("world,N,M", [(2, 64, 128), (4, 128, 64), (2, 4, 64), (2, 128, 8192),
+                                      (4, 48, 8192)])
 def test_rank_p2p_matches_oracle(world, N, M):
     import oracle
 
