@@ -38,6 +38,11 @@ PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 BYTES_PER_FLIP = 1.5  # 4-bit spins: read target + read source + write target
 MULWIDE_PER_FLIP = 4.0  # per-thread 32x32->64 multiplies per draw (16 per Philox block / 4, R6)
 TRAFFIC_FILE = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+# PAPER.md Table 2 (multi-spin kernel, one V100-SXM): lattice -> (flips/ns, line)
+PAPER_TABLE2 = {(2048, 2048): (231.09, "P:277"), (4096, 4096): (318.95, "P:278"),
+                (8192, 8192): (379.27, "P:279"), (16384, 16384): (411.65, "P:280"),
+                (32768, 32768): (420.44, "P:281"), (65536, 65536): (420.77, "P:282"),
+                (131072, 131072): (418.23, "P:283")}
 
 
 def ncu_traffic(config: str, n: int):
@@ -410,6 +415,9 @@ def run_ours(args):
     if rank == 0 and n == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(M)
 
+    # The paper's single-GPU number for this exact lattice, if Table 2 has one (BASELINE.md:
+    # one V100-SXM of a DGX-2; another machine's number — context, not the target).
+    paper = PAPER_TABLE2.get((N, M)) if (n == 1 and not basic) else None
     if rank == 0:
         line = {
             "metric": "spin flips/ns (device-timed)",
@@ -421,7 +429,9 @@ def run_ours(args):
             "ms_per_step": ms / args.steps,
             "higher_is_better": True,
             "scaling": scaling,
-            "vs_baseline": None,
+            "vs_baseline": (value / paper[0]) if paper else None,
+            "baseline": ({"value": paper[0], "unit": "flips/ns", "hardware": "1x V100-SXM (DGX-2)",
+                          "source": f"BASELINE.md Table 2, PAPER.md {paper[1]}"} if paper else None),
             "dtype": "u32",
             "data": "synthetic",
             "config": {
