@@ -267,6 +267,104 @@ __global__ void k_basic_init(int8_t* black, int8_t* white, int64_t nx, int64_t n
 }
 
 // Up count and antiparallel bonds (every bond has one black end: its 4 white neighbours).
+// Vectorised observables (ny % 16 == 0): one thread per 16 black sites of a row, loaded as
+// uint4 together with the white N / C / S words; the side neighbours (j - 1 for even rows, j + 1
+// for odd, Fig. 2 listing) are byte funnel shifts of the C words with the word beyond
+// the chunk.  +-1 bytes differ iff bit 1 differs, so popcounts of (x ^ y) & 0x02020202 count
+// antiparallel bonds; up spins are bytes with bit 1 clear.  Rows are walked with a 2D
+// grid-stride (no 64-bit divisions).
+__global__ void __launch_bounds__(256) k_basic_observables16(const int8_t* black,
+                                                             const int8_t* white, int64_t nx,
+                                                             int64_t ny, unsigned long long* out) {
+  const int64_t chunks = ny >> 4;
+  uint32_t up = 0, anti = 0;  // per thread: <= 4 bonds + 2 spins per site, few chunks
+  unsigned long long up64 = 0, anti64 = 0;
+  for (int64_t i = blockIdx.y; i < nx; i += gridDim.y) {
+    const int64_t inn = i == 0 ? nx - 1 : i - 1, ipp = i + 1 == nx ? 0 : i + 1;
+    const int8_t* wrow = white + i * ny;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < chunks;
+         q += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t j0 = 16 * q;
+      const uint4 b = *reinterpret_cast<const uint4*>(black + i * ny + j0);
+      const uint4 wn = *reinterpret_cast<const uint4*>(white + inn * ny + j0);
+      const uint4 wc = *reinterpret_cast<const uint4*>(wrow + j0);
+      const uint4 ws = *reinterpret_cast<const uint4*>(white + ipp * ny + j0);
+      const uint32_t bb[4] = {b.x, b.y, b.z, b.w}, n[4] = {wn.x, wn.y, wn.z, wn.w};
+      const uint32_t c[4] = {wc.x, wc.y, wc.z, wc.w}, sd[4] = {ws.x, ws.y, ws.z, ws.w};
+      uint32_t side[4];
+      if (i & 1) {  // east: bytes j + 1 .. j + 16
+        const uint32_t e = *reinterpret_cast<const uint32_t*>(wrow + (j0 + 16 == ny ? 0 : j0 + 16));
+        side[0] = __funnelshift_r(c[0], c[1], 8);
+        side[1] = __funnelshift_r(c[1], c[2], 8);
+        side[2] = __funnelshift_r(c[2], c[3], 8);
+        side[3] = __funnelshift_r(c[3], e, 8);
+      } else {  // west: bytes j - 1 .. j + 14
+        const uint32_t w = *reinterpret_cast<const uint32_t*>(wrow + (j0 == 0 ? ny - 4 : j0 - 4));
+        side[0] = __funnelshift_l(w, c[0], 8);
+        side[1] = __funnelshift_l(c[0], c[1], 8);
+        side[2] = __funnelshift_l(c[1], c[2], 8);
+        side[3] = __funnelshift_l(c[2], c[3], 8);
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        up += __popc(~bb[k] & kByteDown) + __popc(~c[k] & kByteDown);
+        anti += __popc((bb[k] ^ n[k]) & kByteDown) + __popc((bb[k] ^ c[k]) & kByteDown) +
+                __popc((bb[k] ^ sd[k]) & kByteDown) + __popc((bb[k] ^ side[k]) & kByteDown);
+      }
+    }
+    up64 += up;
+    anti64 += anti;
+    up = anti = 0;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    up64 += __shfl_xor_sync(0xffffffffu, up64, off);
+    anti64 += __shfl_xor_sync(0xffffffffu, anti64, off);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&out[0], up64);
+    atomicAdd(&out[1], anti64);
+  }
+}
+
+// Vectorised conversion (ny % 8 == 0): one thread per 16 bytes of a full row = 8 sites of each
+// plane; full byte J = 2 j + x comes from colour (i + x) & 1, so the row is a byte interleave
+// of the two planes' 8-byte segments (PRMT both ways).
+__global__ void __launch_bounds__(256) k_basic_convert16(int8_t* black, int8_t* white, int8_t* full,
+                                                         int64_t ny, int64_t r0, int64_t rows,
+                                                         int to_full, unsigned int* bad) {
+  const int64_t M = 2 * ny;
+  const int64_t segs = M >> 4;
+  unsigned int badv = 0;
+  for (int64_t li = blockIdx.y; li < rows; li += gridDim.y) {
+    const int64_t i = r0 + li;
+    int8_t* pa = ((i & 1) ? white : black) + i * ny;  // even full columns
+    int8_t* pb = ((i & 1) ? black : white) + i * ny;  // odd full columns
+    for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < segs;
+         u += (int64_t)gridDim.x * blockDim.x) {
+      uint4* f = reinterpret_cast<uint4*>(full + li * M + 16 * u);
+      uint2* a = reinterpret_cast<uint2*>(pa + 8 * u);
+      uint2* b = reinterpret_cast<uint2*>(pb + 8 * u);
+      if (to_full) {
+        const uint2 A = *a, B = *b;
+        *f = make_uint4(__byte_perm(A.x, B.x, 0x5140), __byte_perm(A.x, B.x, 0x7362),
+                        __byte_perm(A.y, B.y, 0x5140), __byte_perm(A.y, B.y, 0x7362));
+      } else {
+        const uint4 o = *f;
+        const uint32_t w[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {  // every byte must be 0x01 or 0xFF
+          const uint32_t y = w[k] ^ 0x01010101u;
+          badv |= (y & 0x01010101u) | (((y >> 1) ^ y) & 0x7E7E7E7Eu);
+        }
+        *a = make_uint2(__byte_perm(o.x, o.y, 0x6420), __byte_perm(o.z, o.w, 0x6420));
+        *b = make_uint2(__byte_perm(o.x, o.y, 0x7531), __byte_perm(o.z, o.w, 0x7531));
+      }
+    }
+  }
+  if (badv) atomicOr(bad, 1u);
+}
+
 __global__ void __launch_bounds__(256) k_basic_observables(const int8_t* black, const int8_t* white,
                                                            int64_t nx, int64_t ny,
                                                            unsigned long long* out) {
@@ -354,14 +452,28 @@ cudaError_t launch_basic_init(int grid, cudaStream_t st, int8_t* black, int8_t* 
 cudaError_t launch_basic_observables(int grid, cudaStream_t st, const int8_t* black,
                                      const int8_t* white, int64_t nx, int64_t ny,
                                      unsigned long long* out) {
-  k_basic_observables<<<grid, 256, 0, st>>>(black, white, nx, ny, out);
+  if ((ny & 15) == 0) {
+    const int64_t chunks = ny >> 4;
+    const unsigned gx = (unsigned)std::min<int64_t>((chunks + 255) / 256, 65535);
+    const unsigned gy = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nx, std::max(1, grid / (int)gx)));
+    k_basic_observables16<<<dim3(gx, gy), 256, 0, st>>>(black, white, nx, ny, out);
+  } else {
+    k_basic_observables<<<grid, 256, 0, st>>>(black, white, nx, ny, out);
+  }
   return cudaGetLastError();
 }
 
 cudaError_t launch_basic_convert(int grid, cudaStream_t st, int8_t* black, int8_t* white,
                                  int8_t* full, int64_t ny, int64_t r0, int64_t rows, int to_full,
                                  unsigned int* bad) {
-  k_basic_convert<<<grid, 256, 0, st>>>(black, white, full, ny, r0, rows, to_full, bad);
+  if ((ny & 7) == 0) {
+    const int64_t segs = ny >> 3;  // 16-byte segments of a full row
+    const unsigned gx = (unsigned)std::min<int64_t>((segs + 255) / 256, 65535);
+    const unsigned gy = (unsigned)std::max<int64_t>(1, std::min<int64_t>(rows, std::max(1, grid / (int)gx)));
+    k_basic_convert16<<<dim3(gx, gy), 256, 0, st>>>(black, white, full, ny, r0, rows, to_full, bad);
+  } else {
+    k_basic_convert<<<grid, 256, 0, st>>>(black, white, full, ny, r0, rows, to_full, bad);
+  }
   return cudaGetLastError();
 }
 
