@@ -1,5 +1,8 @@
-/* Plain-C use of the library (no Python, no PyTorch): the calls the north_star lists.
- *   ising_c_example L_rows L_cols seed beta sweeps   ->  prints "up E t"
+/* Plain-C use of the library (no Python, no PyTorch): the calls the north_star lists, then
+ * a measured chain through the asynchronous API (two calls in flight).
+ *   ising_c_example L_rows L_cols seed beta sweeps
+ *     -> line 1: "up E t sum" after `sweeps` sweeps
+ *        line 2: "up E" of 2 x 3 samples, one every 2 sweeps, via ising_sweep_measure_async
  * Built by __graft_entry__.build(); tests/test_gpu_capi.py runs it against the oracle. */
 #include <stdio.h>
 #include <stdlib.h>
@@ -39,6 +42,16 @@ int main(int argc, char** argv) {
   for (int64_t k = 0; k < N * M; ++k) sum += lat[k];
   printf("%lld %lld %llu %lld\n", (long long)up, (long long)E, (unsigned long long)t, sum);
   free(lat);
+  /* asynchronous measured chain: enqueue the second chunk before waiting for the first
+   * (host memory here is pageable; pinned memory makes the copies truly asynchronous) */
+  int64_t ups[2][3], Es[2][3], tk[2];
+  CHECK(ising_sweep_measure_async(h, 3, 2, ups[0], Es[0], &tk[0]));
+  CHECK(ising_sweep_measure_async(h, 3, 2, ups[1], Es[1], &tk[1]));
+  CHECK(ising_measure_wait(h, tk[0]));
+  CHECK(ising_measure_wait(h, tk[1]));
+  for (int c = 0; c < 2; ++c)
+    for (int k = 0; k < 3; ++k) printf("%lld %lld ", (long long)ups[c][k], (long long)Es[c][k]);
+  printf("\n");
   CHECK(ising_destroy(h));
   return 0;
 }

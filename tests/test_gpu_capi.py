@@ -19,7 +19,11 @@ def test_c_program_matches_oracle(N, M, seed, beta, sweeps):
     out = subprocess.run([EXE, str(N), str(M), str(seed), repr(beta), str(sweeps)],
                          capture_output=True, text=True, timeout=120)
     assert out.returncode == 0, out.stderr
-    up, E, t, total = (int(x) for x in out.stdout.split())
+    line1, line2 = out.stdout.strip().split("\n")
+    up, E, t, total = (int(x) for x in line1.split())
     o = oracle.Lattice(N, M, seed).init_random().set_beta(beta).sweep(sweeps)
     assert (up, E) == o.observables()
     assert t == sweeps and total == int(o.full().sum())
+    ou, oE = o.chain(12)  # the async chain: 2 calls x 3 samples, one every 2 sweeps
+    got = [int(x) for x in line2.split()]
+    assert got[0::2] == [int(x) for x in ou[1::2]] and got[1::2] == [int(x) for x in oE[1::2]]
