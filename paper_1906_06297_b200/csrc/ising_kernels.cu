@@ -697,9 +697,27 @@ cudaError_t launch_gather(cudaStream_t st, const GatherParams& p) {
 // per C3 half-sweep: the shared-memory reads replace the per-row global loads and their
 // address arithmetic); used whenever W is a multiple of 256 words (ISING_STAGED=0 opts out).
 #ifndef ISING_STAGE_ROWS
-#define ISING_STAGE_ROWS 16
+#define ISING_STAGE_ROWS 20  // 44 KB of source rows per block, 4 blocks per SM
 #endif
-constexpr int kStageRows = ISING_STAGE_ROWS;
+// __launch_bounds__ minimum blocks per SM of the staged kernel.  All of 2, 3, 4 give 118
+// registers (4 resident blocks), but ptxas schedules the Philox / carry-chain stream
+// differently: 3 measured 1524-1531 flips/ns on C3 against 1498 for 4 (profiles/
+// r01_ncu_halfsweep.md); the draw-free variant (RULE 4, memory-bound) keeps 4.
+#ifndef ISING_STAGED_MINB
+#define ISING_STAGED_MINB 3
+#endif
+#ifndef ISING_STAGED_MINB_DRAWFREE
+#define ISING_STAGED_MINB_DRAWFREE 4
+#endif
+__host__ __device__ constexpr int staged_minb(int rule) {
+  return rule == 4 ? ISING_STAGED_MINB_DRAWFREE : ISING_STAGED_MINB;
+}
+#ifndef ISING_STAGE_ROWS_DRAWFREE
+#define ISING_STAGE_ROWS_DRAWFREE 16  // memory-bound variant: 3341 vs 3027 flips/ns at 20 rows
+#endif
+__host__ __device__ constexpr int stage_rows(int rule) {
+  return rule == 4 ? ISING_STAGE_ROWS_DRAWFREE : ISING_STAGE_ROWS;
+}
 constexpr int kStageWords = 256;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -707,7 +725,8 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 }
 
 template <int RULE, bool OBS = false>
-__global__ void __launch_bounds__(128, ISING_MINB) k_halfsweep_staged(const HalfSweepParams p) {
+__global__ void __launch_bounds__(128, staged_minb(RULE)) k_halfsweep_staged(const HalfSweepParams p) {
+  constexpr int kRows = stage_rows(RULE);
   // Programmatic dependent launch (p.pdl: launched with programmatic stream serialisation):
   // let the next kernel in the stream be scheduled as soon as every block of this one is
   // resident, and wait here until the previous kernel has completed and its writes are
@@ -716,21 +735,21 @@ __global__ void __launch_bounds__(128, ISING_MINB) k_halfsweep_staged(const Half
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
   }
-  __shared__ alignas(128) uint64_t tile[kStageRows + 2][kStageWords];
-  __shared__ uint64_t edge[kStageRows + 2][2];
+  __shared__ alignas(128) uint64_t tile[kRows + 2][kStageWords];
+  __shared__ uint64_t edge[kRows + 2][2];
   __shared__ alignas(8) uint64_t mbar;
   const int64_t W = p.W;
   const int64_t bpr = W / kStageWords;  // blocks per band
   const int band = (int)(blockIdx.x / bpr);
   const int64_t w0 = (int64_t)(blockIdx.x - (int64_t)band * bpr) * kStageWords;
-  // bands of kStageRows rows; with a guided tail (tail_band8 > 0) the last bands are 8 and
+  // bands of kRows rows; with a guided tail (tail_band8 > 0) the last bands are 8 and
   // then 4 rows tall, so the partial last wave idles for a short block lifetime only
   int ra, rb;
   if (band < p.tail_band8 || p.tail_band8 == 0) {
-    ra = p.r_begin + band * kStageRows;
-    rb = min(ra + kStageRows, p.r_end);
+    ra = p.r_begin + band * kRows;
+    rb = min(ra + kRows, p.r_end);
   } else if (band < p.tail_band4) {
-    ra = p.r_begin + p.tail_band8 * kStageRows + (band - p.tail_band8) * p.tail_h1;
+    ra = p.r_begin + p.tail_band8 * kRows + (band - p.tail_band8) * p.tail_h1;
     rb = min(ra + p.tail_h1, p.r_begin + p.tail_row4);
   } else {
     ra = p.r_begin + p.tail_row4 + (band - p.tail_band4) * p.tail_h2;
@@ -851,6 +870,7 @@ __global__ void __launch_bounds__(128, ISING_MINB) k_halfsweep_staged(const Half
 // partial last wave costs about half a block lifetime per slot: 3.6 % on C3).
 cudaError_t launch_halfsweep_staged(int rule, int64_t slots, cudaStream_t st, HalfSweepParams p) {
   const int64_t rows = p.r_end - p.r_begin;
+  const int kStageRows = stage_rows(rule);  // band height of this rule's kernel
   const int64_t spans = p.W / kStageWords;
   int64_t bands = (rows + kStageRows - 1) / kStageRows;
   p.tail_band8 = p.tail_band4 = p.tail_row4 = 0;

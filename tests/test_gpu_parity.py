@@ -335,7 +335,7 @@ def test_persistent_kernel_path(monkeypatch):
 
 def test_tma_staged_kernel_path():
     # widths that are a multiple of 256 words use the TMA-staged half-sweep (cp.async.bulk
-    # + mbarrier into shared memory): ragged last band (40 = 16 + 16 + 8 rows), two slabs,
+    # + mbarrier into shared memory): ragged last band (34 = 20 + 14 rows), two slabs,
     # heat bath, measured chain
     for N, M, slabs in [(40, 8192, None), (64, 16384, [0, 0]), (34, 8192, None)]:
         g = gpu_lattice(N, M, 2, "random", 0.4406868, devices=slabs)
