@@ -703,6 +703,10 @@ cudaError_t launch_gather(cudaStream_t st, const GatherParams& p) {
 // registers (4 resident blocks), but ptxas schedules the Philox / carry-chain stream
 // differently: 3 measured 1524-1531 flips/ns on C3 against 1498 for 4 (profiles/
 // r01_ncu_halfsweep.md); the draw-free variant (RULE 4, memory-bound) keeps 4.
+#ifndef ISING_ROW_UNROLL
+#define ISING_ROW_UNROLL 1
+#endif
+constexpr int kRowUnroll = ISING_ROW_UNROLL;  // staged row loop unroll factor
 #ifndef ISING_STAGED_MINB
 #define ISING_STAGED_MINB 3
 #endif
@@ -809,6 +813,7 @@ __global__ void __launch_bounds__(128, staged_minb(RULE)) k_halfsweep_staged(con
   const int64_t wc = w0 + 2 * tid;
   uint32_t obs_up = 0, obs_anti = 0;
   uint64_t* tp = tgt + (int64_t)ra * W + wc;  // target chunk of row r, advanced by W per row
+#pragma unroll kRowUnroll
   for (int rr = 0; rr < nrows; ++rr, tp += W) {
     const int r = ra + rr;
     const int64_t gi = p.row0 + r;
