@@ -771,12 +771,12 @@ __global__ void __launch_bounds__(128, staged_minb(RULE)) k_halfsweep_staged(con
   const uint64_t* src = p.src + W;  // local row r at src + r * W
   uint64_t* tgt = p.tgt + W;
   const uint32_t bar = smem_u32(&mbar);
+  // One block barrier for the start-up: thread 0 initialises the mbarrier (the init fence
+  // orders it before the TMA's complete_tx) and issues the copies; warps 1-2 load the edge
+  // words meanwhile; the barrier below then orders the init before every thread's wait.
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
     const uint32_t bytes = (uint32_t)(nrows + 2) * kStageWords * 8;
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
                  : "memory");
@@ -790,11 +790,12 @@ __global__ void __launch_bounds__(128, staged_minb(RULE)) k_halfsweep_staged(con
   }
   // the word left of the span (west side of the first thread) and right of it (east side
   // of the last thread) for the band's rows, with the periodic wrap
-  if (threadIdx.x < 2 * nrows) {
-    const int rr = threadIdx.x >> 1;
-    const int64_t col = (threadIdx.x & 1) ? ((w0 + kStageWords == W) ? 0 : w0 + kStageWords)
-                                          : ((w0 == 0) ? W - 1 : w0 - 1);
-    edge[rr + 1][threadIdx.x & 1] = ld_nc(src + (int64_t)(ra + rr) * W + col);
+  if (threadIdx.x >= 32 && threadIdx.x < 32 + 2 * nrows) {
+    const int e = threadIdx.x - 32;
+    const int rr = e >> 1;
+    const int64_t col = (e & 1) ? ((w0 + kStageWords == W) ? 0 : w0 + kStageWords)
+                                : ((w0 == 0) ? W - 1 : w0 - 1);
+    edge[rr + 1][e & 1] = ld_nc(src + (int64_t)(ra + rr) * W + col);
   }
   __syncthreads();
   {
