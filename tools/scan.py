@@ -45,9 +45,21 @@ def main():
             g.close()
             m = (2 * ups - L * L) / (L * L)
             m2, m4 = float(np.mean(m ** 2)), float(np.mean(m ** 4))
+            # errors from 50 contiguous blocks: batch means for <|m|>, E; jackknife for U
+            nb = 50
+            blocks = np.array_split(np.arange(len(m)), nb)
+            am = np.array([np.mean(np.abs(m[b])) for b in blocks])
+            eb = np.array([np.mean(Es[b]) for b in blocks]) / (L * L)
+            b2 = np.array([np.mean(m[b] ** 2) for b in blocks])
+            b4 = np.array([np.mean(m[b] ** 4) for b in blocks])
+            jk = np.array([1 - (np.sum(b4) - b4[k]) / (nb - 1) /
+                           (3 * ((np.sum(b2) - b2[k]) / (nb - 1)) ** 2) for k in range(nb)])
             row = {"L": L, "T": T, "abs_m": float(np.mean(np.abs(m))), "onsager": onsager(T),
-                   "E_site": float(np.mean(Es)) / (L * L), "m2": m2, "m4": m4,
+                   "abs_m_se": float(np.std(am, ddof=1) / math.sqrt(nb)),
+                   "E_site": float(np.mean(Es)) / (L * L),
+                   "E_site_se": float(np.std(eb, ddof=1) / math.sqrt(nb)), "m2": m2, "m4": m4,
                    "binder": 1 - m4 / (3 * m2 * m2), "binder_paper_literal": 1 - m4 / (m2 * m2),
+                   "binder_se": float(math.sqrt((nb - 1) / nb * np.sum((jk - np.mean(jk)) ** 2))),
                    "samples": len(m), "seconds": time.perf_counter() - t0}
             rows.append(row)
             print(json.dumps(row), flush=True)
