@@ -337,7 +337,10 @@ def test_tma_staged_kernel_path():
     # widths that are a multiple of 256 words use the TMA-staged half-sweep (cp.async.bulk
     # + mbarrier into shared memory): ragged last band (34 = 20 + 14 rows), two slabs,
     # heat bath, measured chain
-    for N, M, slabs in [(40, 8192, None), (64, 16384, [0, 0]), (34, 8192, None)]:
+    # (4, 8192, [0, 0]): 2-row slabs, every row a boundary row; (2, 8192): N = 2, both halo rows
+    # are the other row
+    for N, M, slabs in [(40, 8192, None), (64, 16384, [0, 0]), (34, 8192, None), (4, 8192, [0, 0]),
+                        (2, 8192, None)]:
         g = gpu_lattice(N, M, 2, "random", 0.4406868, devices=slabs)
         o = oracle_lattice(N, M, 2, "random", 0.4406868)
         for n in [1, 3]:
