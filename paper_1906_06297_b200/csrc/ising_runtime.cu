@@ -521,9 +521,10 @@ int phase_rank(ising_ctx* h, int c, uint32_t t) {
 // One colour phase, RANK-P2P mode (world >= 2): the half-sweep kernel waits for the
 // neighbours' previous phase, stores its boundary rows straight into their halo rows
 // over NVLink, and its last block raises their flags — compute and exchange in one kernel.
-int phase_p2p(ising_ctx* h, int c, uint32_t t) {
+int phase_p2p(ising_ctx* h, int c, uint32_t t, unsigned long long* obs = nullptr) {
   Slab& s = h->slabs[0];
-  TRY(run_halfsweep(h, s, c, 0, (int)s.R, h->up_plane[c] + (s.R + 1) * h->W, h->dn_plane[c], t));
+  TRY(run_halfsweep(h, s, c, 0, (int)s.R, h->up_plane[c] + (s.R + 1) * h->W, h->dn_plane[c], t,
+                    false, obs));
   ++h->phase;
   return ISING_OK;
 }
@@ -862,7 +863,7 @@ int enqueue_sweeps(ising_ctx* h, int64_t n, const std::vector<unsigned long long
     const uint32_t t = (uint32_t)(h->t + (uint64_t)k);
     for (int c = 0; c < 2; ++c) {
       if (h->p2p && h->world > 1)
-        TRY(phase_p2p(h, c, t));
+        TRY(phase_p2p(h, c, t, (k == n && obs && c == 1) ? (*obs)[0] : nullptr));
       else if (h->rank_mode && h->world > 1)
         TRY(phase_rank(h, c, t));
       else
@@ -1571,8 +1572,44 @@ int ising_sweep_measure(ising_t h, int64_t n_samples, int64_t every, int64_t* up
     return ISING_ERR_ARG;
   if (!h->beta_set || !h->state_set) return ISING_ERR_STATE;
   if (h->t + (uint64_t)(n_samples * every) > 0xffffffffull) return ISING_ERR_RANGE;
+  if (h->p2p && h->world > 1) {
+    // rank-p2p: the sample's observables are fused into its last white phase (this slab's
+    // partials), then all-reduced over peer memory (k_gather) and read back; one host sync
+    // per sample keeps consecutive gathers of the shared slots apart
+    Device& d = h->devs[0];
+    CU(cudaSetDevice(d.dev));
+    double total = 0;
+    std::vector<unsigned long long*> red{d.red};
+    for (int64_t k = 0; k < n_samples; ++k) {
+      CU(cudaMemsetAsync(d.red, 0, 2 * sizeof(unsigned long long), d.stream));
+      CU(cudaEventRecord(d.ev_t0, d.stream));
+      TRY(enqueue_sweeps(h, every, &red));
+      CU(cudaEventRecord(d.ev_t1, d.stream));
+      GatherParams g{};
+      g.local = d.red;
+      for (int r = 0; r < h->world; ++r) g.slots[r] = h->peer_sync[r] + 8;
+      g.mine = h->sync + 8;
+      g.out = d.red;
+      g.world = h->world;
+      g.rank = h->rank;
+      g.epoch = ++h->gather_epoch;
+      CU(launch_gather(d.stream, g));
+      ++h->launch_count;
+      unsigned long long v[2];
+      CU(cudaMemcpyAsync(v, d.red, sizeof v, cudaMemcpyDeviceToHost, d.stream));
+      CU(cudaStreamSynchronize(d.stream));
+      float ms = 0;
+      CU(cudaEventElapsedTime(&ms, d.ev_t0, d.ev_t1));
+      total += ms;
+      up_counts[k] = (int64_t)v[0];
+      bond_energies[k] = 2 * (int64_t)v[1] - 2 * h->N * h->M;
+    }
+    h->last_ms = total;
+    return ISING_OK;
+  }
   if ((h->rank_mode && h->world > 1) || h->basic) {
-    // rank mode: the observables need the cross-rank all-reduce per sample
+    // rank-NCCL / basic layout: sweep, then the separate observables pass (all-reduced over
+    // NCCL in rank mode) per sample
     double total = 0;
     for (int64_t k = 0; k < n_samples; ++k) {
       TRY(ising_sweep(h, every));

@@ -56,6 +56,12 @@ def _worker(rank, world, port, N, M, seed, beta, plan, transport, q):
         parts = [torch.zeros((rows, M), dtype=torch.int8) for _ in range(world)]
         dist.all_gather(parts, torch.from_numpy(mine))
         out.append((lat.observables(), torch.cat(parts).numpy()))
+        # measured chain: observables fused into the white phases, all-reduced across ranks
+        ups, Es = lat.measure(3, 2)
+        u2 = np.zeros(2, dtype=np.int64)
+        e2 = np.zeros(2, dtype=np.int64)
+        lat.measure_wait(lat.measure_async(2, 1, u2, e2))
+        out.append((ups.tolist() + u2.tolist(), Es.tolist() + e2.tolist()))
         if rank == 0:
             q.put(("ok", out))
         lat.close()
@@ -94,3 +100,8 @@ def test_rank_p2p_matches_oracle(world, N, M):
     obs, full = payload[len(plan)]
     assert np.array_equal(full, o.full()), "slab-only write + resume"
     assert obs == o.observables()
+    ups, Es = payload[len(plan) + 1]
+    ou, oE = o.chain(6)
+    ou2, oE2 = o.chain(2)
+    assert ups == [int(x) for x in ou[1::2]] + [int(x) for x in ou2], "measured chain (up)"
+    assert Es == [int(x) for x in oE[1::2]] + [int(x) for x in oE2], "measured chain (E)"
