@@ -190,9 +190,13 @@ __device__ __forceinline__ uint4 ld_u4_nc(const int8_t* p) {
 
 constexpr int kBasicRows = 16;  // rows per work item (source rows reused in registers)
 
-template <int RULE>
+// OBS (white phase of a measured sweep): also add the observables of the resulting state —
+// every bond has exactly one white end, whose four black neighbours are the N / C / S / side
+// words here, and every black site is the C word of exactly one white site.
+template <int RULE, bool OBS = false>
 __global__ void __launch_bounds__(128, 4) k_basic_halfsweep(const BasicParams p) {
   const int64_t chunks = p.ny >> 4;  // 16-byte chunks per plane row
+  uint32_t obs_up = 0, obs_anti = 0;
   const int64_t bands = (p.nx + kBasicRows - 1) / kBasicRows;
   const int64_t items = chunks * bands;
   const int8_t* op = p.op_lattice;
@@ -239,8 +243,31 @@ __global__ void __launch_bounds__(128, 4) k_basic_halfsweep(const BasicParams p)
       t.w = basic_update(t.w, up.w, mid.w, dn.w, side.w,
                          basic_nc<RULE>(philox_basic(p.t, ctr + 3, p.colour, row, p.keys), p.acc));
       *reinterpret_cast<uint4*>(tp) = t;
+      if (OBS) {  // +-1 bytes differ iff bit 1 differs; +1 has bit 1 clear
+        const uint32_t tw[4] = {t.x, t.y, t.z, t.w}, nw[4] = {up.x, up.y, up.z, up.w};
+        const uint32_t cw[4] = {mid.x, mid.y, mid.z, mid.w}, sw[4] = {dn.x, dn.y, dn.z, dn.w};
+        const uint32_t dw[4] = {side.x, side.y, side.z, side.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          obs_up += __popc(~tw[k] & kByteDown) + __popc(~cw[k] & kByteDown);
+          obs_anti += __popc((tw[k] ^ nw[k]) & kByteDown) + __popc((tw[k] ^ cw[k]) & kByteDown) +
+                      __popc((tw[k] ^ sw[k]) & kByteDown) + __popc((tw[k] ^ dw[k]) & kByteDown);
+        }
+      }
       up = mid;
       mid = dn;
+    }
+  }
+  if (OBS) {
+    unsigned long long u = obs_up, a = obs_anti;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      u += __shfl_xor_sync(0xffffffffu, u, off);
+      a += __shfl_xor_sync(0xffffffffu, a, off);
+    }
+    if ((threadIdx.x & 31) == 0 && (u | a)) {
+      atomicAdd(&p.obs_out[0], u);
+      atomicAdd(&p.obs_out[1], a);
     }
   }
 }
@@ -417,6 +444,7 @@ __global__ void k_basic_convert(int8_t* black, int8_t* white, int8_t* full, int6
 cudaError_t launch_basic_halfsweep(int rule, int listing, int sms, cudaStream_t st,
                                    const BasicParams& p) {
   if (listing || (p.ny & 15) != 0) {  // the SWAR kernel needs whole 16-byte chunks
+    if (p.obs_out) return cudaErrorInvalidValue;  // fused observables: SWAR kernel only
     const int64_t quads = p.ny >> 2;
     const dim3 g((unsigned)((quads + 255) / 256), (unsigned)(p.nx < 65535 ? p.nx : 65535));
     const bool metropolis = rule == 0 || rule == 2 || rule == 4;
@@ -429,17 +457,25 @@ cudaError_t launch_basic_halfsweep(int rule, int listing, int sms, cudaStream_t 
   const int64_t items = (p.ny >> 4) * ((p.nx + kBasicRows - 1) / kBasicRows);
   const int64_t cap = (int64_t)sms * 4 * 64;  // grid-stride beyond 64 waves
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((items + 127) / 128, cap));
+#define ISING_BASIC_CASE(R)                                                     \
+  case R:                                                                       \
+    if (p.obs_out)                                                              \
+      k_basic_halfsweep<R, true><<<grid, 128, 0, st>>>(p);                      \
+    else                                                                        \
+      k_basic_halfsweep<R><<<grid, 128, 0, st>>>(p);                            \
+    break;
   switch (rule) {
-    case 0: k_basic_halfsweep<0><<<grid, 128, 0, st>>>(p); break;
-    case 1: k_basic_halfsweep<1><<<grid, 128, 0, st>>>(p); break;
-    case 2: k_basic_halfsweep<2><<<grid, 128, 0, st>>>(p); break;
-    case 3: k_basic_halfsweep<3><<<grid, 128, 0, st>>>(p); break;
-    case 4: k_basic_halfsweep<4><<<grid, 128, 0, st>>>(p); break;
-    case 5: k_basic_halfsweep<5><<<grid, 128, 0, st>>>(p); break;
-    case 6: k_basic_halfsweep<6><<<grid, 128, 0, st>>>(p); break;
-    case 7: k_basic_halfsweep<7><<<grid, 128, 0, st>>>(p); break;
+    ISING_BASIC_CASE(0)
+    ISING_BASIC_CASE(1)
+    ISING_BASIC_CASE(2)
+    ISING_BASIC_CASE(3)
+    ISING_BASIC_CASE(4)
+    ISING_BASIC_CASE(5)
+    ISING_BASIC_CASE(6)
+    ISING_BASIC_CASE(7)
     default: return cudaErrorInvalidValue;
   }
+#undef ISING_BASIC_CASE
   return cudaGetLastError();
 }
 

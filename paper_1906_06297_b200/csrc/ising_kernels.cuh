@@ -156,6 +156,7 @@ struct BasicParams {
   uint32_t t, colour;
   Accept acc;  // same threshold table / variant flags as the multi-spin path
   PhiloxKeys keys;
+  unsigned long long* obs_out;  // white phase of a measured sweep: += [up, antiparallel] (or null)
 };
 // rule: kernel variant as for launch_halfsweep (0, 2, 4 Metropolis; 3, 5, 6, 1 heat bath).
 // listing != 0 selects the per-site kernel that mirrors the Fig. 2 listing line by line.

@@ -914,12 +914,20 @@ int basic_init(ising_ctx* h, int cold) {
   return ISING_OK;
 }
 
-int basic_enqueue_sweeps(ising_ctx* h, int64_t n) {
+bool basic_listing() {
+  const char* listing_env = getenv("ISING_BASIC_LISTING");
+  return listing_env && listing_env[0] == '1';
+}
+
+// The basic layout's measured chains fuse the observables into the SWAR kernel's white phase.
+bool basic_fused_obs(const ising_ctx* h) { return !basic_listing() && ((h->M / 2) & 15) == 0; }
+
+// obs: add the observables of the state after the last sweep into obs[0..1] (SWAR kernel).
+int basic_enqueue_sweeps(ising_ctx* h, int64_t n, unsigned long long* obs = nullptr) {
   Device& d = h->devs[0];
   const int64_t ny = h->M / 2;
   const int rule = kernel_variant(h);
-  const char* listing_env = getenv("ISING_BASIC_LISTING");
-  const int listing = (listing_env && listing_env[0] == '1') ? 1 : 0;
+  const int listing = basic_listing() ? 1 : 0;
   for (int64_t k = 1; k <= n; ++k) {
     for (int c = 0; c < 2; ++c) {
       BasicParams p{};
@@ -931,6 +939,7 @@ int basic_enqueue_sweeps(ising_ctx* h, int64_t n) {
       p.colour = (uint32_t)c;
       p.acc = h->acc;
       p.keys = h->keys;
+      p.obs_out = (k == n && c == 1) ? obs : nullptr;
       const bool prof = h->profiling && h->kernel_launches < kMaxProfiledLaunches;
       if (prof) CU(cudaEventRecord(h->prof_events[2 * h->kernel_launches], d.stream));
       CU(launch_basic_halfsweep(rule, listing, d.sms, d.stream, p));
@@ -1515,7 +1524,8 @@ int ising_observables(ising_t h, int64_t* up_count, int64_t* bond_energy) {
 
 // Enqueue n_samples x `every` sweeps with the observables of every sample's white phase
 // reduced into each device's meas buffer ([up, antiparallel] per sample), bracketed by the
-// devices' ev_t0 / ev_t1 events.  Single-process handles (not rank mode, not basic).
+// devices' ev_t0 / ev_t1 events.  Single-process handles (not rank mode); basic-layout
+// handles with the SWAR kernel (basic_fused_obs).
 static int measure_enqueue(ising_ctx* h, int64_t n_samples, int64_t every) {
   const size_t need = (size_t)std::max<int64_t>(n_samples, 1) * 2;
   std::vector<unsigned long long*> base;
@@ -1534,7 +1544,9 @@ static int measure_enqueue(ising_ctx* h, int64_t n_samples, int64_t every) {
   }
   h->kernel_launches = 0;
   std::vector<unsigned long long*> slot(base.size());
-  if (n_samples > 0 && persistent_eligible(h)) {
+  if (h->basic) {  // byte layout: observables fused into each sample's last white phase
+    for (int64_t k = 0; k < n_samples; ++k) TRY(basic_enqueue_sweeps(h, every, base[0] + 2 * k));
+  } else if (n_samples > 0 && persistent_eligible(h)) {
     TRY(run_persistent(h, n_samples * every, base[0], every));  // the whole chain, one launch
   } else {
     int64_t k0 = 0;
@@ -1607,9 +1619,9 @@ int ising_sweep_measure(ising_t h, int64_t n_samples, int64_t every, int64_t* up
     h->last_ms = total;
     return ISING_OK;
   }
-  if ((h->rank_mode && h->world > 1) || h->basic) {
-    // rank-NCCL / basic layout: sweep, then the separate observables pass (all-reduced over
-    // NCCL in rank mode) per sample
+  if ((h->rank_mode && h->world > 1) || (h->basic && !basic_fused_obs(h))) {
+    // rank-NCCL / listing-shaped basic kernel: sweep, then the separate observables pass
+    // (all-reduced over NCCL in rank mode) per sample
     double total = 0;
     for (int64_t k = 0; k < n_samples; ++k) {
       TRY(ising_sweep(h, every));
@@ -1662,7 +1674,8 @@ int ising_sweep_measure_async(ising_t h, int64_t n_samples, int64_t every, int64
   pm->energy = bond_energies;
   pm->n = n_samples;
   pm->ready = false;
-  if ((h->rank_mode && h->world > 1) || h->basic || h->devs.size() > 1 || n_samples == 0) {
+  if ((h->rank_mode && h->world > 1) || (h->basic && !basic_fused_obs(h)) || h->devs.size() > 1 ||
+      n_samples == 0) {
     // cross-device reductions: the synchronous path, complete on return
     TRY(ising_sweep_measure(h, n_samples, every, up_counts, bond_energies));
     pm->ready = true;

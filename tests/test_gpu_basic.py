@@ -69,3 +69,25 @@ def test_basic_write_resume_and_measure():
     assert np.array_equal(ups, ou[1::2]) and np.array_equal(Es, oE[1::2])
     with pytest.raises(ising.IsingError):
         IsingLattice.basic(64, 60, 1)
+
+
+@pytest.mark.parametrize("N,M", [(64, 64), (130, 192), (34, 1024), (8, 24)])
+@pytest.mark.parametrize("beta,rule", [(0.4406868, 0), (0.4406868, 1), (math.inf, 0)])
+def test_basic_measured_chain(N, M, beta, rule, monkeypatch):
+    # measured chains on the byte layout: observables fused into the SWAR kernel's white phase
+    # (plane widths that are multiples of 16 bytes), else the separate observables pass (8 x 24,
+    # and the listing-shaped kernel); synchronous and asynchronous forms
+    for listing in ["0", "1"]:
+        monkeypatch.setenv("ISING_BASIC_LISTING", listing)
+        g = IsingLattice.basic(N, M, 5).set_beta(beta, rule).init_random()
+        o = oracle.Lattice(N, M, 5).set_beta(beta, rule).init_random()
+        ups, Es = g.measure(4, 2)
+        ou, oE = o.chain(8)
+        assert np.array_equal(ups, ou[1::2]) and np.array_equal(Es, oE[1::2]), (listing, N, M)
+        u = np.zeros(3, dtype=np.int64)
+        e = np.zeros(3, dtype=np.int64)
+        g.measure_wait(g.measure_async(3, 1, u, e))
+        ou, oE = o.chain(3)
+        assert np.array_equal(u, ou) and np.array_equal(e, oE), (listing, N, M)
+        assert np.array_equal(g.read_lattice(), o.full())
+        g.close()
