@@ -412,6 +412,92 @@ __device__ __forceinline__ uint64_t update_word<1>(uint64_t tgt, uint64_t n, uin
   return tgt ^ flip;
 }
 
+// Eight Philox blocks (counter words 1 = c1base + b, b = 0..7) advanced round by round in
+// lockstep — the two words of a thread's 128-bit chunk.  Written this way (rather than block by
+// block inside update_word) ptxas schedules the staged kernel's row better: Metropolis
+// 1541 -> 1551, symmetric heat bath 1276 -> 1303 flips/ns on C3 (ISING_PHILOX8=0: old form).
+#ifndef ISING_PHILOX8
+#define ISING_PHILOX8 1
+#endif
+__device__ __forceinline__ void philox8(uint32_t t, uint32_t c1base, uint32_t colour, uint32_t row,
+                                        const PhiloxKeys& K, uint4 (&out)[8]) {
+  uint32_t c0[8], c1[8], c2[8], c3[8];
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    c0[b] = t;
+    c1[b] = c1base + b;
+    c2[b] = colour;
+    c3[b] = row;
+  }
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      const uint64_t p0 = (uint64_t)c0[b] * kPhiloxM0;
+      const uint64_t p1 = (uint64_t)c2[b] * kPhiloxM1;
+      const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1[b] ^ K.k0[r];
+      const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3[b] ^ K.k1[r];
+      c1[b] = (uint32_t)p1;
+      c3[b] = (uint32_t)p0;
+      c0[b] = n0;
+      c2[b] = n2;
+    }
+  }
+#pragma unroll
+  for (int b = 0; b < 8; ++b) out[b] = make_uint4(c0[b], c1[b], c2[b], c3[b]);
+}
+
+// Metropolis (RULE 0) acceptance of one word from its four precomputed blocks rb[0..3]
+// (block q serves lanes 4q .. 4q + 3), same Horner order as update_word_metropolis.
+__device__ __forceinline__ uint64_t metropolis_from_draws(uint64_t tgt, uint64_t n, uint64_t c,
+                                                          uint64_t s, uint64_t side,
+                                                          const uint4* rb, const HalfSweepParams& p) {
+  const uint32_t sum_lo = (uint32_t)n + (uint32_t)c + (uint32_t)s + (uint32_t)side;
+  const uint32_t sum_hi =
+      (uint32_t)(n >> 32) + (uint32_t)(c >> 32) + (uint32_t)(s >> 32) + (uint32_t)(side >> 32);
+  const uint32_t t3 = p.acc.thr[3], t4 = p.acc.thr[4];
+  uint32_t a3lo = 0, a4lo = 0, a3hi = 0, a4hi = 0;
+  nc_step(a3lo, a4lo, rb[1].w, t3, t4);
+  nc_step(a3lo, a4lo, rb[1].z, t3, t4);
+  nc_step(a3lo, a4lo, rb[1].y, t3, t4);
+  nc_step(a3lo, a4lo, rb[1].x, t3, t4);
+  nc_step(a3lo, a4lo, rb[0].w, t3, t4);
+  nc_step(a3lo, a4lo, rb[0].z, t3, t4);
+  nc_step(a3lo, a4lo, rb[0].y, t3, t4);
+  nc_step(a3lo, a4lo, rb[0].x, t3, t4);
+  nc_step(a3hi, a4hi, rb[3].w, t3, t4);
+  nc_step(a3hi, a4hi, rb[3].z, t3, t4);
+  nc_step(a3hi, a4hi, rb[3].y, t3, t4);
+  nc_step(a3hi, a4hi, rb[3].x, t3, t4);
+  nc_step(a3hi, a4hi, rb[2].w, t3, t4);
+  nc_step(a3hi, a4hi, rb[2].z, t3, t4);
+  nc_step(a3hi, a4hi, rb[2].y, t3, t4);
+  nc_step(a3hi, a4hi, rb[2].x, t3, t4);
+  const uint32_t lo = accept8((uint32_t)tgt, sum_lo, a3lo + a4lo);
+  const uint32_t hi = accept8((uint32_t)(tgt >> 32), sum_hi, a3hi + a4hi);
+  return ((uint64_t)hi << 32) | lo;
+}
+
+// Symmetric heat bath (RULE 7) of one word from its four precomputed blocks.
+__device__ __forceinline__ uint64_t hbs_from_draws(uint64_t tgt, uint64_t n, uint64_t c, uint64_t s,
+                                                   uint64_t side, const uint4* rb,
+                                                   const HalfSweepParams& p) {
+  const uint32_t sum_lo = (uint32_t)n + (uint32_t)c + (uint32_t)s + (uint32_t)side;
+  const uint32_t sum_hi =
+      (uint32_t)(n >> 32) + (uint32_t)(c >> 32) + (uint32_t)(s >> 32) + (uint32_t)(side >> 32);
+  const uint32_t t3 = p.acc.thr[3], t4 = p.acc.thr[4];
+  uint32_t a3lo = 0, a4lo = 0, amlo = 0, a3hi = 0, a4hi = 0, amhi = 0;
+  const uint32_t lo_draws[8] = {rb[1].w, rb[1].z, rb[1].y, rb[1].x, rb[0].w, rb[0].z, rb[0].y, rb[0].x};
+  const uint32_t hi_draws[8] = {rb[3].w, rb[3].z, rb[3].y, rb[3].x, rb[2].w, rb[2].z, rb[2].y, rb[2].x};
+#pragma unroll
+  for (int q = 0; q < 8; ++q) hbs_step(a3lo, a4lo, amlo, lo_draws[q], t3, t4);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) hbs_step(a3hi, a4hi, amhi, hi_draws[q], t3, t4);
+  const uint32_t flo = hb_accept8((uint32_t)tgt, sum_lo, hbs_nc(a3lo + a4lo, amlo));
+  const uint32_t fhi = hb_accept8((uint32_t)(tgt >> 32), sum_hi, hbs_nc(a3hi + a4hi, amhi));
+  return ((uint64_t)fhi << 32) | flo;
+}
+
 // Host-side rule dispatch shared by every launcher: f(integral_constant<int, RULE>,
 // bool_constant<OBS>).  An unknown rule is an error, never a silent fallback.
 template <typename F>
@@ -579,13 +665,26 @@ __device__ __forceinline__ void halfsweep_items(const HalfSweepParams& p, const 
         else
           side[k] = splice_east(cv[k], k == kWords - 1 ? sw : cv[k + 1]);
       }
+#if ISING_PHILOX8
+      if constexpr (kWords == 2 && (RULE == 0 || RULE == 7)) {  // lockstep Philox, as staged
+        uint4 rb[8];
+        philox8(t, (uint32_t)(4 * wc), p.colour, (uint32_t)gi, p.keys, rb);
 #pragma unroll
-      for (int k = 0; k < kWords; ++k) {
-        const uint32_t ctr0 = (uint32_t)(4 * (wc + k));  // Philox counter word 1 = j / 4 (R6)
-        tv[k] = update_word<RULE>(tv[k], nv[k], cv[k], sv[k], side[k], ctr0, (uint32_t)gi, t, p);
-        if (OBS) {
-          obs_word(tv[k], nv[k], cv[k], sv[k], side[k], obs_up, obs_anti);
+        for (int k = 0; k < 2; ++k)
+          tv[k] = RULE == 0 ? metropolis_from_draws(tv[k], nv[k], cv[k], sv[k], side[k], rb + 4 * k, p)
+                            : hbs_from_draws(tv[k], nv[k], cv[k], sv[k], side[k], rb + 4 * k, p);
+      } else
+#endif
+      {
+#pragma unroll
+        for (int k = 0; k < kWords; ++k) {
+          const uint32_t ctr0 = (uint32_t)(4 * (wc + k));  // Philox counter word 1 = j / 4 (R6)
+          tv[k] = update_word<RULE>(tv[k], nv[k], cv[k], sv[k], side[k], ctr0, (uint32_t)gi, t, p);
         }
+      }
+      if (OBS) {
+#pragma unroll
+        for (int k = 0; k < kWords; ++k) obs_word(tv[k], nv[k], cv[k], sv[k], side[k], obs_up, obs_anti);
       }
 #pragma unroll
       for (int v = 0; v < kWords / 2; ++v) {
@@ -685,92 +784,6 @@ cudaError_t launch_sync(cudaStream_t st, const SyncParams& p) {
 cudaError_t launch_gather(cudaStream_t st, const GatherParams& p) {
   k_gather<<<1, 1, 0, st>>>(p);
   return cudaGetLastError();
-}
-
-// Eight Philox blocks (counter words 1 = c1base + b, b = 0..7) advanced round by round in
-// lockstep — the two words of a thread's 128-bit chunk.  Written this way (rather than block by
-// block inside update_word) ptxas schedules the staged kernel's row better: Metropolis
-// 1541 -> 1551, symmetric heat bath 1276 -> 1303 flips/ns on C3 (ISING_PHILOX8=0: old form).
-#ifndef ISING_PHILOX8
-#define ISING_PHILOX8 1
-#endif
-__device__ __forceinline__ void philox8(uint32_t t, uint32_t c1base, uint32_t colour, uint32_t row,
-                                        const PhiloxKeys& K, uint4 (&out)[8]) {
-  uint32_t c0[8], c1[8], c2[8], c3[8];
-#pragma unroll
-  for (int b = 0; b < 8; ++b) {
-    c0[b] = t;
-    c1[b] = c1base + b;
-    c2[b] = colour;
-    c3[b] = row;
-  }
-#pragma unroll
-  for (int r = 0; r < 10; ++r) {
-#pragma unroll
-    for (int b = 0; b < 8; ++b) {
-      const uint64_t p0 = (uint64_t)c0[b] * kPhiloxM0;
-      const uint64_t p1 = (uint64_t)c2[b] * kPhiloxM1;
-      const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1[b] ^ K.k0[r];
-      const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3[b] ^ K.k1[r];
-      c1[b] = (uint32_t)p1;
-      c3[b] = (uint32_t)p0;
-      c0[b] = n0;
-      c2[b] = n2;
-    }
-  }
-#pragma unroll
-  for (int b = 0; b < 8; ++b) out[b] = make_uint4(c0[b], c1[b], c2[b], c3[b]);
-}
-
-// Metropolis (RULE 0) acceptance of one word from its four precomputed blocks rb[0..3]
-// (block q serves lanes 4q .. 4q + 3), same Horner order as update_word_metropolis.
-__device__ __forceinline__ uint64_t metropolis_from_draws(uint64_t tgt, uint64_t n, uint64_t c,
-                                                          uint64_t s, uint64_t side,
-                                                          const uint4* rb, const HalfSweepParams& p) {
-  const uint32_t sum_lo = (uint32_t)n + (uint32_t)c + (uint32_t)s + (uint32_t)side;
-  const uint32_t sum_hi =
-      (uint32_t)(n >> 32) + (uint32_t)(c >> 32) + (uint32_t)(s >> 32) + (uint32_t)(side >> 32);
-  const uint32_t t3 = p.acc.thr[3], t4 = p.acc.thr[4];
-  uint32_t a3lo = 0, a4lo = 0, a3hi = 0, a4hi = 0;
-  nc_step(a3lo, a4lo, rb[1].w, t3, t4);
-  nc_step(a3lo, a4lo, rb[1].z, t3, t4);
-  nc_step(a3lo, a4lo, rb[1].y, t3, t4);
-  nc_step(a3lo, a4lo, rb[1].x, t3, t4);
-  nc_step(a3lo, a4lo, rb[0].w, t3, t4);
-  nc_step(a3lo, a4lo, rb[0].z, t3, t4);
-  nc_step(a3lo, a4lo, rb[0].y, t3, t4);
-  nc_step(a3lo, a4lo, rb[0].x, t3, t4);
-  nc_step(a3hi, a4hi, rb[3].w, t3, t4);
-  nc_step(a3hi, a4hi, rb[3].z, t3, t4);
-  nc_step(a3hi, a4hi, rb[3].y, t3, t4);
-  nc_step(a3hi, a4hi, rb[3].x, t3, t4);
-  nc_step(a3hi, a4hi, rb[2].w, t3, t4);
-  nc_step(a3hi, a4hi, rb[2].z, t3, t4);
-  nc_step(a3hi, a4hi, rb[2].y, t3, t4);
-  nc_step(a3hi, a4hi, rb[2].x, t3, t4);
-  const uint32_t lo = accept8((uint32_t)tgt, sum_lo, a3lo + a4lo);
-  const uint32_t hi = accept8((uint32_t)(tgt >> 32), sum_hi, a3hi + a4hi);
-  return ((uint64_t)hi << 32) | lo;
-}
-
-// Symmetric heat bath (RULE 7) of one word from its four precomputed blocks.
-__device__ __forceinline__ uint64_t hbs_from_draws(uint64_t tgt, uint64_t n, uint64_t c, uint64_t s,
-                                                   uint64_t side, const uint4* rb,
-                                                   const HalfSweepParams& p) {
-  const uint32_t sum_lo = (uint32_t)n + (uint32_t)c + (uint32_t)s + (uint32_t)side;
-  const uint32_t sum_hi =
-      (uint32_t)(n >> 32) + (uint32_t)(c >> 32) + (uint32_t)(s >> 32) + (uint32_t)(side >> 32);
-  const uint32_t t3 = p.acc.thr[3], t4 = p.acc.thr[4];
-  uint32_t a3lo = 0, a4lo = 0, amlo = 0, a3hi = 0, a4hi = 0, amhi = 0;
-  const uint32_t lo_draws[8] = {rb[1].w, rb[1].z, rb[1].y, rb[1].x, rb[0].w, rb[0].z, rb[0].y, rb[0].x};
-  const uint32_t hi_draws[8] = {rb[3].w, rb[3].z, rb[3].y, rb[3].x, rb[2].w, rb[2].z, rb[2].y, rb[2].x};
-#pragma unroll
-  for (int q = 0; q < 8; ++q) hbs_step(a3lo, a4lo, amlo, lo_draws[q], t3, t4);
-#pragma unroll
-  for (int q = 0; q < 8; ++q) hbs_step(a3hi, a4hi, amhi, hi_draws[q], t3, t4);
-  const uint32_t flo = hb_accept8((uint32_t)tgt, sum_lo, hbs_nc(a3lo + a4lo, amlo));
-  const uint32_t fhi = hb_accept8((uint32_t)(tgt >> 32), sum_hi, hbs_nc(a3hi + a4hi, amhi));
-  return ((uint64_t)fhi << 32) | flo;
 }
 
 // ------------------------------------------------------- TMA-staged variant
