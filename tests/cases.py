@@ -23,7 +23,10 @@ PARITY_BETAS = [0.0, 0.2, BETA_TC, 0.8, math.inf, 4e-11]
 PARITY_SEEDS = [1, 2]
 
 # (rows, cols, slabs): R = 2 (every row a boundary row), 2 slabs (up = down peer)
-SLAB_CASES = [(16, 64, 8), (64, 64, 2), (256, 256, 4), (96, 192, 3)]
+# (SURVEY §8(c) multi-GPU additions: 16 x 64 at n = 8 (R = 2), 64 x 64 at n = 2, 4096^2 at
+# n = 2, 4, 8; 4096 x 8192 at n = 8 runs the TMA-staged kernel)
+SLAB_CASES = [(16, 64, 8), (64, 64, 2), (256, 256, 4), (96, 192, 3), (4096, 4096, 2),
+              (4096, 4096, 4), (4096, 4096, 8), (4096, 8192, 8)]
 
 
 def random_pm1(rng: np.random.Generator, N: int, M: int, p_up: float = 0.5) -> np.ndarray:
