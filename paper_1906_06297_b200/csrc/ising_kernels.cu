@@ -460,22 +460,12 @@ __device__ __forceinline__ uint64_t metropolis_from_draws(uint64_t tgt, uint64_t
       (uint32_t)(n >> 32) + (uint32_t)(c >> 32) + (uint32_t)(s >> 32) + (uint32_t)(side >> 32);
   const uint32_t t3 = p.acc.thr[3], t4 = p.acc.thr[4];
   uint32_t a3lo = 0, a4lo = 0, a3hi = 0, a4hi = 0;
-  nc_step(a3lo, a4lo, rb[1].w, t3, t4);
-  nc_step(a3lo, a4lo, rb[1].z, t3, t4);
-  nc_step(a3lo, a4lo, rb[1].y, t3, t4);
-  nc_step(a3lo, a4lo, rb[1].x, t3, t4);
-  nc_step(a3lo, a4lo, rb[0].w, t3, t4);
-  nc_step(a3lo, a4lo, rb[0].z, t3, t4);
-  nc_step(a3lo, a4lo, rb[0].y, t3, t4);
-  nc_step(a3lo, a4lo, rb[0].x, t3, t4);
-  nc_step(a3hi, a4hi, rb[3].w, t3, t4);
-  nc_step(a3hi, a4hi, rb[3].z, t3, t4);
-  nc_step(a3hi, a4hi, rb[3].y, t3, t4);
-  nc_step(a3hi, a4hi, rb[3].x, t3, t4);
-  nc_step(a3hi, a4hi, rb[2].w, t3, t4);
-  nc_step(a3hi, a4hi, rb[2].z, t3, t4);
-  nc_step(a3hi, a4hi, rb[2].y, t3, t4);
-  nc_step(a3hi, a4hi, rb[2].x, t3, t4);
+  const uint32_t dl[8] = {rb[1].w, rb[1].z, rb[1].y, rb[1].x, rb[0].w, rb[0].z, rb[0].y, rb[0].x};
+  const uint32_t dh[8] = {rb[3].w, rb[3].z, rb[3].y, rb[3].x, rb[2].w, rb[2].z, rb[2].y, rb[2].x};
+#pragma unroll
+  for (int q = 0; q < 8; ++q) nc_step(a3lo, a4lo, dl[q], t3, t4);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) nc_step(a3hi, a4hi, dh[q], t3, t4);
   const uint32_t lo = accept8((uint32_t)tgt, sum_lo, a3lo + a4lo);
   const uint32_t hi = accept8((uint32_t)(tgt >> 32), sum_hi, a3hi + a4hi);
   return ((uint64_t)hi << 32) | lo;
