@@ -305,6 +305,29 @@ def test_full_size_sampled_rows_after_one_sweep(N, M):
     g.close()
 
 
+@pytest.mark.slow
+def test_c4_slab_count_invariance():
+    # the 131072^2 lattice after 8 sweeps is the same split into 8 row slabs
+    # (the n = 8 strong-scaling geometry, here 8 virtual slabs on one device, 2 x 8 GiB) as in
+    # one: observables equal and rows byte-identical, sampled at every slab boundary
+    N = M = cases.C4[0]
+    beta = cases.BETA_TC
+    one = gpu_lattice(N, M, 3, "random", beta)
+    one.sweep(8)
+    obs1 = one.observables()
+    R = N // 8
+    rows = sorted({k * R + d for k in range(8) for d in (-1, 0)} | {1, N // 3, N - 1})
+    rows = [r % N for r in rows]
+    ref = {r: one.read_rows(r, 1)[0].copy() for r in rows}
+    one.close()
+    eight = gpu_lattice(N, M, 3, "random", beta, devices=[0] * 8)
+    eight.sweep(8)
+    assert eight.observables() == obs1
+    for r in rows:
+        assert np.array_equal(eight.read_rows(r, 1)[0], ref[r]), f"row {r}"
+    eight.close()
+
+
 def test_persistent_kernel_path(monkeypatch):
     # opt-in persistent multi-sweep kernel (ISING_PERSISTENT=1): same lattices and series
     monkeypatch.setenv("ISING_PERSISTENT", "1")
