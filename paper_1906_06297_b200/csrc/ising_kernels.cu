@@ -452,6 +452,7 @@ __device__ __forceinline__ void philox8(uint32_t t, uint32_t c1base, uint32_t co
 
 // Metropolis (RULE 0) acceptance of one word from its four precomputed blocks rb[0..3]
 // (block q serves lanes 4q .. 4q + 3), same Horner order as update_word_metropolis.
+template <int RULE>
 __device__ __forceinline__ uint64_t metropolis_from_draws(uint64_t tgt, uint64_t n, uint64_t c,
                                                           uint64_t s, uint64_t side,
                                                           const uint4* rb, const HalfSweepParams& p) {
@@ -466,9 +467,36 @@ __device__ __forceinline__ uint64_t metropolis_from_draws(uint64_t tgt, uint64_t
   for (int q = 0; q < 8; ++q) nc_step(a3lo, a4lo, dl[q], t3, t4);
 #pragma unroll
   for (int q = 0; q < 8; ++q) nc_step(a3hi, a4hi, dh[q], t3, t4);
-  const uint32_t lo = accept8((uint32_t)tgt, sum_lo, a3lo + a4lo);
-  const uint32_t hi = accept8((uint32_t)(tgt >> 32), sum_hi, a3hi + a4hi);
+  uint32_t nclo = a3lo + a4lo, nchi = a3hi + a4hi;
+  if constexpr (RULE == 2) {  // a class whose threshold is 2^32 never blocks a flip
+    const uint32_t k3 = p.acc.keep3, k4 = p.acc.keep4;
+    nclo = (a3lo & k3) + (a4lo & k4);
+    nchi = (a3hi & k3) + (a4hi & k4);
+  }
+  const uint32_t lo = accept8((uint32_t)tgt, sum_lo, nclo);
+  const uint32_t hi = accept8((uint32_t)(tgt >> 32), sum_hi, nchi);
   return ((uint64_t)hi << 32) | lo;
+}
+
+// Five-compare heat bath (RULE 3 / 5 / 6: NA leading "always" classes) from precomputed draws.
+template <int NA>
+__device__ __forceinline__ uint64_t hb_from_draws(uint64_t tgt, uint64_t n, uint64_t c, uint64_t s,
+                                                  uint64_t side, const uint4* rb,
+                                                  const HalfSweepParams& p) {
+  const uint32_t sum_lo = (uint32_t)n + (uint32_t)c + (uint32_t)s + (uint32_t)side;
+  const uint32_t sum_hi =
+      (uint32_t)(n >> 32) + (uint32_t)(c >> 32) + (uint32_t)(s >> 32) + (uint32_t)(side >> 32);
+  const uint32_t* T = p.acc.thr;
+  uint32_t lo = 0, hi = 0;
+  const uint32_t dl[8] = {rb[1].w, rb[1].z, rb[1].y, rb[1].x, rb[0].w, rb[0].z, rb[0].y, rb[0].x};
+  const uint32_t dh[8] = {rb[3].w, rb[3].z, rb[3].y, rb[3].x, rb[2].w, rb[2].z, rb[2].y, rb[2].x};
+#pragma unroll
+  for (int q = 0; q < 8; ++q) hb_step<NA>(lo, dl[q], T);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) hb_step<NA>(hi, dh[q], T);
+  const uint32_t flo = hb_accept8((uint32_t)tgt, sum_lo, lo);
+  const uint32_t fhi = hb_accept8((uint32_t)(tgt >> 32), sum_hi, hi);
+  return ((uint64_t)fhi << 32) | flo;
 }
 
 // Symmetric heat bath (RULE 7) of one word from its four precomputed blocks.
@@ -489,6 +517,20 @@ __device__ __forceinline__ uint64_t hbs_from_draws(uint64_t tgt, uint64_t n, uin
   const uint32_t flo = hb_accept8((uint32_t)tgt, sum_lo, hbs_nc(a3lo + a4lo, amlo));
   const uint32_t fhi = hb_accept8((uint32_t)(tgt >> 32), sum_hi, hbs_nc(a3hi + a4hi, amhi));
   return ((uint64_t)fhi << 32) | flo;
+}
+
+// One word of RULE from its four precomputed Philox blocks (every rule that draws, except the
+// unreachable generic heat bath RULE 1, which keeps update_word).
+template <int RULE>
+__device__ __forceinline__ uint64_t word_from_draws(uint64_t tgt, uint64_t n, uint64_t c, uint64_t s,
+                                                    uint64_t side, const uint4* rb,
+                                                    const HalfSweepParams& p) {
+  if constexpr (RULE == 0 || RULE == 2) return metropolis_from_draws<RULE>(tgt, n, c, s, side, rb, p);
+  else if constexpr (RULE == 7) return hbs_from_draws(tgt, n, c, s, side, rb, p);
+  else return hb_from_draws<RULE == 3 ? 0 : RULE == 5 ? 1 : 2>(tgt, n, c, s, side, rb, p);
+}
+__host__ __device__ constexpr bool lockstep_rule(int rule) {
+  return rule == 0 || rule == 2 || rule == 3 || rule == 5 || rule == 6 || rule == 7;
 }
 
 // Host-side rule dispatch shared by every launcher: f(integral_constant<int, RULE>,
@@ -659,13 +701,12 @@ __device__ __forceinline__ void halfsweep_items(const HalfSweepParams& p, const 
           side[k] = splice_east(cv[k], k == kWords - 1 ? sw : cv[k + 1]);
       }
 #if ISING_PHILOX8
-      if constexpr (kWords == 2 && (RULE == 0 || RULE == 7)) {  // lockstep Philox, as staged
+      if constexpr (kWords == 2 && lockstep_rule(RULE)) {  // lockstep Philox, as staged
         uint4 rb[8];
         philox8(t, (uint32_t)(4 * wc), p.colour, (uint32_t)gi, p.keys, rb);
 #pragma unroll
         for (int k = 0; k < 2; ++k)
-          tv[k] = RULE == 0 ? metropolis_from_draws(tv[k], nv[k], cv[k], sv[k], side[k], rb + 4 * k, p)
-                            : hbs_from_draws(tv[k], nv[k], cv[k], sv[k], side[k], rb + 4 * k, p);
+          tv[k] = word_from_draws<RULE>(tv[k], nv[k], cv[k], sv[k], side[k], rb + 4 * k, p);
       } else
 #endif
       {
@@ -927,16 +968,11 @@ __global__ void __launch_bounds__(128, staged_minb(RULE)) k_halfsweep_staged(con
     ulonglong2 tv = *reinterpret_cast<const ulonglong2*>(tp);
     const uint32_t ctr0 = (uint32_t)(4 * wc);
 #if ISING_PHILOX8
-    if constexpr (RULE == 0) {
+    if constexpr (lockstep_rule(RULE)) {
       uint4 rb[8];
       philox8(t, ctr0, p.colour, (uint32_t)gi, p.keys, rb);
-      tv.x = metropolis_from_draws(tv.x, n0, c0, s0, side0, rb, p);
-      tv.y = metropolis_from_draws(tv.y, n1, c1, s1, side1, rb + 4, p);
-    } else if constexpr (RULE == 7) {
-      uint4 rb[8];
-      philox8(t, ctr0, p.colour, (uint32_t)gi, p.keys, rb);
-      tv.x = hbs_from_draws(tv.x, n0, c0, s0, side0, rb, p);
-      tv.y = hbs_from_draws(tv.y, n1, c1, s1, side1, rb + 4, p);
+      tv.x = word_from_draws<RULE>(tv.x, n0, c0, s0, side0, rb, p);
+      tv.y = word_from_draws<RULE>(tv.y, n1, c1, s1, side1, rb + 4, p);
     } else
 #endif
     {
