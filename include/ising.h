@@ -171,9 +171,9 @@ int ising_sweep_measure(ising_t h, int64_t n_samples, int64_t every, int64_t* up
 /* Asynchronous measured chain: the same sweeps and fused observables as
  * ising_sweep_measure, but the call returns once the work and the device->host copy of the
  * results are enqueued on the handle's stream, so the host can enqueue the next chunk while
- * this one runs.  up_counts / bond_energies (n_samples entries each; pinned host memory for a
- * truly asynchronous copy) stay owned by the caller, must stay valid, and hold undefined
- * values until ising_measure_wait(h, *ticket) returns ISING_OK; the wait also sets
+ * this one runs (the results land in a pinned buffer of the library).  up_counts /
+ * bond_energies (n_samples entries each) stay owned by the caller, must stay valid, and are
+ * written by ising_measure_wait(h, *ticket); the wait also sets
  * ising_last_sweep_ms to this call's device time.  At most 8 calls may be pending
  * (ISING_ERR_STATE beyond).  Rank-mode, multi-device and basic-layout handles run the
  * synchronous path (results final on return; the wait is then a no-op).  The sweep counter

@@ -742,6 +742,10 @@ __global__ void __launch_bounds__(128, ISING_MINB) k_halfsweep(const HalfSweepPa
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
   }
+  if (p.obs_clear && blockIdx.x == 0 && threadIdx.x == 0) {  // after the grid dependency
+    p.obs_clear[0] = 0;
+    p.obs_clear[1] = 0;
+  }
   if (p.wait_flags) {  // rank-p2p: neighbours done with the previous phase
     if (threadIdx.x == 0) spin_until(p.wait_flags, 2, p.wait_value);
     __syncthreads();
@@ -871,6 +875,10 @@ __global__ void __launch_bounds__(128, staged_minb(RULE)) k_halfsweep_staged(con
   if (p.pdl) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
+  if (p.obs_clear && blockIdx.x == 0 && threadIdx.x == 0) {  // after the grid dependency
+    p.obs_clear[0] = 0;
+    p.obs_clear[1] = 0;
   }
   __shared__ alignas(128) uint64_t tile[kRows + 2][kStageWords];
   __shared__ uint64_t edge[kRows + 2][2];

@@ -72,6 +72,9 @@ struct HalfSweepParams {
   // state into obs_out[0..1] (null: no measurement)
   unsigned long long* obs_out;
   const uint32_t* slot_dev;  // graph replays: device-resident sample index added to obs_out
+  // black phase of a measured sweep: zero these two counters (the slot the white phase adds
+  // into) — replaces a separate memset node between the sweeps of a measured chain
+  unsigned long long* obs_clear;
 };
 
 // Persistent multi-sweep kernel for small lattices (one slab, one device).

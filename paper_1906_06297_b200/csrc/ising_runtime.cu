@@ -140,6 +140,8 @@ struct PendingMeasure {
   bool ready = false;   // completed synchronously (fallback path): nothing to wait for
   double ms = 0;
   cudaEvent_t t0 = nullptr, t1 = nullptr, done = nullptr;
+  unsigned long long* host = nullptr;  // pinned landing buffer of the [up, anti] pairs
+  size_t host_cap = 0;                 // in pairs
 };
 constexpr int kMaxPending = 8;
 
@@ -341,9 +343,11 @@ void destroy_ctx(ising_ctx* h) {
     if (d.comm) cudaStreamDestroy(d.comm);
   }
   for (cudaEvent_t e : h->prof_events) cudaEventDestroy(e);
-  for (auto& pm : h->pending)
+  for (auto& pm : h->pending) {
     for (cudaEvent_t e : {pm.t0, pm.t1, pm.done})
       if (e) cudaEventDestroy(e);
+    if (pm.host) cudaFreeHost(pm.host);
+  }
   if (h->gexec) cudaGraphExecDestroy(h->gexec);
   for (int c = 0; c < 2; ++c)
     if (h->bplane[c]) cudaFree(h->bplane[c]);
@@ -413,8 +417,11 @@ int run_halfsweep(ising_ctx* h, Slab& s, int c, int r_begin, int r_end, uint64_t
   halfsweep_geometry(h, d, r_end - r_begin, &p.H, &p.items, &grid);
   p.t = t;
   p.t_dev = t_from_dev ? h->t_dev : nullptr;
-  p.obs_out = obs;
-  p.slot_dev = (obs && slot_from_dev) ? h->t_dev + 1 : nullptr;
+  // measured sweeps: the white phase adds into obs, the black phase before it zeroes it
+  // (graph replays index a device-resident slot and keep the memset of all slots instead)
+  p.obs_out = c == 1 ? obs : nullptr;
+  p.obs_clear = (c == 0 && obs && !slot_from_dev) ? obs : nullptr;
+  p.slot_dev = (c == 1 && obs && slot_from_dev) ? h->t_dev + 1 : nullptr;
   p.colour = (uint32_t)c;
   p.keys = h->keys;
   p.acc = h->acc;
@@ -482,7 +489,7 @@ int phase_local(ising_ctx* h, int c, uint32_t t, bool t_from_dev = false,
     // local row 0 -> upper slab's bottom halo (padded row R+1); local row R-1 -> lower
     // slab's top halo (padded row 0).
     TRY(run_halfsweep(h, s, c, 0, (int)s.R, up.plane[c] + (up.R + 1) * h->W, dn.plane[c], t,
-                      t_from_dev, (obs && c == 1) ? (*obs)[s.devi] : nullptr, slot_from_dev));
+                      t_from_dev, obs ? (*obs)[s.devi] : nullptr, slot_from_dev));
   }
   if (multi_dev) {
     for (auto& d : h->devs) {
@@ -863,7 +870,7 @@ int enqueue_sweeps(ising_ctx* h, int64_t n, const std::vector<unsigned long long
     const uint32_t t = (uint32_t)(h->t + (uint64_t)k);
     for (int c = 0; c < 2; ++c) {
       if (h->p2p && h->world > 1)
-        TRY(phase_p2p(h, c, t, (k == n && obs && c == 1) ? (*obs)[0] : nullptr));
+        TRY(phase_p2p(h, c, t, (k == n && obs) ? (*obs)[0] : nullptr));
       else if (h->rank_mode && h->world > 1)
         TRY(phase_rank(h, c, t));
       else
@@ -1528,6 +1535,9 @@ int ising_observables(ising_t h, int64_t* up_count, int64_t* bond_energy) {
 // handles with the SWAR kernel (basic_fused_obs).
 static int measure_enqueue(ising_ctx* h, int64_t n_samples, int64_t every) {
   const size_t need = (size_t)std::max<int64_t>(n_samples, 1) * 2;
+  const bool zero_slots =
+      h->basic || (n_samples > 0 && persistent_eligible(h)) ||
+      (graph_eligible(h) && every <= kGraphSweeps && n_samples >= std::max<int64_t>(1, kGraphSweeps / every));
   std::vector<unsigned long long*> base;
   for (auto& d : h->devs) {
     CU(cudaSetDevice(d.dev));
@@ -1538,7 +1548,9 @@ static int measure_enqueue(ising_ctx* h, int64_t n_samples, int64_t every) {
       CU(cudaMalloc(&d.meas, need * sizeof(unsigned long long)));
       d.meas_cap = need;
     }
-    CU(cudaMemsetAsync(d.meas, 0, need * sizeof(unsigned long long), d.stream));
+    // directly launched samples zero their own slot in their black phase (obs_clear); the
+    // graph-replayed and persistent paths add into slots zeroed here
+    if (zero_slots) CU(cudaMemsetAsync(d.meas, 0, need * sizeof(unsigned long long), d.stream));
     base.push_back(d.meas);
     CU(cudaEventRecord(d.ev_t0, d.stream));
   }
@@ -1688,12 +1700,18 @@ int ising_sweep_measure_async(ising_t h, int64_t n_samples, int64_t every, int64
     CU(cudaEventRecord(pm->t0, d.stream));
     TRY(measure_enqueue(h, n_samples, every));
     CU(cudaEventRecord(pm->t1, d.stream));
-    // the two columns of [up, antiparallel] pairs straight into the caller's arrays
-    CU(cudaMemcpy2DAsync(up_counts, sizeof(int64_t), d.meas, 2 * sizeof(unsigned long long),
-                         sizeof(int64_t), (size_t)n_samples, cudaMemcpyDeviceToHost, d.stream));
-    CU(cudaMemcpy2DAsync(bond_energies, sizeof(int64_t), d.meas + 1,
-                         2 * sizeof(unsigned long long), sizeof(int64_t), (size_t)n_samples,
-                         cudaMemcpyDeviceToHost, d.stream));
+    // one copy of the [up, antiparallel] pairs into this slot's pinned landing buffer; the
+    // wait splits them into the caller's arrays
+    if (pm->host_cap < (size_t)n_samples) {
+      if (pm->host) CU(cudaFreeHost(pm->host));
+      pm->host = nullptr;
+      pm->host_cap = 0;
+      CU(cudaHostAlloc(&pm->host, 2 * sizeof(unsigned long long) * (size_t)n_samples,
+                       cudaHostAllocDefault));
+      pm->host_cap = (size_t)n_samples;
+    }
+    CU(cudaMemcpyAsync(pm->host, d.meas, 2 * sizeof(unsigned long long) * (size_t)n_samples,
+                       cudaMemcpyDeviceToHost, d.stream));
     CU(cudaEventRecord(pm->done, d.stream));
   }
   pm->ticket = h->next_ticket++;
@@ -1710,8 +1728,10 @@ int ising_measure_wait(ising_t h, int64_t ticket) {
   if (!pm->ready) {
     CU(cudaSetDevice(h->devs[0].dev));
     CU(cudaEventSynchronize(pm->done));
-    for (int64_t k = 0; k < pm->n; ++k)  // antiparallel bonds -> bond energy (Eq. 1, R11)
-      pm->energy[k] = 2 * pm->energy[k] - 2 * h->N * h->M;
+    for (int64_t k = 0; k < pm->n; ++k) {  // antiparallel bonds -> bond energy (Eq. 1, R11)
+      pm->up[k] = (int64_t)pm->host[2 * k];
+      pm->energy[k] = 2 * (int64_t)pm->host[2 * k + 1] - 2 * h->N * h->M;
+    }
     float ms = 0;
     CU(cudaEventElapsedTime(&ms, pm->t0, pm->t1));
     pm->ms = ms;
