@@ -328,6 +328,19 @@ def test_c4_slab_count_invariance():
     eight.close()
 
 
+@pytest.mark.slow
+@pytest.mark.parametrize("N,M,sweeps", [(1024, 8192, 500), (2048, 2048, 1000)])
+def test_long_chains_bit_exact(N, M, sweeps):
+    # long chains through the production paths (CUDA-graph replay of PDL-launched staged /
+    # register-rolling half-sweeps, 64 sweeps per replay plus remainders) stay bit-exact
+    g = gpu_lattice(N, M, 21, "random", 0.4406868)
+    o = oracle_lattice(N, M, 21, "random", 0.4406868)
+    g.sweep(sweeps - 37)
+    g.sweep(37)
+    o.sweep(sweeps)
+    assert_same(g, o, f"{N}x{M} after {sweeps} sweeps")
+
+
 def test_persistent_kernel_path(monkeypatch):
     # opt-in persistent multi-sweep kernel (ISING_PERSISTENT=1): same lattices and series
     monkeypatch.setenv("ISING_PERSISTENT", "1")
