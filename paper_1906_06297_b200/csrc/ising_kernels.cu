@@ -38,18 +38,6 @@ __device__ __forceinline__ uint4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_
   return make_uint4(c0, c1, c2, c3);
 }
 
-__device__ __forceinline__ ulonglong2 ld_nc_v2(const uint64_t* p) {
-  ulonglong2 v;
-  asm("ld.global.nc.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p));
-  return v;
-}
-
-__device__ __forceinline__ uint64_t ld_nc(const uint64_t* p) {
-  uint64_t v;
-  asm("ld.global.nc.u64 %0, [%1];" : "=l"(v) : "l"(p));
-  return v;
-}
-
 constexpr uint32_t kLane0 = 0x11111111u;  // bit 0 of every nibble of a 32-bit half
 
 // Side-word splices (reading R10) as funnel shifts on the 32-bit halves (two
@@ -621,18 +609,18 @@ __device__ __forceinline__ void spin_until(const unsigned long long* flags, int 
     }
 }
 
-// Loads.  COHERENT (the persistent kernel, where a plane written in one phase is read by
-// other SMs in the next phase of the same launch): L2-coherent ld.global.cg; otherwise the
-// read-only path for the source plane.
+// Loads of the source plane: L2-coherent ld.global.cg everywhere.  The persistent kernel
+// reads in one phase what other SMs wrote in the previous phase of the same launch, and with
+// programmatic dependent launch a half-sweep grid is resident (its launch-time L1
+// invalidation behind it) while older grids may still run, so the non-coherent read-only path
+// (ld.global.nc, "read-only for the lifetime of the kernel") is not used for plane data.
 template <bool COHERENT>
 __device__ __forceinline__ ulonglong2 ld_v2(const uint64_t* p) {
-  if (COHERENT) return __ldcg(reinterpret_cast<const ulonglong2*>(p));
-  return ld_nc_v2(p);
+  return __ldcg(reinterpret_cast<const ulonglong2*>(p));
 }
 template <bool COHERENT>
 __device__ __forceinline__ uint64_t ld_1(const uint64_t* p) {
-  if (COHERENT) return __ldcg(reinterpret_cast<const unsigned long long*>(p));
-  return ld_nc(p);
+  return __ldcg(reinterpret_cast<const unsigned long long*>(p));
 }
 template <bool COHERENT>
 __device__ __forceinline__ ulonglong2 ld_tgt(const uint64_t* p) {
@@ -936,7 +924,7 @@ __global__ void __launch_bounds__(128, staged_minb(RULE)) k_halfsweep_staged(con
     const int rr = e >> 1;
     const int64_t col = (e & 1) ? ((w0 + kStageWords == W) ? 0 : w0 + kStageWords)
                                 : ((w0 == 0) ? W - 1 : w0 - 1);
-    edge[rr + 1][e & 1] = ld_nc(src + (int64_t)(ra + rr) * W + col);
+    edge[rr + 1][e & 1] = __ldcg(reinterpret_cast<const unsigned long long*>(src + (int64_t)(ra + rr) * W + col));
   }
   __syncthreads();
   {
