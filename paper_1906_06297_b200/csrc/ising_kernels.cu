@@ -623,9 +623,8 @@ __device__ __forceinline__ uint64_t ld_1(const uint64_t* p) {
   return __ldcg(reinterpret_cast<const unsigned long long*>(p));
 }
 template <bool COHERENT>
-__device__ __forceinline__ ulonglong2 ld_tgt(const uint64_t* p) {
-  if (COHERENT) return __ldcg(reinterpret_cast<const ulonglong2*>(p));
-  return *reinterpret_cast<const ulonglong2*>(p);
+__device__ __forceinline__ ulonglong2 ld_tgt(const uint64_t* p) {  // streaming: no L1 reuse
+  return __ldcg(reinterpret_cast<const ulonglong2*>(p));
 }
 
 // All work items of one colour phase (the half-sweep proper).  OBS: also reduce the
@@ -961,7 +960,7 @@ __global__ void __launch_bounds__(128, staged_minb(RULE)) k_halfsweep_staged(con
       side0 = splice_east(c0, c1);
       side1 = splice_east(c1, er);
     }
-    ulonglong2 tv = *reinterpret_cast<const ulonglong2*>(tp);
+    ulonglong2 tv = __ldcg(reinterpret_cast<const ulonglong2*>(tp));  // L2: see ld_v2
     const uint32_t ctr0 = (uint32_t)(4 * wc);
 #if ISING_PHILOX8
     if constexpr (lockstep_rule(RULE)) {
