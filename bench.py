@@ -1,7 +1,8 @@
 #!/usr/bin/env python
 """Benchmark: spin flips/ns of the multi-spin checkerboard Metropolis sweep on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c3|c4|c5]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c2|c3|c4|c5] [--layout multispin|basic] [--no-cpu-baseline]
 
 A step is one full sweep (black + white half-sweep) of the whole lattice.  N = 1 runs
 BASELINE.json configs[2] (C3: 32768 x 32768, beta = 0.4406868, random start, seed 1).
@@ -14,8 +15,11 @@ unavailable — config.transport says which) ("scaling": "weak").  --config c4 s
 
 value: flips/ns over the K timed sweeps, device-timed with CUDA events on the launching
 stream inside the library, max over ranks.  e2e: the same workload through the C ABI with
-host buffers — write_lattice from pinned host memory, K sweeps, observables each sweep,
-read_lattice back — all inside the timed region.  --impl reference times the CPU oracle
+host buffers — write_lattice from pinned host memory, K sweeps with the observables of each
+sweep fused into its white phase and copied to the host every step (ising_sweep_measure_async,
+the host waiting one step behind), read_lattice back — all inside the timed region.
+vs_baseline: value / the paper's single-V100 number for the same lattice (Table 2) where it
+has one (context: another machine).  --impl reference times the CPU oracle
 (oracle/, the "reference arm" of this tier) on a bounded sample of the same workload.
 """
 from __future__ import annotations
