@@ -562,10 +562,11 @@ __device__ __forceinline__ void obs_word(uint64_t t, uint64_t n, uint64_t c, uin
 // Launch with programmatic stream serialisation (the kernel itself calls
 // griddepcontrol.launch_dependents / griddepcontrol.wait before touching global memory).
 template <typename K>
-static cudaError_t launch_pdl(K kernel, unsigned grid, cudaStream_t st, const HalfSweepParams& p) {
+static cudaError_t launch_pdl(K kernel, unsigned grid, cudaStream_t st, const HalfSweepParams& p,
+                              unsigned threads = 128) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(128);
+  cfg.blockDim = dim3(threads);
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -846,14 +847,13 @@ __host__ __device__ constexpr int staged_minb(int rule) {
 __host__ __device__ constexpr int stage_rows(int rule) {
   return rule == 4 ? ISING_STAGE_ROWS_DRAWFREE : ISING_STAGE_ROWS;
 }
-constexpr int kStageWords = 256;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
 template <int RULE, bool OBS = false>
-__global__ void __launch_bounds__(128, staged_minb(RULE)) k_halfsweep_staged(const HalfSweepParams p) {
+__global__ void __launch_bounds__(kStageThreads, staged_minb(RULE)) k_halfsweep_staged(const HalfSweepParams p) {
   constexpr int kRows = stage_rows(RULE);
   // Programmatic dependent launch (p.pdl: launched with programmatic stream serialisation):
   // let the next kernel in the stream be scheduled as soon as every block of this one is
@@ -956,7 +956,7 @@ __global__ void __launch_bounds__(128, staged_minb(RULE)) k_halfsweep_staged(con
       side0 = splice_west(c0, wl);
       side1 = splice_west(c1, c0);
     } else {
-      const uint64_t er = tid == 127 ? edge[rr + 1][1] : tile[rr + 1][2 * tid + 2];
+      const uint64_t er = tid == kStageThreads - 1 ? edge[rr + 1][1] : tile[rr + 1][2 * tid + 2];
       side0 = splice_east(c0, c1);
       side1 = splice_east(c1, er);
     }
@@ -1036,15 +1036,17 @@ cudaError_t launch_halfsweep_staged(int rule, int64_t slots, cudaStream_t st, Ha
   const unsigned grid = (unsigned)(spans * bands);
   return dispatch_rule(rule, p.obs_out != nullptr, [&](auto R, auto O) {
     if (!p.pdl) {
-      k_halfsweep_staged<decltype(R)::value, decltype(O)::value><<<grid, 128, 0, st>>>(p);
+      k_halfsweep_staged<decltype(R)::value, decltype(O)::value><<<grid, kStageThreads, 0, st>>>(p);
       return cudaGetLastError();
     }
-    return launch_pdl(k_halfsweep_staged<decltype(R)::value, decltype(O)::value>, grid, st, p);
+    return launch_pdl(k_halfsweep_staged<decltype(R)::value, decltype(O)::value>, grid, st, p,
+                      kStageThreads);
   });
 }
 
 cudaError_t staged_occupancy(int* blocks_per_sm) {
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_halfsweep_staged<0>, 128, 0);
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_halfsweep_staged<0>,
+                                                       kStageThreads, 0);
 }
 
 // ------------------------------------------------------- persistent sweeps

@@ -100,6 +100,15 @@ struct SyncParams {
 // Observable all-reduce across ranks over peer memory: each rank stores its partials
 // into slot `rank` of every rank's gather area, then spins until all slots carry epoch.
 constexpr int kMaxRanks = 8;
+
+// TMA-staged half-sweep: a block owns a span of kStageWords words of a row band (2 words per
+// thread); widths that are a multiple of the span use it.  (The tile is static shared memory:
+// (rows + 2) x kStageWords x 8 B must stay within 48 KB.)
+#ifndef ISING_STAGE_WORDS
+#define ISING_STAGE_WORDS 256
+#endif
+constexpr int kStageWords = ISING_STAGE_WORDS;
+constexpr int kStageThreads = kStageWords / 2;
 struct GatherParams {
   const unsigned long long* local;       // this rank's [up, anti] partials
   unsigned long long* slots[kMaxRanks];  // rank r's gather area (3 u64 per rank)

@@ -438,7 +438,7 @@ int run_halfsweep(ising_ctx* h, Slab& s, int c, int r_begin, int r_end, uint64_t
   const bool prof = h->profiling && s.devi == 0 && h->kernel_launches < kMaxProfiledLaunches;
   if (prof) CU(cudaEventRecord(h->prof_events[2 * h->kernel_launches], d.stream));
   p.pdl = h->pdl ? 1 : 0;
-  if (h->staged && h->W % 256 == 0) {
+  if (h->staged && h->W % kStageWords == 0) {
     CU(launch_halfsweep_staged(kernel_variant(h),
                                h->guided_tail ? (int64_t)d.sms * d.staged_blocks_per_sm : 0, d.stream, p));
   } else {
