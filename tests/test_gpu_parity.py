@@ -341,6 +341,21 @@ def test_long_chains_bit_exact(N, M, sweeps):
     assert_same(g, o, f"{N}x{M} after {sweeps} sweeps")
 
 
+@pytest.mark.slow
+def test_c3_runs_are_deterministic_and_chunking_invariant():
+    # bench.py's C3 workload: two runs of 100 sweeps (one call, and 37 + 63 calls) end in the
+    # same lattice and observables (integer, race-free kernels; counter-based draws)
+    N = M = cases.C3[0]
+    digests = []
+    for plan in ([100], [37, 63]):
+        g = gpu_lattice(N, M, 1, "random", cases.C3[2])
+        for n in plan:
+            g.sweep(n)
+        digests.append((g.observables(), hashlib.sha256(g.read_lattice().tobytes()).hexdigest()))
+        g.close()
+    assert digests[0] == digests[1]
+
+
 def test_persistent_kernel_path(monkeypatch):
     # opt-in persistent multi-sweep kernel (ISING_PERSISTENT=1): same lattices and series
     monkeypatch.setenv("ISING_PERSISTENT", "1")
