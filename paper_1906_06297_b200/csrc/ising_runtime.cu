@@ -24,6 +24,8 @@
 // byte-per-spin layout (ising_create_basic, §3.1) has its own kernels.
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
+#include <sched.h>
 
 #include <algorithm>
 #include <cmath>
@@ -49,6 +51,20 @@ using namespace ising;
 namespace {
 
 thread_local std::string g_last_error;
+
+void nvtx_yield() { sched_yield(); }
+
+// NVTX ranges (SURVEY §5 tracing): one per API call that enqueues sweeps and one per
+// half-sweep launch, visible in nsys / ncu timelines; no cost without a tool attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  NvtxRange(const char* fmt, long long a, long long b) {
+    char buf[96];
+    snprintf(buf, sizeof buf, fmt, a, b);
+    nvtxRangePushA(buf);
+  }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 int fail_cuda(cudaError_t e, const char* what, int line) {
   char buf[512];
@@ -88,6 +104,9 @@ constexpr size_t kStagingBytes = size_t(64) << 20;  // pack/unpack staging chunk
 #endif
 constexpr int64_t kWordsPerItem = 2 * ISING_VPT;  // must match the kernel's kWords
 constexpr size_t kSyncBytes = 4096;                   // rank-p2p flags + gather area
+constexpr int kGatherOffset = 8;                      // u64 index of the gather area
+static_assert((kGatherOffset + 2 * 3 * ising::kMaxRanks) * 8 <= (int)kSyncBytes,
+              "gather slots (2 parities x kMaxRanks x 3 u64) must fit the sync buffer");
 constexpr int64_t kMaxProfiledLaunches = 4096;        // profiling times the first launches
 constexpr uint32_t kIpcMagic = 0x49534e47u;           // "ISNG"
 
@@ -104,6 +123,10 @@ static bool env_is_zero(const char* name) {
   const char* v = getenv(name);
   return v && v[0] == '0';
 }
+static bool env_is_one(const char* name) {
+  const char* v = getenv(name);
+  return v && v[0] == '1';
+}
 
 struct Device {
   int dev = -1;
@@ -116,7 +139,13 @@ struct Device {
   cudaEvent_t ev_bnd = nullptr;    // rank mode: boundary rows done
   cudaEvent_t ev_comm = nullptr;   // rank mode: halo exchange done
   cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;
-  int8_t* staging = nullptr;
+  // host <-> device staging of the +-1 byte lattice, double-buffered: chunk k uses buffer
+  // k & 1; copies run on `copy`, pack / unpack kernels on `stream`, ordered by the events
+  // (ev_copy[b]: last copy through buffer b done; ev_stage[b]: last kernel on b done)
+  int8_t* staging[2] = {nullptr, nullptr};
+  size_t staging_bytes = 0;
+  cudaStream_t copy = nullptr;
+  cudaEvent_t ev_copy[2] = {nullptr, nullptr}, ev_stage[2] = {nullptr, nullptr};
   unsigned long long* red = nullptr;  // [0] up, [1] antiparallel, [2] bad-value flag
   unsigned long long* meas = nullptr; // ising_sweep_measure: 2 per sample
   size_t meas_cap = 0;
@@ -163,6 +192,7 @@ struct ising_ctx {
   uint64_t t = 0;
   double last_ms = 0;
   bool profiling = false;
+  bool prof_active = false;  // inside ising_sweep with profiling on: launches are timed
   double kernel_ms = 0;
   int64_t kernel_launches = 0;
   int64_t launch_count = 0;
@@ -170,6 +200,11 @@ struct ising_ctx {
   int rows_per_item_override = 0;
   // rank-p2p transport (ising_create_rank_p2p): halos by peer stores, flags in peer memory
   bool p2p = false, connected = false;
+  // world == 1 rank handles with ISING_SELF_EXCHANGE=1: the rank is its own neighbour through
+  // the full protocol (p2p: flags / fences / peer-store path; NCCL: a one-rank communicator
+  // with self send / recv of the halo rows) — the per-GPU cost of each transport, measured
+  // on one device
+  bool self_exchange = false;
   unsigned long long* sync = nullptr;      // [0] from_up, [1] from_dn, [8 + 3 r ..] gather
   unsigned int* done_counter = nullptr;
   uint64_t* up_plane[2] = {nullptr, nullptr};
@@ -246,11 +281,22 @@ void make_keys(uint64_t seed, PhiloxKeys* K) {
   }
 }
 
+// Size limits (include/ising.h).  The draw counter (reading R6) carries the global row in a
+// 32-bit word and the plane column j / 4 = M / 8 at most in another, so L_rows <= 2^32 and
+// L_cols <= 2^35 keep every site's counter distinct; slab rows are int32 in the kernels'
+// row arithmetic (with margins for the halo rows and band heights), so R <= 2^30.
+constexpr int64_t kMaxRows = int64_t(1) << 32;
+constexpr int64_t kMaxCols = int64_t(1) << 35;
+constexpr int64_t kMaxSlabRows = int64_t(1) << 30;
+
 int check_shape(int64_t N, int64_t M, int n_slabs) {
   if (N < 2 || (N & 1) || M < 64 || (M % 64) != 0 || ((M / 32) % kWordsPerItem) != 0 ||
-      n_slabs < 1 || N % n_slabs != 0 ||
-      N / n_slabs < 2 || N > (int64_t(1) << 32) || M > (int64_t(1) << 36)) {
+      n_slabs < 1 || N % n_slabs != 0 || N / n_slabs < 2) {
     g_last_error = "shape: need L_rows even, L_rows % n == 0, L_rows/n >= 2, L_cols % 64 == 0";
+    return ISING_ERR_ARG;
+  }
+  if (N > kMaxRows || M > kMaxCols || N / n_slabs > kMaxSlabRows) {
+    g_last_error = "shape: need L_rows <= 2^32, L_cols <= 2^35, L_rows / n <= 2^30";
     return ISING_ERR_ARG;
   }
   return ISING_OK;
@@ -274,6 +320,11 @@ int setup_device(Device& d, int dev) {
   CU(cudaSetDevice(dev));
   CU(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
   CU(cudaStreamCreateWithFlags(&d.comm, cudaStreamNonBlocking));
+  CU(cudaStreamCreateWithFlags(&d.copy, cudaStreamNonBlocking));
+  for (int b = 0; b < 2; ++b) {
+    CU(cudaEventCreateWithFlags(&d.ev_copy[b], cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&d.ev_stage[b], cudaEventDisableTiming));
+  }
   CU(cudaEventCreateWithFlags(&d.ev_phase, cudaEventDisableTiming));
   CU(cudaEventCreateWithFlags(&d.ev_bnd, cudaEventDisableTiming));
   CU(cudaEventCreateWithFlags(&d.ev_comm, cudaEventDisableTiming));
@@ -303,19 +354,94 @@ int alloc_slabs(ising_ctx* h) {
   return ISING_OK;
 }
 
-int ensure_staging(Device& d) {
-  if (!d.staging) {
-    CU(cudaSetDevice(d.dev));
-    CU(cudaMalloc(&d.staging, kStagingBytes));
+// Release every resource of a Device (streams, events, buffers); safe on a partial setup.
+void teardown_device(Device& d) {
+  if (d.dev < 0) return;
+  cudaSetDevice(d.dev);
+  for (int b = 0; b < 2; ++b) {
+    if (d.staging[b]) cudaFree(d.staging[b]);
+    d.staging[b] = nullptr;
   }
+  if (d.red) cudaFree(d.red);
+  if (d.meas) cudaFree(d.meas);
+  d.red = nullptr;
+  d.meas = nullptr;
+  for (cudaEvent_t e : {d.ev_phase, d.ev_bnd, d.ev_comm, d.ev_t0, d.ev_t1, d.ev_copy[0],
+                        d.ev_copy[1], d.ev_stage[0], d.ev_stage[1]})
+    if (e) cudaEventDestroy(e);
+  for (cudaStream_t s : {d.stream, d.comm, d.copy})
+    if (s) cudaStreamDestroy(s);
+  d.dev = -1;
+}
+
+// Two staging buffers of max(64 MiB, one lattice row) bytes: a chunk always holds at least
+// one full row (the pack / unpack kernels work on whole rows).
+int ensure_staging(Device& d, int64_t row_bytes) {
+  const size_t want = std::max<size_t>(kStagingBytes, (size_t)row_bytes);
+  if (d.staging[0] && d.staging_bytes >= want) return ISING_OK;
+  CU(cudaSetDevice(d.dev));
+  for (int b = 0; b < 2; ++b) {
+    if (d.staging[b]) {
+      CU(cudaStreamSynchronize(d.stream));
+      CU(cudaStreamSynchronize(d.copy));
+      CU(cudaFree(d.staging[b]));
+      d.staging[b] = nullptr;
+    }
+  }
+  d.staging_bytes = 0;
+  for (int b = 0; b < 2; ++b) CU(cudaMalloc(&d.staging[b], want));
+  d.staging_bytes = want;
+  return ISING_OK;
+}
+
+int64_t staging_rows(const Device& d, int64_t row_bytes) {
+  return std::max<int64_t>(1, (int64_t)(d.staging_bytes / (size_t)row_bytes));
+}
+
+// Host -> device in chunks: copy(k, buf, copy_stream) fills staging buffer k & 1 on the copy
+// stream while kern(k, buf, stream) consumes the previous chunk on the compute stream.
+template <typename C, typename K>
+int pipeline_in(Device& d, int64_t nchunks, C&& copy, K&& kern) {
+  for (int64_t k = 0; k < nchunks; ++k) {
+    const int b = (int)(k & 1);
+    CU(cudaStreamWaitEvent(d.copy, d.ev_stage[b], 0));  // the kernel that last read b is done
+    TRY(copy(k, d.staging[b], d.copy));
+    CU(cudaEventRecord(d.ev_copy[b], d.copy));
+    CU(cudaStreamWaitEvent(d.stream, d.ev_copy[b], 0));
+    TRY(kern(k, d.staging[b], d.stream));
+    CU(cudaEventRecord(d.ev_stage[b], d.stream));
+  }
+  return ISING_OK;
+}
+
+// Device -> host in chunks: kern(k, buf, stream) fills staging buffer k & 1 on the compute
+// stream while copy(k, buf, copy_stream) drains the previous chunk; the compute stream then
+// waits for the last copies (so later calls on it see the host buffer complete).
+template <typename K, typename C>
+int pipeline_out(Device& d, int64_t nchunks, K&& kern, C&& copy) {
+  for (int64_t k = 0; k < nchunks; ++k) {
+    const int b = (int)(k & 1);
+    CU(cudaStreamWaitEvent(d.stream, d.ev_copy[b], 0));  // the copy that last read b is done
+    TRY(kern(k, d.staging[b], d.stream));
+    CU(cudaEventRecord(d.ev_stage[b], d.stream));
+    CU(cudaStreamWaitEvent(d.copy, d.ev_stage[b], 0));
+    TRY(copy(k, d.staging[b], d.copy));
+    CU(cudaEventRecord(d.ev_copy[b], d.copy));
+  }
+  for (int b = 0; b < 2; ++b) CU(cudaStreamWaitEvent(d.stream, d.ev_copy[b], 0));
   return ISING_OK;
 }
 
 int p2p_wait(ising_ctx* h);
 
+// rank-p2p handle whose half-sweeps run the flag protocol (neighbours, or itself)
+bool p2p_flags(const ising_ctx* h) { return h->p2p && (h->world > 1 || h->self_exchange); }
+// rank handle whose halos move by NCCL send / recv (neighbours, or itself)
+bool nccl_halos(const ising_ctx* h) { return h->rank_mode && !h->p2p && h->comm != nullptr; }
+
 void destroy_ctx(ising_ctx* h) {
   if (!h) return;
-  if (h->p2p && h->connected && h->world > 1 && !h->devs.empty()) {
+  if (p2p_flags(h) && h->connected && !h->devs.empty()) {
     // the neighbours may still be storing into this slab's halo rows (their last phase):
     // wait for them before the memory goes away (best effort: errors are ignored here)
     cudaSetDevice(h->devs[0].dev);
@@ -331,17 +457,7 @@ void destroy_ctx(ising_ctx* h) {
   for (void* ptr : h->opened) cudaIpcCloseMemHandle(ptr);
   if (h->sync) cudaFree(h->sync);
   if (h->done_counter) cudaFree(h->done_counter);
-  for (auto& d : h->devs) {
-    if (d.dev < 0) continue;
-    cudaSetDevice(d.dev);
-    if (d.staging) cudaFree(d.staging);
-    if (d.red) cudaFree(d.red);
-    if (d.meas) cudaFree(d.meas);
-    for (cudaEvent_t e : {d.ev_phase, d.ev_bnd, d.ev_comm, d.ev_t0, d.ev_t1})
-      if (e) cudaEventDestroy(e);
-    if (d.stream) cudaStreamDestroy(d.stream);
-    if (d.comm) cudaStreamDestroy(d.comm);
-  }
+  for (auto& d : h->devs) teardown_device(d);
   for (cudaEvent_t e : h->prof_events) cudaEventDestroy(e);
   for (auto& pm : h->pending) {
     for (cudaEvent_t e : {pm.t0, pm.t1, pm.done})
@@ -425,7 +541,7 @@ int run_halfsweep(ising_ctx* h, Slab& s, int c, int r_begin, int r_end, uint64_t
   p.colour = (uint32_t)c;
   p.keys = h->keys;
   p.acc = h->acc;
-  if (h->p2p && h->world > 1) {
+  if (p2p_flags(h)) {
     // wait for both neighbours to finish the previous phase; publish this one
     const int up = (h->rank + h->world - 1) % h->world, dn = (h->rank + 1) % h->world;
     p.wait_flags = h->sync;
@@ -435,7 +551,8 @@ int run_halfsweep(ising_ctx* h, Slab& s, int c, int r_begin, int r_end, uint64_t
     p.signal_value = h->phase + 1;
     p.done_counter = h->done_counter;
   }
-  const bool prof = h->profiling && s.devi == 0 && h->kernel_launches < kMaxProfiledLaunches;
+  const bool prof = h->prof_active && s.devi == 0 &&
+                    (size_t)(2 * h->kernel_launches + 1) < h->prof_events.size();
   if (prof) CU(cudaEventRecord(h->prof_events[2 * h->kernel_launches], d.stream));
   p.pdl = h->pdl ? 1 : 0;
   if (h->staged && h->W % kStageWords == 0) {
@@ -452,11 +569,60 @@ int run_halfsweep(ising_ctx* h, Slab& s, int c, int r_begin, int r_end, uint64_t
   return ISING_OK;
 }
 
+// NCCL reports failures of a peer / the network asynchronously: poll the communicator's
+// error state (SURVEY §5 failure detection).  On an error the communicator is aborted, so a
+// stream blocked in an NCCL kernel does not hang the process.
+int nccl_poll(ising_ctx* h) {
+  if (!h->comm) return ISING_OK;
+  ncclResult_t ae = ncclSuccess;
+  NC(ncclCommGetAsyncError(h->comm, &ae));
+  if (ae != ncclSuccess && ae != ncclInProgress) {
+    const int st = fail_nccl(ae, "NCCL asynchronous error (communicator aborted)", __LINE__);
+    ncclCommAbort(h->comm);
+    h->comm = nullptr;
+    return st;
+  }
+  return ISING_OK;
+}
+
+// Wait for a stream; in NCCL rank mode by polling, checking the communicator meanwhile.
+int wait_stream(ising_ctx* h, cudaStream_t st) {
+  if (!h->comm) {
+    CU(cudaStreamSynchronize(st));
+    return ISING_OK;
+  }
+  for (;;) {
+    const cudaError_t e = cudaStreamQuery(st);
+    if (e == cudaSuccess) return nccl_poll(h);
+    if (e != cudaErrorNotReady) return fail_cuda(e, "cudaStreamQuery", __LINE__);
+    TRY(nccl_poll(h));
+    nvtx_yield();
+  }
+}
+
 int sync_all(ising_ctx* h) {
   for (auto& d : h->devs) {
     CU(cudaSetDevice(d.dev));
-    CU(cudaStreamSynchronize(d.stream));
-    CU(cudaStreamSynchronize(d.comm));
+    TRY(wait_stream(h, d.stream));
+    TRY(wait_stream(h, d.comm));
+    TRY(wait_stream(h, d.copy));
+  }
+  return ISING_OK;
+}
+
+// Profiling: one event pair per timed half-sweep launch of ising_sweep (at most
+// kMaxProfiledLaunches).  Only ising_sweep times launches (h->prof_active, set after this
+// sizing); the launch paths also check the pool size, so no path can index past it.
+int ensure_prof_events(ising_ctx* h, int64_t n_sweeps) {
+  if (!h->profiling) return ISING_OK;
+  const size_t per_phase = std::max<size_t>(3, h->slabs.size());
+  const size_t want = (size_t)std::min<int64_t>(std::max<int64_t>(n_sweeps, 1), kMaxProfiledLaunches);
+  const size_t need = std::min<size_t>(want * 2 * 2 * per_phase, 2 * kMaxProfiledLaunches);
+  if (!h->devs.empty()) CU(cudaSetDevice(h->devs[0].dev));
+  while (h->prof_events.size() < need) {
+    cudaEvent_t e;
+    CU(cudaEventCreate(&e));
+    h->prof_events.push_back(e);
   }
   return ISING_OK;
 }
@@ -464,6 +630,7 @@ int sync_all(ising_ctx* h) {
 // One colour phase, LOCAL mode.
 int phase_local(ising_ctx* h, int c, uint32_t t, bool t_from_dev = false,
                 const std::vector<unsigned long long*>* obs = nullptr, bool slot_from_dev = false) {
+  NvtxRange range("half-sweep c=%lld t=%lld", c, t);
   const int n = (int)h->slabs.size();
   const bool multi_dev = h->devs.size() > 1;
   if (multi_dev) {
@@ -503,6 +670,7 @@ int phase_local(ising_ctx* h, int c, uint32_t t, bool t_from_dev = false,
 // One colour phase, RANK mode (world >= 2): boundary rows, then NCCL halo exchange
 // overlapped with the interior rows.
 int phase_rank(ising_ctx* h, int c, uint32_t t) {
+  NvtxRange range("half-sweep nccl c=%lld t=%lld", c, t);
   Slab& s = h->slabs[0];
   Device& d = h->devs[0];
   const int R = (int)s.R;
@@ -529,6 +697,7 @@ int phase_rank(ising_ctx* h, int c, uint32_t t) {
 // neighbours' previous phase, stores its boundary rows straight into their halo rows
 // over NVLink, and its last block raises their flags — compute and exchange in one kernel.
 int phase_p2p(ising_ctx* h, int c, uint32_t t, unsigned long long* obs = nullptr) {
+  NvtxRange range("half-sweep p2p c=%lld t=%lld", c, t);
   Slab& s = h->slabs[0];
   TRY(run_halfsweep(h, s, c, 0, (int)s.R, h->up_plane[c] + (s.R + 1) * h->W, h->dn_plane[c], t,
                     false, obs));
@@ -568,7 +737,7 @@ int exchange_halos(ising_ctx* h) {
 // RANK-P2P: wait until both neighbours have finished every phase issued so far (before
 // this rank overwrites its halo rows or reads them).
 int p2p_wait(ising_ctx* h) {
-  if (!(h->p2p && h->world > 1)) return ISING_OK;
+  if (!p2p_flags(h)) return ISING_OK;
   SyncParams p{};
   p.wait_flags = h->sync;
   p.wait_count = 2;
@@ -580,7 +749,7 @@ int p2p_wait(ising_ctx* h) {
 
 // RANK-P2P: a state reset (init / write) counts as a phase: publish it to the neighbours.
 int p2p_publish(ising_ctx* h) {
-  if (!(h->p2p && h->world > 1)) return ISING_OK;
+  if (!p2p_flags(h)) return ISING_OK;
   const int up = (h->rank + h->world - 1) % h->world, dn = (h->rank + 1) % h->world;
   SyncParams p{};
   p.signal[0] = h->peer_sync[up] + 1;
@@ -694,6 +863,16 @@ int enable_peers(ising_ctx* h) {
   return ISING_OK;
 }
 
+// Experiment / test knobs read once at creation (every handle type).
+void read_env_knobs(ising_ctx* h) {
+  const char* env = getenv("ISING_ROWS_PER_ITEM");
+  if (env) h->rows_per_item_override = atoi(env);
+  if (env_is_zero("ISING_GRAPHS")) h->graphs_enabled = false;
+  if (env_is_zero("ISING_DRAW_FREE")) h->draw_free_enabled = false;
+  if (env_is_zero("ISING_STAGED")) h->staged = false;
+  if (env_is_one("ISING_PERSISTENT")) h->persistent_enabled = true;
+}
+
 int create_local(ising_t* out, int64_t N, int64_t M, uint64_t seed, int n_slabs, const int* devices) {
   if (!out) return ISING_ERR_ARG;
   *out = nullptr;
@@ -731,16 +910,7 @@ int create_local(ising_t* out, int64_t N, int64_t M, uint64_t seed, int n_slabs,
     destroy_ctx(h);
     return st;
   }
-  const char* env = getenv("ISING_ROWS_PER_ITEM");
-  if (env) h->rows_per_item_override = atoi(env);
-  const char* genv = getenv("ISING_GRAPHS");
-  if (genv && genv[0] == '0') h->graphs_enabled = false;
-  const char* denv = getenv("ISING_DRAW_FREE");
-  if (denv && denv[0] == '0') h->draw_free_enabled = false;
-  const char* senv = getenv("ISING_STAGED");
-  if (senv && senv[0] == '0') h->staged = false;
-  const char* penv = getenv("ISING_PERSISTENT");
-  if (penv && penv[0] == '1') h->persistent_enabled = true;
+  read_env_knobs(h);
   *out = h;
   return ISING_OK;
 }
@@ -869,9 +1039,9 @@ int enqueue_sweeps(ising_ctx* h, int64_t n, const std::vector<unsigned long long
   for (int64_t k = k0; k <= n; ++k) {
     const uint32_t t = (uint32_t)(h->t + (uint64_t)k);
     for (int c = 0; c < 2; ++c) {
-      if (h->p2p && h->world > 1)
+      if (p2p_flags(h))
         TRY(phase_p2p(h, c, t, (k == n && obs) ? (*obs)[0] : nullptr));
-      else if (h->rank_mode && h->world > 1)
+      else if (nccl_halos(h))
         TRY(phase_rank(h, c, t));
       else
         TRY(phase_local(h, c, t, false, k == n ? obs : nullptr));
@@ -901,6 +1071,46 @@ int enqueue_observables(ising_ctx* h, const std::vector<unsigned long long*>& ou
     ++h->launch_count;
   }
   return ISING_OK;
+}
+
+// Unpack local rows [la, lb) of slab s into host rows at dst (row-major, M bytes each):
+// unpack of chunk k + 1 overlaps the D2H copy of chunk k (pipeline_out).
+int unpack_rows_to_host(ising_ctx* h, Slab& s, int64_t la, int64_t lb, int8_t* dst) {
+  Device& d = h->devs[s.devi];
+  CU(cudaSetDevice(d.dev));
+  TRY(ensure_staging(d, h->M));
+  const int64_t rpc = staging_rows(d, h->M);
+  auto span = [&](int64_t k, int64_t* ra, int64_t* rb) {
+    *ra = la + k * rpc;
+    *rb = std::min<int64_t>(*ra + rpc, lb);
+  };
+  auto kern = [&](int64_t k, int8_t* buf, cudaStream_t st) -> int {
+    int64_t ra, rb;
+    span(k, &ra, &rb);
+    UnpackParams p;
+    p.plane[0] = s.plane[0];
+    p.plane[1] = s.plane[1];
+    p.full = buf;
+    p.W = h->W;
+    p.M = h->M;
+    p.row0 = s.row0;
+    p.ra = (int32_t)ra;
+    p.rb = (int32_t)rb;
+    const int64_t total = 2 * (rb - ra) * h->W;
+    const int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)d.sms * 64);
+    k_unpack<<<grid, 256, 0, st>>>(p);
+    CU(cudaGetLastError());
+    ++h->launch_count;
+    return ISING_OK;
+  };
+  auto copy = [&](int64_t k, int8_t* buf, cudaStream_t st) -> int {
+    int64_t ra, rb;
+    span(k, &ra, &rb);
+    CU(cudaMemcpyAsync(dst + (ra - la) * h->M, buf, (size_t)((rb - ra) * h->M),
+                       cudaMemcpyDeviceToHost, st));
+    return ISING_OK;
+  };
+  return pipeline_out(d, (lb - la + rpc - 1) / rpc, kern, copy);
 }
 
 // ------------------------------------------------------------- basic layout
@@ -947,7 +1157,7 @@ int basic_enqueue_sweeps(ising_ctx* h, int64_t n, unsigned long long* obs = null
       p.acc = h->acc;
       p.keys = h->keys;
       p.obs_out = (k == n && c == 1) ? obs : nullptr;
-      const bool prof = h->profiling && h->kernel_launches < kMaxProfiledLaunches;
+      const bool prof = h->prof_active && (size_t)(2 * h->kernel_launches + 1) < h->prof_events.size();
       if (prof) CU(cudaEventRecord(h->prof_events[2 * h->kernel_launches], d.stream));
       CU(launch_basic_halfsweep(rule, listing, d.sms, d.stream, p));
       if (prof) {
@@ -964,23 +1174,33 @@ int basic_enqueue_sweeps(ising_ctx* h, int64_t n, unsigned long long* obs = null
 int basic_convert(ising_ctx* h, int8_t* host, bool to_host) {
   Device& d = h->devs[0];
   CU(cudaSetDevice(d.dev));
-  TRY(ensure_staging(d));
+  TRY(ensure_staging(d, h->M));
   const int64_t ny = h->M / 2;
   CU(cudaMemsetAsync(d.red, 0, 4 * sizeof(unsigned long long), d.stream));
-  const int64_t rows_per_chunk = std::max<int64_t>(1, (int64_t)kStagingBytes / h->M);
-  for (int64_t r0 = 0; r0 < h->N; r0 += rows_per_chunk) {
-    const int64_t rows = std::min<int64_t>(rows_per_chunk, h->N - r0);
-    const size_t bytes = (size_t)(rows * h->M);
-    if (!to_host)
-      CU(cudaMemcpyAsync(d.staging, host + r0 * h->M, bytes, cudaMemcpyHostToDevice, d.stream));
-    CU(launch_basic_convert(basic_grid(d, rows * h->M), d.stream, h->bplane[0], h->bplane[1],
-                            d.staging, ny, r0, rows, to_host ? 1 : 0,
+  const int64_t rpc = staging_rows(d, h->M);
+  const int64_t nchunks = (h->N + rpc - 1) / rpc;
+  auto rows_of = [&](int64_t k) { return std::min<int64_t>(rpc, h->N - k * rpc); };
+  auto kern = [&](int64_t k, int8_t* buf, cudaStream_t st) -> int {
+    CU(launch_basic_convert(basic_grid(d, rows_of(k) * h->M), st, h->bplane[0], h->bplane[1], buf,
+                            ny, k * rpc, rows_of(k), to_host ? 1 : 0,
                             reinterpret_cast<unsigned int*>(d.red + 2)));
     ++h->launch_count;
+    return ISING_OK;
+  };
+  auto copy = [&](int64_t k, int8_t* buf, cudaStream_t st) -> int {
+    const size_t bytes = (size_t)(rows_of(k) * h->M);
     if (to_host)
-      CU(cudaMemcpyAsync(host + r0 * h->M, d.staging, bytes, cudaMemcpyDeviceToHost, d.stream));
-  }
+      CU(cudaMemcpyAsync(host + k * rpc * h->M, buf, bytes, cudaMemcpyDeviceToHost, st));
+    else
+      CU(cudaMemcpyAsync(buf, host + k * rpc * h->M, bytes, cudaMemcpyHostToDevice, st));
+    return ISING_OK;
+  };
+  if (to_host)
+    TRY(pipeline_out(d, nchunks, kern, copy));
+  else
+    TRY(pipeline_in(d, nchunks, copy, kern));
   CU(cudaStreamSynchronize(d.stream));
+  CU(cudaStreamSynchronize(d.copy));
   if (!to_host) {
     unsigned long long bad = 0;
     CU(cudaMemcpy(&bad, d.red + 2, sizeof bad, cudaMemcpyDeviceToHost));
@@ -1061,19 +1281,23 @@ int ising_create_rank(ising_t* out, int64_t L_rows, int64_t L_cols, uint64_t see
   s.row0 = rank * s.R;
   h->slabs.push_back(s);
   st = alloc_slabs(h);
-  if (st == ISING_OK && world > 1) {
+  h->self_exchange = world == 1 && env_is_one("ISING_SELF_EXCHANGE");
+  if (st == ISING_OK && (world > 1 || h->self_exchange)) {
     ncclUniqueId u;
-    memcpy(&u, nccl_id, sizeof u);
+    ncclResult_t r = ncclSuccess;
+    if (world > 1)
+      memcpy(&u, nccl_id, sizeof u);
+    else
+      r = ncclGetUniqueId(&u);  // a one-rank communicator: the rank exchanges with itself
     cudaSetDevice(device);
-    ncclResult_t r = ncclCommInitRank(&h->comm, world, u, rank);
+    if (r == ncclSuccess) r = ncclCommInitRank(&h->comm, world, u, rank);
     if (r != ncclSuccess) st = fail_nccl(r, "ncclCommInitRank", __LINE__);
   }
   if (st != ISING_OK) {
     destroy_ctx(h);
     return st;
   }
-  const char* env = getenv("ISING_ROWS_PER_ITEM");
-  if (env) h->rows_per_item_override = atoi(env);
+  read_env_knobs(h);
   *out = h;
   return ISING_OK;
 }
@@ -1121,13 +1345,15 @@ int ising_create_rank_p2p(ising_t* out, int64_t L_rows, int64_t L_cols, uint64_t
     destroy_ctx(h);
     return st;
   }
-  if (world == 1) {  // its own neighbour: plain fused halos, no flags
+  if (world == 1) {  // its own neighbour: fused halos into its own rows (flags only in
+                     // self-exchange mode)
     h->up_plane[0] = h->dn_plane[0] = h->slabs[0].plane[0];
     h->up_plane[1] = h->dn_plane[1] = h->slabs[0].plane[1];
+    h->peer_sync[0] = h->sync;
+    h->self_exchange = env_is_one("ISING_SELF_EXCHANGE");
     h->connected = true;
   }
-  const char* env = getenv("ISING_ROWS_PER_ITEM");
-  if (env) h->rows_per_item_override = atoi(env);
+  read_env_knobs(h);
   *out = h;
   return ISING_OK;
 }
@@ -1135,8 +1361,12 @@ int ising_create_rank_p2p(ising_t* out, int64_t L_rows, int64_t L_cols, uint64_t
 int ising_create_basic(ising_t* out, int64_t L_rows, int64_t L_cols, uint64_t seed, int device) {
   if (!out) return ISING_ERR_ARG;
   *out = nullptr;
-  if (L_rows < 2 || (L_rows & 1) || L_cols < 8 || (L_cols % 8) != 0 || L_rows > (int64_t(1) << 32)) {
+  if (L_rows < 2 || (L_rows & 1) || L_cols < 8 || (L_cols % 8) != 0) {
     g_last_error = "basic layout: need L_rows even >= 2 and L_cols % 8 == 0";
+    return ISING_ERR_ARG;
+  }
+  if (L_rows > kMaxRows || L_cols > kMaxCols) {  // same draw-counter limits as check_shape
+    g_last_error = "basic layout: need L_rows <= 2^32 and L_cols <= 2^35";
     return ISING_ERR_ARG;
   }
   ising_ctx* h = new (std::nothrow) ising_ctx;
@@ -1164,6 +1394,7 @@ int ising_create_basic(ising_t* out, int64_t L_rows, int64_t L_cols, uint64_t se
     destroy_ctx(h);
     return st;
   }
+  read_env_knobs(h);
   *out = h;
   return ISING_OK;
 }
@@ -1218,6 +1449,48 @@ int ising_ipc_connect(ising_t h, const void* blobs, size_t len) {
     }
   }
   h->connected = true;
+  return ISING_OK;
+}
+
+int ising_p2p_connect_local(const ising_t* handles, int n) {
+  if (!handles || n < 1 || n > kMaxRanks) return ISING_ERR_ARG;
+  for (int r = 0; r < n; ++r) {
+    const ising_t h = handles[r];
+    if (!h || !h->p2p || h->world != n || h->rank != r || h->N != handles[0]->N ||
+        h->M != handles[0]->M || h->seed != handles[0]->seed) {
+      g_last_error = "ising_p2p_connect_local: handles[r] must be rank r of one rank-p2p lattice";
+      return ISING_ERR_ARG;
+    }
+  }
+  if (n == 1) return ISING_OK;  // connected at creation
+  for (int r = 0; r < n; ++r) {
+    ising_t h = handles[r];
+    if (h->connected) continue;
+    const int up = (r + n - 1) % n, dn = (r + 1) % n;
+    const int dev = h->devs[0].dev;
+    CU(cudaSetDevice(dev));
+    for (int q : {up, dn}) {  // direct peer access to the neighbours' memory (NVLink P2P)
+      const int qd = handles[q]->devs[0].dev;
+      if (qd == dev) continue;
+      int can = 0;
+      CU(cudaDeviceCanAccessPeer(&can, dev, qd));
+      if (!can) {
+        g_last_error = "ising_p2p_connect_local: no P2P access between neighbouring devices";
+        return ISING_ERR_DEVICE;
+      }
+      cudaError_t e = cudaDeviceEnablePeerAccess(qd, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled)
+        cudaGetLastError();
+      else if (e != cudaSuccess)
+        return fail_cuda(e, "cudaDeviceEnablePeerAccess", __LINE__);
+    }
+    for (int q = 0; q < n; ++q) h->peer_sync[q] = handles[q]->sync;
+    for (int c = 0; c < 2; ++c) {
+      h->up_plane[c] = handles[up]->slabs[0].plane[c];
+      h->dn_plane[c] = handles[dn]->slabs[0].plane[c];
+    }
+    h->connected = true;
+  }
   return ISING_OK;
 }
 
@@ -1296,25 +1569,43 @@ int ising_write_lattice(ising_t h, const int8_t* in, int64_t in_len, uint64_t t)
   const bool slab_only = h->rank_mode && h->world > 1 && in_len == h->slabs[0].R * h->M;
   if (!slab_only && in_len < h->N * h->M) return ISING_ERR_RANGE;
   if (h->p2p && h->world > 1 && !h->connected) return ISING_ERR_STATE;
-  TRY(p2p_wait(h));
+  if (p2p_flags(h)) {
+    // wait (by polling the stream, not inside a copy) until the neighbours are done with
+    // this slab's halo rows, before any possibly pageable host copy is issued (see the
+    // rank-p2p branch of ising_sweep_measure)
+    TRY(p2p_wait(h));
+    TRY(wait_stream(h, h->devs[0].stream));
+  }
   for (auto& s : h->slabs) {
     Device& d = h->devs[s.devi];
     CU(cudaSetDevice(d.dev));
-    TRY(ensure_staging(d));
+    TRY(ensure_staging(d, h->M));
     CU(cudaMemsetAsync(d.red, 0, 4 * sizeof(unsigned long long), d.stream));
-    const int64_t rows_per_chunk = std::max<int64_t>(1, (int64_t)kStagingBytes / h->M);
+    const int64_t rpc = staging_rows(d, h->M);
     const int64_t r_lo = slab_only ? 0 : -1, r_hi = slab_only ? s.R : s.R + 1;
-    for (int64_t ra = r_lo; ra < r_hi; ra += rows_per_chunk) {
-      const int64_t rb = std::min<int64_t>(ra + rows_per_chunk, r_hi);
+    const int64_t nchunks = (r_hi - r_lo + rpc - 1) / rpc;
+    auto span = [&](int64_t k, int64_t* ra, int64_t* rb) {
+      *ra = r_lo + k * rpc;
+      *rb = std::min<int64_t>(*ra + rpc, r_hi);
+    };
+    // H2D of chunk k + 1 overlaps the packing of chunk k (pipeline_in)
+    auto copy = [&](int64_t k, int8_t* buf, cudaStream_t st) -> int {
+      int64_t ra, rb;
+      span(k, &ra, &rb);
       if (slab_only)
-        CU(cudaMemcpyAsync(d.staging, in + ra * h->M, (size_t)((rb - ra) * h->M),
-                           cudaMemcpyHostToDevice, d.stream));
+        CU(cudaMemcpyAsync(buf, in + ra * h->M, (size_t)((rb - ra) * h->M),
+                           cudaMemcpyHostToDevice, st));
       else
-        TRY(h2d_rows(h, d.staging, in, s.row0 + ra, rb - ra, d.stream));
+        TRY(h2d_rows(h, buf, in, s.row0 + ra, rb - ra, st));
+      return ISING_OK;
+    };
+    auto kern = [&](int64_t k, int8_t* buf, cudaStream_t st) -> int {
+      int64_t ra, rb;
+      span(k, &ra, &rb);
       PackParams p;
       p.plane[0] = s.plane[0];
       p.plane[1] = s.plane[1];
-      p.full = d.staging;
+      p.full = buf;
       p.W = h->W;
       p.M = h->M;
       p.row0 = s.row0;
@@ -1324,10 +1615,12 @@ int ising_write_lattice(ising_t h, const int8_t* in, int64_t in_len, uint64_t t)
       p.bad = reinterpret_cast<unsigned int*>(d.red + 2);
       const int64_t total = 2 * (rb - ra) * h->W;
       const int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)d.sms * 64);
-      k_pack<<<grid, 256, 0, d.stream>>>(p);
+      k_pack<<<grid, 256, 0, st>>>(p);
       CU(cudaGetLastError());
       ++h->launch_count;
-    }
+      return ISING_OK;
+    };
+    TRY(pipeline_in(d, nchunks, copy, kern));
   }
   if (slab_only) TRY(exchange_halos(h));
   TRY(p2p_publish(h));
@@ -1352,22 +1645,17 @@ int ising_sweep(ising_t h, int64_t n) {
   if (!h->beta_set || !h->state_set) return ISING_ERR_STATE;
   if (h->p2p && h->world > 1 && !h->connected) return ISING_ERR_STATE;
   if (h->t + (uint64_t)n > 0xffffffffull) return ISING_ERR_RANGE;
-  if (h->profiling) {
-    const size_t per_phase = std::max<size_t>(3, h->slabs.size());
-    const size_t need = std::min<size_t>((size_t)n * 2 * 2 * per_phase, 2 * kMaxProfiledLaunches);
-    if (!h->devs.empty()) CU(cudaSetDevice(h->devs[0].dev));
-    while (h->prof_events.size() < need) {
-      cudaEvent_t e;
-      CU(cudaEventCreate(&e));
-      h->prof_events.push_back(e);
-    }
-  }
+  NvtxRange range("ising_sweep n=%lld t0=%lld", n, (long long)h->t);
+  TRY(ensure_prof_events(h, n));
   h->kernel_launches = 0;
   for (auto& d : h->devs) {
     CU(cudaSetDevice(d.dev));
     CU(cudaEventRecord(d.ev_t0, d.stream));
   }
-  TRY(h->basic ? basic_enqueue_sweeps(h, n) : enqueue_sweeps(h, n));
+  h->prof_active = h->profiling;
+  const int est = h->basic ? basic_enqueue_sweeps(h, n) : enqueue_sweeps(h, n);
+  h->prof_active = false;
+  TRY(est);
   for (auto& d : h->devs) {
     CU(cudaSetDevice(d.dev));
     CU(cudaEventRecord(d.ev_t1, d.stream));
@@ -1400,29 +1688,8 @@ int ising_read_lattice(ising_t h, int8_t* out, int64_t out_len) {
   if (!h->state_set) return ISING_ERR_STATE;
   if (h->basic) return basic_convert(h, out, true);
   for (auto& s : h->slabs) {
-    Device& d = h->devs[s.devi];
-    CU(cudaSetDevice(d.dev));
-    TRY(ensure_staging(d));
-    const int64_t rows_per_chunk = std::max<int64_t>(1, (int64_t)kStagingBytes / h->M);
-    for (int64_t ra = 0; ra < s.R; ra += rows_per_chunk) {
-      const int64_t rb = std::min<int64_t>(ra + rows_per_chunk, s.R);
-      UnpackParams p;
-      p.plane[0] = s.plane[0];
-      p.plane[1] = s.plane[1];
-      p.full = d.staging;
-      p.W = h->W;
-      p.M = h->M;
-      p.row0 = s.row0;
-      p.ra = (int32_t)ra;
-      p.rb = (int32_t)rb;
-      const int64_t total = 2 * (rb - ra) * h->W;
-      const int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)d.sms * 64);
-      k_unpack<<<grid, 256, 0, d.stream>>>(p);
-      CU(cudaGetLastError());
-      ++h->launch_count;
-      CU(cudaMemcpyAsync(out + ((slab_only ? 0 : s.row0) + ra) * h->M, d.staging,
-                         (size_t)((rb - ra) * h->M), cudaMemcpyDeviceToHost, d.stream));
-    }
+    // local rows [0, R) of this slab -> host rows starting at its global row (or at 0)
+    TRY(unpack_rows_to_host(h, s, 0, s.R, out + (slab_only ? 0 : s.row0) * h->M));
   }
   TRY(sync_all(h));
   return ISING_OK;
@@ -1436,16 +1703,21 @@ int ising_read_rows(ising_t h, int64_t row_begin, int64_t nrows, int8_t* out, in
   if (h->basic) {
     Device& d = h->devs[0];
     CU(cudaSetDevice(d.dev));
-    TRY(ensure_staging(d));
-    const int64_t rows_per_chunk = std::max<int64_t>(1, (int64_t)kStagingBytes / h->M);
-    for (int64_t r0 = row_begin; r0 < row_begin + nrows; r0 += rows_per_chunk) {
-      const int64_t rows = std::min<int64_t>(rows_per_chunk, row_begin + nrows - r0);
-      CU(launch_basic_convert(basic_grid(d, rows * h->M), d.stream, h->bplane[0], h->bplane[1],
-                              d.staging, h->M / 2, r0, rows, 1, nullptr));
+    TRY(ensure_staging(d, h->M));
+    const int64_t rpc = staging_rows(d, h->M);
+    auto rows_of = [&](int64_t k) { return std::min<int64_t>(rpc, nrows - k * rpc); };
+    auto kern = [&](int64_t k, int8_t* buf, cudaStream_t st) -> int {
+      CU(launch_basic_convert(basic_grid(d, rows_of(k) * h->M), st, h->bplane[0], h->bplane[1],
+                              buf, h->M / 2, row_begin + k * rpc, rows_of(k), 1, nullptr));
       ++h->launch_count;
-      CU(cudaMemcpyAsync(out + (r0 - row_begin) * h->M, d.staging, (size_t)(rows * h->M),
-                         cudaMemcpyDeviceToHost, d.stream));
-    }
+      return ISING_OK;
+    };
+    auto copy = [&](int64_t k, int8_t* buf, cudaStream_t st) -> int {
+      CU(cudaMemcpyAsync(out + k * rpc * h->M, buf, (size_t)(rows_of(k) * h->M),
+                         cudaMemcpyDeviceToHost, st));
+      return ISING_OK;
+    };
+    TRY(pipeline_out(d, (nrows + rpc - 1) / rpc, kern, copy));
     CU(cudaStreamSynchronize(d.stream));
     return ISING_OK;
   }
@@ -1454,29 +1726,7 @@ int ising_read_rows(ising_t h, int64_t row_begin, int64_t nrows, int8_t* out, in
     const int64_t lo = std::max(row_begin, s.row0), hi = std::min(row_begin + nrows, s.row0 + s.R);
     if (lo >= hi) continue;
     covered += hi - lo;
-    Device& d = h->devs[s.devi];
-    CU(cudaSetDevice(d.dev));
-    TRY(ensure_staging(d));
-    const int64_t rows_per_chunk = std::max<int64_t>(1, (int64_t)kStagingBytes / h->M);
-    for (int64_t ga = lo; ga < hi; ga += rows_per_chunk) {
-      const int64_t gb = std::min<int64_t>(ga + rows_per_chunk, hi);
-      UnpackParams p;
-      p.plane[0] = s.plane[0];
-      p.plane[1] = s.plane[1];
-      p.full = d.staging;
-      p.W = h->W;
-      p.M = h->M;
-      p.row0 = s.row0;
-      p.ra = (int32_t)(ga - s.row0);
-      p.rb = (int32_t)(gb - s.row0);
-      const int64_t total = 2 * (gb - ga) * h->W;
-      const int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)d.sms * 64);
-      k_unpack<<<grid, 256, 0, d.stream>>>(p);
-      CU(cudaGetLastError());
-      ++h->launch_count;
-      CU(cudaMemcpyAsync(out + (ga - row_begin) * h->M, d.staging, (size_t)((gb - ga) * h->M),
-                         cudaMemcpyDeviceToHost, d.stream));
-    }
+    TRY(unpack_rows_to_host(h, s, lo - s.row0, hi - s.row0, out + (lo - row_begin) * h->M));
   }
   TRY(sync_all(h));
   if (covered != nrows) {
@@ -1498,20 +1748,20 @@ int ising_observables(ising_t h, int64_t* up_count, int64_t* bond_energy) {
     outs.push_back(d.red);
   }
   TRY(enqueue_observables(h, outs));
-  if (h->p2p && h->world > 1) {
+  if (p2p_flags(h)) {
     // all-reduce of the two partials over peer memory
     Device& d = h->devs[0];
     GatherParams g{};
     g.local = d.red;
-    for (int r = 0; r < h->world; ++r) g.slots[r] = h->peer_sync[r] + 8;
-    g.mine = h->sync + 8;
+    for (int r = 0; r < h->world; ++r) g.slots[r] = h->peer_sync[r] + kGatherOffset;
+    g.mine = h->sync + kGatherOffset;
     g.out = d.red;
     g.world = h->world;
     g.rank = h->rank;
     g.epoch = ++h->gather_epoch;
     CU(launch_gather(d.stream, g));
     ++h->launch_count;
-  } else if (h->rank_mode && h->world > 1) {
+  } else if (nccl_halos(h)) {
     Device& d = h->devs[0];
     NC(ncclAllReduce(d.red, d.red, 2, ncclUint64, ncclSum, h->comm, d.stream));
   }
@@ -1554,7 +1804,6 @@ static int measure_enqueue(ising_ctx* h, int64_t n_samples, int64_t every) {
     base.push_back(d.meas);
     CU(cudaEventRecord(d.ev_t0, d.stream));
   }
-  h->kernel_launches = 0;
   std::vector<unsigned long long*> slot(base.size());
   if (h->basic) {  // byte layout: observables fused into each sample's last white phase
     for (int64_t k = 0; k < n_samples; ++k) TRY(basic_enqueue_sweeps(h, every, base[0] + 2 * k));
@@ -1596,7 +1845,7 @@ int ising_sweep_measure(ising_t h, int64_t n_samples, int64_t every, int64_t* up
     return ISING_ERR_ARG;
   if (!h->beta_set || !h->state_set) return ISING_ERR_STATE;
   if (h->t + (uint64_t)(n_samples * every) > 0xffffffffull) return ISING_ERR_RANGE;
-  if (h->p2p && h->world > 1) {
+  if (p2p_flags(h)) {
     // rank-p2p: the sample's observables are fused into its last white phase (this slab's
     // partials), then all-reduced over peer memory (k_gather) and read back; one host sync
     // per sample keeps consecutive gathers of the shared slots apart
@@ -1611,17 +1860,21 @@ int ising_sweep_measure(ising_t h, int64_t n_samples, int64_t every, int64_t* up
       CU(cudaEventRecord(d.ev_t1, d.stream));
       GatherParams g{};
       g.local = d.red;
-      for (int r = 0; r < h->world; ++r) g.slots[r] = h->peer_sync[r] + 8;
-      g.mine = h->sync + 8;
+      for (int r = 0; r < h->world; ++r) g.slots[r] = h->peer_sync[r] + kGatherOffset;
+      g.mine = h->sync + kGatherOffset;
       g.out = d.red;
       g.world = h->world;
       g.rank = h->rank;
       g.epoch = ++h->gather_epoch;
       CU(launch_gather(d.stream, g));
       ++h->launch_count;
+      // Wait for the stream first: a copy to pageable memory issued while this stream still
+      // waits on the other ranks blocks this thread inside the driver, where it can keep the
+      // other ranks' threads of the same process (ising_p2p_connect_local) from launching
+      // the phases it waits for.
+      TRY(wait_stream(h, d.stream));
       unsigned long long v[2];
-      CU(cudaMemcpyAsync(v, d.red, sizeof v, cudaMemcpyDeviceToHost, d.stream));
-      CU(cudaStreamSynchronize(d.stream));
+      CU(cudaMemcpy(v, d.red, sizeof v, cudaMemcpyDeviceToHost));
       float ms = 0;
       CU(cudaEventElapsedTime(&ms, d.ev_t0, d.ev_t1));
       total += ms;
@@ -1631,7 +1884,7 @@ int ising_sweep_measure(ising_t h, int64_t n_samples, int64_t every, int64_t* up
     h->last_ms = total;
     return ISING_OK;
   }
-  if ((h->rank_mode && h->world > 1) || (h->basic && !basic_fused_obs(h))) {
+  if (nccl_halos(h) || (h->basic && !basic_fused_obs(h))) {
     // rank-NCCL / listing-shaped basic kernel: sweep, then the separate observables pass
     // (all-reduced over NCCL in rank mode) per sample
     double total = 0;
@@ -1686,7 +1939,7 @@ int ising_sweep_measure_async(ising_t h, int64_t n_samples, int64_t every, int64
   pm->energy = bond_energies;
   pm->n = n_samples;
   pm->ready = false;
-  if ((h->rank_mode && h->world > 1) || (h->basic && !basic_fused_obs(h)) || h->devs.size() > 1 ||
+  if (p2p_flags(h) || nccl_halos(h) || (h->basic && !basic_fused_obs(h)) || h->devs.size() > 1 ||
       n_samples == 0) {
     // cross-device reductions: the synchronous path, complete on return
     TRY(ising_sweep_measure(h, n_samples, every, up_counts, bond_energies));
@@ -1825,10 +2078,7 @@ int ising_probe_philox(int device, double* draws_per_ns) {
   cudaEventDestroy(a);
   cudaEventDestroy(b);
   cudaFree(sink);
-  cudaFree(d.red);
-  cudaStreamDestroy(d.stream);
-  cudaStreamDestroy(d.comm);
-  for (cudaEvent_t e : {d.ev_phase, d.ev_bnd, d.ev_comm, d.ev_t0, d.ev_t1}) cudaEventDestroy(e);
+  teardown_device(d);
   *draws_per_ns = best;
   return ISING_OK;
 }

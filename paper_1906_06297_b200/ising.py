@@ -41,6 +41,7 @@ SIGNATURES = {
     "ising_create_basic": (_INT, [ctypes.POINTER(_VP), _I64, _I64, _U64, _INT]),
     "ising_ipc_handle": (_INT, [_VP, _VP, _SZ]),
     "ising_ipc_connect": (_INT, [_VP, _VP, _SZ]),
+    "ising_p2p_connect_local": (_INT, [ctypes.POINTER(_VP), _INT]),
     "ising_destroy": (_INT, [_VP]),
     "ising_set_beta": (_INT, [_VP, _DBL]),
     "ising_set_rule": (_INT, [_VP, _INT]),
@@ -174,6 +175,11 @@ def ising_ipc_handle(h: int) -> bytes:
 def ising_ipc_connect(h: int, blobs: bytes) -> None:
     buf = ctypes.create_string_buffer(blobs, len(blobs))
     _check(load().ising_ipc_connect(h, buf, len(blobs)), "ising_ipc_connect")
+
+
+def ising_p2p_connect_local(handles) -> None:
+    arr = (_VP * len(handles))(*handles)
+    _check(load().ising_p2p_connect_local(arr, len(handles)), "ising_p2p_connect_local")
 
 
 def ising_destroy(h: int) -> None:
@@ -342,18 +348,26 @@ class IsingLattice:
             device = int(os.environ.get("LOCAL_RANK", rank))
         if transport == "p2p":
             # every rank must agree: if CUDA IPC / peer mapping fails anywhere, all ranks
-            # fall back to the NCCL transport together (both are GPU paths)
-            h, err = None, None
+            # fall back to the NCCL transport together (both are GPU paths).  Every rank
+            # makes the same collective calls whatever failed locally.
+            h, err, blob = None, None, None
             try:
                 h = ising_create_rank_p2p(L_rows, L_cols, seed, rank, world, device)
-                blobs = [None] * world
-                dist.all_gather_object(blobs, ising_ipc_handle(h))
-                ising_ipc_connect(h, b"".join(blobs))
+                blob = ising_ipc_handle(h)
             except IsingError as e:
                 err = e
-            ok = [err is None]
+            blobs = [None] * world
+            dist.all_gather_object(blobs, blob)
+            if err is None:
+                if any(b is None for b in blobs):
+                    err = "IPC handle export failed on another rank"
+                else:
+                    try:
+                        ising_ipc_connect(h, b"".join(blobs))
+                    except IsingError as e:
+                        err = e
             oks = [None] * world
-            dist.all_gather_object(oks, ok[0])
+            dist.all_gather_object(oks, err is None)
             if all(oks):
                 lat = cls(L_rows, L_cols, seed, _handle=h)
                 lat.transport = "p2p"
@@ -374,6 +388,26 @@ class IsingLattice:
         lat = cls(L_rows, L_cols, seed, _handle=h)
         lat.transport = "nccl"
         return lat
+
+    @classmethod
+    def local_group(cls, L_rows: int, L_cols: int, world: int, seed: int = 1, devices=None):
+        """All `world` ranks of one rank-p2p lattice in this process (ising_p2p_connect_local):
+        rank r on devices[r] (default: all on device 0).  Drive them from one host thread each
+        (every collective call must be made on every handle); see run_ranks."""
+        devices = list(devices) if devices is not None else [0] * world
+        hs = []
+        try:
+            for r in range(world):
+                hs.append(ising_create_rank_p2p(L_rows, L_cols, seed, r, world, devices[r]))
+            ising_p2p_connect_local(hs)
+        except Exception:
+            for h in hs:
+                ising_destroy(h)
+            raise
+        lats = [cls(L_rows, L_cols, seed, _handle=h) for h in hs]
+        for lat in lats:
+            lat.transport = "p2p-local"
+        return lats
 
     def close(self):
         if getattr(self, "h", None):
@@ -466,3 +500,29 @@ class IsingLattice:
 
     def kernel_variant(self) -> int:
         return ising_kernel_variant(self.h)
+
+
+def run_ranks(lats, fn):
+    """Run fn(rank, lattice) on one host thread per rank of a local group and return the
+    results in rank order (the ctypes calls release the GIL, so the ranks' host calls and
+    their kernels run concurrently).  An exception on any rank is re-raised."""
+    import threading
+
+    out = [None] * len(lats)
+    errs = []
+
+    def body(r):
+        try:
+            out[r] = fn(r, lats[r])
+        except BaseException as e:  # reported below
+            errs.append((r, e))
+
+    ths = [threading.Thread(target=body, args=(r,)) for r in range(len(lats))]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    if errs:
+        r, e = errs[0]
+        raise RuntimeError(f"rank {r}: {e!r}") from e
+    return out

@@ -65,3 +65,40 @@ def test_no_device_is_an_error_not_a_fallback():
     with pytest.raises(ising.IsingError) as ei:
         ising.ising_create(64, 64, 1, 1)
     assert ei.value.status in (ising.ISING_ERR_CUDA, ising.ISING_ERR_DEVICE)
+
+
+def test_shapes_beyond_the_draw_counter_or_int32_slab_rows_are_rejected():
+    """The draw counter (reading R6) holds the global row and the plane column / 4 in 32-bit
+    words, and slab rows are int32 in the kernels: L_rows > 2^32, L_cols > 2^35 and slab rows
+    > 2^30 must be ARG errors from every constructor, before any device call (no GPU here)."""
+    big_rows = [(1 << 33, 64, 1), (1 << 31, 64, 1), ((1 << 31) + 2, 64, 1)]  # R >= 2^31
+    big_cols = [(64, 1 << 36, 1), (64, (1 << 35) + 64, 1)]                # M > 2^35
+    slab_rows = [((1 << 30) + 2, 64, 1), (1 << 32, 64, 2)]               # R > 2^30
+    for N, M, n in big_rows + big_cols + slab_rows:
+        with pytest.raises(ising.IsingError) as ei:
+            ising.ising_create(N, M, 1, n)
+        assert ei.value.status == ising.ISING_ERR_ARG, (N, M, n)
+        with pytest.raises(ising.IsingError) as ei:
+            ising.ising_create_rank_p2p(N, M, 1, 0, n, 0)
+        assert ei.value.status == ising.ISING_ERR_ARG, (N, M, n)
+        with pytest.raises(ising.IsingError) as ei:
+            ising.ising_create_rank(N, M, 1, 0, 1, 0, None)
+        assert ei.value.status == ising.ISING_ERR_ARG, (N, M)
+    # 2^32 rows in 4 slabs of 2^30 is within every limit: it gets past the shape check and
+    # fails only at the device (none here)
+    with pytest.raises(ising.IsingError) as ei:
+        ising.ising_create(1 << 32, 64, 1, 4)
+    assert ei.value.status in (ising.ISING_ERR_CUDA, ising.ISING_ERR_DEVICE)
+    for N, M in [(1 << 33, 64), (64, 1 << 36), ((1 << 32) + 2, 64)]:
+        with pytest.raises(ising.IsingError) as ei:
+            ising.ising_create_basic(N, M, 1, 0)
+        assert ei.value.status == ising.ISING_ERR_ARG, (N, M)
+
+
+def test_connect_local_argument_errors():
+    lib = ising.load()
+    assert lib.ising_p2p_connect_local(None, 2) == ising.ISING_ERR_ARG
+    arr = (ising._VP * 2)(None, None)
+    assert lib.ising_p2p_connect_local(arr, 2) == ising.ISING_ERR_ARG
+    assert lib.ising_p2p_connect_local(arr, 0) == ising.ISING_ERR_ARG
+    assert lib.ising_p2p_connect_local(arr, 9) == ising.ISING_ERR_ARG

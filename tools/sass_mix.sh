@@ -1,0 +1,4 @@
+#!/bin/bash
+# Instruction mix of one kernel's SASS: tools/sass_mix.sh LIB.so MANGLED_NAME
+cuobjdump -sass "$1" 2>/dev/null | awk -v f="$2" '/Function :/{on = ($3 == f)} on' | \
+  grep -oE "^\s+/\*[0-9a-f]+\*/\s+[A-Z0-9_.]+" | awk '{split($2,a,"."); print a[1]}' | sort | uniq -c | sort -rn | head -${3:-22}
