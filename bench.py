@@ -44,6 +44,7 @@ BYTES_PER_FLIP = 1.5  # 4-bit spins: read target + read source + write target (D
 MULWIDE_PER_FLIP = 4.0  # per-thread 32x32->64 multiplies per draw (16 per Philox block / 4, R6)
 IMADWIDE_PER_CLK_SM = 27.65  # measured IMAD.WIDE.U32 issue rate (profiles/r01_pipes_microbench.txt)
 TRAFFIC_FILE = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+JSON_OUT = sys.stdout  # the bench line's stream (run_ours keeps the real stdout for it)
 # PAPER.md Table 2 (multi-spin kernel, one V100-SXM): lattice -> (flips/ns, line)
 PAPER_TABLE2 = {(2048, 2048): (231.09, "P:277"), (4096, 4096): (318.95, "P:278"),
                 (8192, 8192): (379.27, "P:279"), (16384, 16384): (411.65, "P:280"),
@@ -707,7 +708,7 @@ def run_ours(args):
             "legs": legs or None,
             "clocks": clocks,
         }
-        print(json.dumps(line), flush=True)
+        print(json.dumps(line), file=JSON_OUT, flush=True)
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
@@ -749,6 +750,11 @@ def main():
         return run_reference(args)
     if "WORLD_SIZE" not in os.environ and args.gpus > 1:
         return spawn(args)
+    # stdout carries exactly one JSON line: anything the libraries print (NCCL's version
+    # banner, ...) goes to stderr
+    global JSON_OUT
+    JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if world != args.gpus:
         print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)

@@ -1,7 +1,8 @@
 /* Plain-C use of the library (no Python, no PyTorch): the calls the north_star lists, then
  * a measured chain through the asynchronous API (two calls in flight).
- *   ising_c_example L_rows L_cols seed beta sweeps
- *     -> line 1: "up E t sum" after `sweeps` sweeps
+ *   ising_c_example L_rows L_cols seed beta sweeps [lattice.bin]
+ *     -> line 1: "up E t sum" after `sweeps` sweeps (and the +-1 bytes, row-major, written
+ *        to lattice.bin when given)
  *        line 2: "up E" of 2 x 3 samples, one every 2 sweeps, via ising_sweep_measure_async
  * Built by __graft_entry__.build(); tests/test_gpu_capi.py runs it against the oracle. */
 #include <stdio.h>
@@ -19,8 +20,8 @@
   } while (0)
 
 int main(int argc, char** argv) {
-  if (argc != 6) {
-    fprintf(stderr, "usage: %s L_rows L_cols seed beta sweeps\n", argv[0]);
+  if (argc != 6 && argc != 7) {
+    fprintf(stderr, "usage: %s L_rows L_cols seed beta sweeps [lattice.bin]\n", argv[0]);
     return 2;
   }
   const int64_t N = atoll(argv[1]), M = atoll(argv[2]);
@@ -41,6 +42,14 @@ int main(int argc, char** argv) {
   long long sum = 0;
   for (int64_t k = 0; k < N * M; ++k) sum += lat[k];
   printf("%lld %lld %llu %lld\n", (long long)up, (long long)E, (unsigned long long)t, sum);
+  if (argc == 7) {
+    FILE* f = fopen(argv[6], "wb");
+    if (!f || fwrite(lat, 1, (size_t)(N * M), f) != (size_t)(N * M)) {
+      fprintf(stderr, "cannot write %s\n", argv[6]);
+      return 1;
+    }
+    fclose(f);
+  }
   free(lat);
   /* asynchronous measured chain: enqueue the second chunk before waiting for the first
    * (host memory here is pageable; pinned memory makes the copies truly asynchronous) */

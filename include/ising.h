@@ -113,7 +113,11 @@ int ising_ipc_connect(ising_t h, const void* blobs, size_t len);    /* world * 2
  * kernels run concurrently on one GPU, each on its own stream, and the flag protocol is
  * exercised under real concurrency (the multi-process same-GPU runs are time-sliced).
  * Sweeps, observables, init and write are collective across the n handles exactly as across
- * processes; destroy them together, after their last collective call.
+ * processes; destroy them together, after their last collective call.  Ranks that share a
+ * device run without programmatic dependent launch (waiting dependent grids would otherwise
+ * hold the SM slots a spinning neighbour waits for); with widths that are not a multiple of
+ * 8192 columns (register-rolling kernel: every block waits for the neighbours) keep such
+ * groups small enough that one rank's grid does not fill the device.
  * Errors: ARG (NULL, n outside 1..8, handles not ranks 0..n-1 of one lattice), DEVICE, CUDA. */
 int ising_p2p_connect_local(const ising_t* handles, int n);
 

@@ -8,6 +8,7 @@
 //   k_pack / k_unpack  +-1 byte full lattice <-> packed planes (row a9).
 //
 // All arithmetic is integer.  Nothing here is shared with oracle/.
+#include <algorithm>
 #include <cstdio>
 #include <type_traits>
 #include <cuda_runtime.h>
@@ -411,9 +412,61 @@ __device__ __forceinline__ uint64_t update_word<1>(uint64_t tgt, uint64_t n, uin
 #ifndef ISING_PROBE8
 #define ISING_PROBE8 1  // the probe advances eight blocks in lockstep, like the kernels (1899 -> 2005 draws/ns)
 #endif
+// Experiment (ISING_R2DECOMP): the second round's only per-thread product, M0 x c0, has
+// c0 = U ^ (c1base + b) with U warp-uniform and c1base a multiple of 8 (b = 0..7), so
+// c0 = Y + d_b with Y = c1base ^ (U & ~7) per thread and d_b = (b ^ U) & 7 warp-uniform:
+// M0 c0 = M0 Y + M0 d_b — one IMAD.WIDE and eight 64-bit adds of uniform constants instead of
+// eight IMAD.WIDE (exact: same 64-bit products).
+#ifndef ISING_R2DECOMP
+#define ISING_R2DECOMP 0
+#endif
 __device__ __forceinline__ void philox8(uint32_t t, uint32_t c1base, uint32_t colour, uint32_t row,
                                         const PhiloxKeys& K, uint4 (&out)[8]) {
   uint32_t c0[8], c1[8], c2[8], c3[8];
+#if ISING_R2DECOMP
+  {
+    const uint64_t p0u = (uint64_t)t * kPhiloxM0, p1u = (uint64_t)colour * kPhiloxM1;  // round 1
+    const uint32_t U = (uint32_t)(p1u >> 32) ^ K.k0[0];  // round-1 c0 = U ^ (c1base + b)
+    const uint32_t c1u = (uint32_t)p1u;
+    const uint32_t c2u = (uint32_t)(p0u >> 32) ^ row ^ K.k1[0];
+    const uint32_t c3u = (uint32_t)p0u;
+    const uint64_t q1 = (uint64_t)c2u * kPhiloxM1;  // round 2, uniform product
+    const uint32_t n0 = (uint32_t)(q1 >> 32) ^ c1u ^ K.k0[1];
+    const uint64_t Q = (uint64_t)(c1base ^ (U & ~7u)) * kPhiloxM0;  // round 2, per thread
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      const uint64_t C = (uint64_t)((b ^ U) & 7u) * kPhiloxM0;  // warp-uniform
+      uint64_t P;  // Q + C as two ALU adds (ptxas would re-fuse a plain add into IMAD.WIDE)
+      asm("{\n\t.reg .u32 ql, qh, cl, ch, pl, ph;\n\t"
+          "mov.b64 {ql, qh}, %1;\n\tmov.b64 {cl, ch}, %2;\n\t"
+          "add.cc.u32 pl, ql, cl;\n\taddc.u32 ph, qh, ch;\n\t"
+          "mov.b64 %0, {pl, ph};\n\t}"
+          : "=l"(P)
+          : "l"(Q), "l"(C));
+      c0[b] = n0;
+      c1[b] = (uint32_t)q1;
+      c2[b] = (uint32_t)(P >> 32) ^ c3u ^ K.k1[1];
+      c3[b] = (uint32_t)P;
+    }
+  }
+#pragma unroll
+  for (int r = 2; r < 10; ++r) {
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      const uint64_t p0 = (uint64_t)c0[b] * kPhiloxM0;
+      const uint64_t p1 = (uint64_t)c2[b] * kPhiloxM1;
+      const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1[b] ^ K.k0[r];
+      const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3[b] ^ K.k1[r];
+      c1[b] = (uint32_t)p1;
+      c3[b] = (uint32_t)p0;
+      c0[b] = n0;
+      c2[b] = n2;
+    }
+  }
+#pragma unroll
+  for (int b = 0; b < 8; ++b) out[b] = make_uint4(c0[b], c1[b], c2[b], c3[b]);
+  return;
+#endif
 #pragma unroll
   for (int b = 0; b < 8; ++b) {
     c0[b] = t;
@@ -878,6 +931,32 @@ __global__ void k_gather(const GatherParams p) {
 
 __global__ void k_set_u32(uint32_t* dst, uint32_t v, int add) { *dst = add ? *dst + v : v; }
 
+__global__ void k_zero_u64(unsigned long long* dst, int n) {
+  for (int k = threadIdx.x; k < n; k += blockDim.x) dst[k] = 0;
+}
+
+// Small zero fills as a kernel rather than cudaMemsetAsync: in one process driving several
+// rank-p2p handles on one device (ising_p2p_connect_local), a memset queued behind another
+// rank's phase that spins on this rank's flags was observed never to run (a deadlock the
+// flag timeout turned into a trap); kernels on independent streams do not have that problem.
+cudaError_t launch_zero_u64(cudaStream_t st, unsigned long long* dst, int n) {
+  k_zero_u64<<<1, 32, 0, st>>>(dst, n);
+  return cudaGetLastError();
+}
+
+__global__ void k_copy_u64(uint64_t* __restrict__ dst, const uint64_t* __restrict__ src, int64_t n) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x)
+    dst[k] = src[k];
+}
+
+// Row copies into a neighbour's halo (possibly peer memory) as a kernel, for the same reason.
+cudaError_t launch_copy_u64(cudaStream_t st, uint64_t* dst, const uint64_t* src, int64_t n) {
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, 1024);
+  k_copy_u64<<<grid, 256, 0, st>>>(dst, src, n);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_set_u32(cudaStream_t st, uint32_t* dst, uint32_t v, int add) {
   k_set_u32<<<1, 1, 0, st>>>(dst, v, add);
   return cudaGetLastError();
@@ -953,8 +1032,15 @@ __global__ void __launch_bounds__(kStageThreads, staged_minb(RULE)) k_halfsweep_
   __shared__ alignas(8) uint64_t mbar;
   const int64_t W = p.W;
   const int64_t bpr = W / kStageWords;  // blocks per band
-  const int band = (int)(blockIdx.x / bpr);
-  const int64_t w0 = (int64_t)(blockIdx.x - (int64_t)band * bpr) * kStageWords;
+  const int pband = (int)(blockIdx.x / bpr);
+  const int64_t w0 = (int64_t)(blockIdx.x - (int64_t)pband * bpr) * kStageWords;
+  // rank-p2p: the two edge bands (the only ones that wait for / signal the neighbours) take
+  // the first two slots of the grid, so their system fences and the phase signal happen while
+  // the interior bands still run instead of at the end of the kernel
+  const int64_t bands = gridDim.x / bpr;
+  const int band = (p.wait_flags && bands > 1)
+                       ? (pband == 0 ? 0 : (pband == 1 ? (int)(bands - 1) : pband - 1))
+                       : pband;
   // bands of kRows rows; with a guided tail (tail_band8 > 0) the last bands are 8 and
   // then 4 rows tall, so the partial last wave idles for a short block lifetime only
   int ra, rb;
@@ -975,7 +1061,6 @@ __global__ void __launch_bounds__(kStageThreads, staged_minb(RULE)) k_halfsweep_
   // phase; interior blocks touch this slab's own rows only (ordered by the stream)
   // the first and the last band of the slab (the only bands of a rank-p2p launch that read
   // halo rows or store into the neighbours' halo rows: it always updates rows 0 .. R - 1)
-  const int64_t bands = gridDim.x / bpr;
   const bool edge_band = band == 0 || band == bands - 1;
   if (p.wait_flags && edge_band) {
     if (threadIdx.x == 0) {
@@ -1417,6 +1502,45 @@ __global__ void k_unpack(const UnpackParams p) {
     *reinterpret_cast<uint4*>(p.full + lr * p.M + 16 * u) =
         odd_row ? lanes_to_bytes(b, a) : lanes_to_bytes(a, b);
   }
+}
+
+}  // namespace ising
+
+namespace ising {
+
+// Load every kernel the multi-slab / rank paths can launch, on the current device, before
+// any of them runs.  With CUDA's lazy module loading (the default), the first launch of a
+// kernel loads it, and loading can wait for kernels already running in the context; when
+// several ranks share one process (ising_p2p_connect_local), a rank whose half-sweep spins on
+// another rank's flags then blocks that other rank's first launch of a kernel — a deadlock
+// (observed: the flag-wait timeout fired).  cudaFuncGetAttributes forces the load.
+template <int R>
+static cudaError_t preload_rule() {
+  cudaFuncAttributes a;
+  cudaError_t e;
+  if ((e = cudaFuncGetAttributes(&a, k_halfsweep<R, false>)) != cudaSuccess) return e;
+  if ((e = cudaFuncGetAttributes(&a, k_halfsweep<R, true>)) != cudaSuccess) return e;
+  if ((e = cudaFuncGetAttributes(&a, k_halfsweep_staged<R, false>)) != cudaSuccess) return e;
+  return cudaFuncGetAttributes(&a, k_halfsweep_staged<R, true>);
+}
+
+cudaError_t preload_kernels() {
+  cudaError_t e;
+  if ((e = preload_rule<0>()) != cudaSuccess) return e;
+  if ((e = preload_rule<1>()) != cudaSuccess) return e;
+  if ((e = preload_rule<2>()) != cudaSuccess) return e;
+  if ((e = preload_rule<3>()) != cudaSuccess) return e;
+  if ((e = preload_rule<4>()) != cudaSuccess) return e;
+  if ((e = preload_rule<5>()) != cudaSuccess) return e;
+  if ((e = preload_rule<6>()) != cudaSuccess) return e;
+  if ((e = preload_rule<7>()) != cudaSuccess) return e;
+  cudaFuncAttributes a;
+  const void* others[] = {(const void*)k_sync,      (const void*)k_gather, (const void*)k_set_u32,
+                          (const void*)k_zero_u64,  (const void*)k_copy_u64, (const void*)k_init,
+                          (const void*)k_observables, (const void*)k_pack,  (const void*)k_unpack};
+  for (const void* f : others)
+    if ((e = cudaFuncGetAttributes(&a, f)) != cudaSuccess) return e;
+  return cudaSuccess;
 }
 
 }  // namespace ising

@@ -190,6 +190,9 @@ cudaError_t staged_occupancy(int* blocks_per_sm);
 cudaError_t launch_persistent(int rule, int grid, cudaStream_t st, const PersistentParams& P);
 cudaError_t persistent_occupancy(int* blocks_per_sm);
 cudaError_t launch_set_u32(cudaStream_t st, uint32_t* dst, uint32_t v, int add);
+cudaError_t launch_zero_u64(cudaStream_t st, unsigned long long* dst, int n);
+cudaError_t preload_kernels();  // force-load every kernel of the slab / rank paths (lazy loading)
+cudaError_t launch_copy_u64(cudaStream_t st, uint64_t* dst, const uint64_t* src, int64_t n);
 cudaError_t launch_gather(cudaStream_t st, const GatherParams& p);
 cudaError_t launch_halfsweep(int rule, int grid, cudaStream_t st, const HalfSweepParams& p);
 cudaError_t halfsweep_occupancy(int* blocks_per_sm);

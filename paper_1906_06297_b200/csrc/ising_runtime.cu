@@ -32,6 +32,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -335,6 +336,16 @@ int setup_device(Device& d, int dev) {
   if (d.hs_blocks_per_sm < 1) d.hs_blocks_per_sm = 1;
   CU(staged_occupancy(&d.staged_blocks_per_sm));
   if (d.staged_blocks_per_sm < 1) d.staged_blocks_per_sm = 1;
+  {  // once per device and process (see preload_kernels)
+    static std::mutex mu;
+    static std::vector<bool> loaded;
+    std::lock_guard<std::mutex> lock(mu);
+    if ((int)loaded.size() <= dev) loaded.resize(dev + 1, false);
+    if (!loaded[dev]) {
+      CU(preload_kernels());
+      loaded[dev] = true;
+    }
+  }
   return ISING_OK;
 }
 
@@ -712,12 +723,11 @@ int exchange_halos(ising_ctx* h) {
   Device& d = h->devs[0];
   const size_t W = (size_t)h->W;
   const int R = (int)s.R;
-  if (h->p2p) {
+  if (h->p2p) {  // peer stores by a kernel (see launch_copy_u64)
     for (int c = 0; c < 2; ++c) {
-      CU(cudaMemcpyAsync(h->up_plane[c] + (size_t)(R + 1) * W, s.plane[c] + W, W * 8,
-                         cudaMemcpyDeviceToDevice, d.stream));
-      CU(cudaMemcpyAsync(h->dn_plane[c], s.plane[c] + (size_t)R * W, W * 8,
-                         cudaMemcpyDeviceToDevice, d.stream));
+      CU(launch_copy_u64(d.stream, h->up_plane[c] + (size_t)(R + 1) * W, s.plane[c] + W, (int64_t)W));
+      CU(launch_copy_u64(d.stream, h->dn_plane[c], s.plane[c] + (size_t)R * W, (int64_t)W));
+      h->launch_count += 2;
     }
     return ISING_OK;
   }
@@ -1463,6 +1473,16 @@ int ising_p2p_connect_local(const ising_t* handles, int n) {
     }
   }
   if (n == 1) return ISING_OK;  // connected at creation
+  // Ranks sharing a device: no programmatic dependent launch.  A PDL-launched half-sweep's
+  // blocks become resident as soon as the previous one's have started and then wait for it
+  // to finish; while that one spins on another rank's flags, the waiting grids of several
+  // ranks can hold every SM slot, so the awaited rank's phase never gets resident (observed:
+  // 4 ranks of 8192 x 32768 on one B200 deadlocked).  Ranks on separate GPUs keep PDL.
+  bool shared = false;
+  for (int r = 0; r < n; ++r)
+    for (int q = 0; q < r; ++q) shared |= handles[r]->devs[0].dev == handles[q]->devs[0].dev;
+  if (shared)
+    for (int r = 0; r < n; ++r) handles[r]->pdl = false;
   for (int r = 0; r < n; ++r) {
     ising_t h = handles[r];
     if (h->connected) continue;
@@ -1580,7 +1600,8 @@ int ising_write_lattice(ising_t h, const int8_t* in, int64_t in_len, uint64_t t)
     Device& d = h->devs[s.devi];
     CU(cudaSetDevice(d.dev));
     TRY(ensure_staging(d, h->M));
-    CU(cudaMemsetAsync(d.red, 0, 4 * sizeof(unsigned long long), d.stream));
+    CU(launch_zero_u64(d.stream, d.red, 4));  // a kernel, not a memset (see launch_zero_u64)
+    ++h->launch_count;
     const int64_t rpc = staging_rows(d, h->M);
     const int64_t r_lo = slab_only ? 0 : -1, r_hi = slab_only ? s.R : s.R + 1;
     const int64_t nchunks = (r_hi - r_lo + rpc - 1) / rpc;
@@ -1744,7 +1765,8 @@ int ising_observables(ising_t h, int64_t* up_count, int64_t* bond_energy) {
   std::vector<unsigned long long*> outs;
   for (auto& d : h->devs) {
     CU(cudaSetDevice(d.dev));
-    CU(cudaMemsetAsync(d.red, 0, 2 * sizeof(unsigned long long), d.stream));
+    CU(launch_zero_u64(d.stream, d.red, 2));  // a kernel, not a memset (see launch_zero_u64)
+    ++h->launch_count;
     outs.push_back(d.red);
   }
   TRY(enqueue_observables(h, outs));
@@ -1854,7 +1876,7 @@ int ising_sweep_measure(ising_t h, int64_t n_samples, int64_t every, int64_t* up
     double total = 0;
     std::vector<unsigned long long*> red{d.red};
     for (int64_t k = 0; k < n_samples; ++k) {
-      CU(cudaMemsetAsync(d.red, 0, 2 * sizeof(unsigned long long), d.stream));
+      // (no memset: the black phase of the sample's last sweep zeroes d.red, obs_clear)
       CU(cudaEventRecord(d.ev_t0, d.stream));
       TRY(enqueue_sweeps(h, every, &red));
       CU(cudaEventRecord(d.ev_t1, d.stream));

@@ -135,3 +135,79 @@ def test_nccl_id_rendezvous_over_gloo():
     from paper_1906_06297_b200 import ising
 
     assert all(s in (ising.ISING_ERR_CUDA, ising.ISING_ERR_DEVICE) for s in stats), stats
+
+
+def _agree_worker(rank, world, port, fail_rank, fail_at, q):
+    """IsingLattice.distributed's transport agreement with the ABI calls replaced by fakes
+    (no GPU here): rank `fail_rank` fails at `fail_at` ("create", "handle" or "connect"); every
+    rank must make the same collective calls and all must fall back to NCCL together."""
+    import sys
+
+    sys.path.insert(0, ROOT)
+    from paper_1906_06297_b200 import ising
+
+    calls = []
+
+    def fail(name):
+        if rank == fail_rank and fail_at == name:
+            raise ising.IsingError.__new__(ising.IsingError)
+
+    def create_p2p(*a):
+        calls.append("create_p2p")
+        fail("create")
+        return 1000 + rank
+
+    def ipc_handle(h):
+        calls.append("ipc_handle")
+        fail("handle")
+        return bytes([rank]) * ising.IPC_BLOB_BYTES
+
+    def ipc_connect(h, blobs):
+        calls.append("ipc_connect")
+        assert len(blobs) == world * ising.IPC_BLOB_BYTES
+        fail("connect")
+
+    ising.ising_create_rank_p2p = create_p2p
+    ising.ising_ipc_handle = ipc_handle
+    ising.ising_ipc_connect = ipc_connect
+    ising.ising_destroy = lambda h: calls.append("destroy")
+    ising.ising_nccl_unique_id = lambda: b"\x07" * ising.NCCL_ID_BYTES
+    ising.ising_create_rank = lambda *a: calls.append(("create_rank", a[-1])) or 2000 + rank
+    ising.IsingError.__init__ = lambda self, *a: None
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        lat = ising.IsingLattice.distributed(64, 64, 1, device=0)
+        q.put((rank, lat.transport, lat.h, calls))
+        lat.h = None  # a fake handle: nothing to destroy
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("fail_rank,fail_at", [(None, None), (1, "create"), (0, "handle"),
+                                               (1, "connect")])
+def test_distributed_transport_agreement(fail_rank, fail_at):
+    """when CUDA IPC setup fails on one rank only, every rank still makes the same
+    collective calls (no mismatched all_gather, no hang) and all ranks fall back to the NCCL
+    transport together; with no failure all use rank-p2p."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_agree_worker, args=(r, world, port, fail_rank, fail_at, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict((r, rest) for r, *rest in (q.get(timeout=120) for _ in range(world)))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = "p2p" if fail_rank is None else "nccl"
+    assert all(res[r][0] == want for r in range(world)), res
+    if want == "nccl":
+        for r in range(world):
+            calls = res[r][2]
+            assert calls.count(("create_rank", b"\x07" * 128)) == 1, calls  # the broadcast id
+            # a rank whose p2p handle was created destroys it before falling back
+            if "create_p2p" in calls and not (r == fail_rank and fail_at == "create"):
+                assert "destroy" in calls, calls
