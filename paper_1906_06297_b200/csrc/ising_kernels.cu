@@ -523,6 +523,37 @@ __device__ __forceinline__ uint32_t sel1_half(uint32_t t, uint32_t n, uint32_t c
   return t ^ ((x >> 3) & kLane0);
 }
 
+// NB Philox blocks (counter word 1 = c1base + b) advanced in lockstep: philox8's form for
+// the four blocks of one word.
+template <int NB>
+__device__ __forceinline__ void philox_n(uint32_t t, uint32_t c1base, uint32_t colour, uint32_t row,
+                                         const PhiloxKeys& K, uint4 (&out)[NB]) {
+  uint32_t c0[NB], c1[NB], c2[NB], c3[NB];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    c0[b] = t;
+    c1[b] = c1base + b;
+    c2[b] = colour;
+    c3[b] = row;
+  }
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const uint64_t p0 = (uint64_t)c0[b] * kPhiloxM0;
+      const uint64_t p1 = (uint64_t)c2[b] * kPhiloxM1;
+      const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1[b] ^ K.k0[r];
+      const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3[b] ^ K.k1[r];
+      c1[b] = (uint32_t)p1;
+      c3[b] = (uint32_t)p0;
+      c0[b] = n0;
+      c2[b] = n2;
+    }
+  }
+#pragma unroll
+  for (int b = 0; b < NB; ++b) out[b] = make_uint4(c0[b], c1[b], c2[b], c3[b]);
+}
+
 // Metropolis (RULE 0) acceptance of one word from its four precomputed blocks rb[0..3]
 // (block q serves lanes 4q .. 4q + 3), same Horner order as update_word_metropolis.
 template <int RULE>
@@ -995,6 +1026,9 @@ constexpr int kRowUnroll = ISING_ROW_UNROLL;  // staged row loop unroll factor
 #ifndef ISING_STAGED_MINB
 #define ISING_STAGED_MINB 3
 #endif
+#ifndef ISING_PIPE
+#define ISING_PIPE 0
+#endif
 #ifndef ISING_STAGED_MINB_DRAWFREE
 #define ISING_STAGED_MINB_DRAWFREE 4
 #endif
@@ -1118,6 +1152,48 @@ __global__ void __launch_bounds__(kStageThreads, staged_minb(RULE)) k_halfsweep_
   const int64_t wc = w0 + 2 * tid;
   uint32_t obs_up = 0, obs_anti = 0;
   uint64_t* tp = tgt + (int64_t)ra * W + wc;  // target chunk of row r, advanced by W per row
+#if ISING_PIPE
+  // Experiment: software-pipelined draws.  The four blocks of a row's second word are drawn
+  // while its first word is accepted, and the next row's first word while the second is
+  // accepted, so the Philox multiplies (FMA-heavy pipe) and the acceptance (ALU) of one warp
+  // interleave instead of alternating.
+  if constexpr (lockstep_rule(RULE)) {
+    uint4 d0[4];
+    philox_n<4>(t, (uint32_t)(4 * wc), p.colour, (uint32_t)(p.row0 + ra), p.keys, d0);
+    for (int rr = 0; rr < nrows; ++rr, tp += W) {
+      const int r = ra + rr;
+      const int64_t gi = p.row0 + r;
+      const bool west = ((gi & 1) == 0) == (p.colour == 0);
+      const uint64_t n0 = tile[rr][2 * tid], n1 = tile[rr][2 * tid + 1];
+      const uint64_t c0 = tile[rr + 1][2 * tid], c1 = tile[rr + 1][2 * tid + 1];
+      const uint64_t s0 = tile[rr + 2][2 * tid], s1 = tile[rr + 2][2 * tid + 1];
+      uint64_t side0, side1;
+      if (west) {
+        const uint64_t wl = tid == 0 ? edge[rr + 1][0] : tile[rr + 1][2 * tid - 1];
+        side0 = splice_west(c0, wl);
+        side1 = splice_west(c1, c0);
+      } else {
+        const uint64_t er = tid == kStageThreads - 1 ? edge[rr + 1][1] : tile[rr + 1][2 * tid + 2];
+        side0 = splice_east(c0, c1);
+        side1 = splice_east(c1, er);
+      }
+      ulonglong2 tv = __ldcg(reinterpret_cast<const ulonglong2*>(tp));
+      const uint32_t ctr0 = (uint32_t)(4 * wc);
+      uint4 d1[4];
+      philox_n<4>(t, ctr0 + 4, p.colour, (uint32_t)gi, p.keys, d1);
+      tv.x = word_from_draws<RULE>(tv.x, n0, c0, s0, side0, d0, p);
+      philox_n<4>(t, ctr0, p.colour, (uint32_t)(gi + 1), p.keys, d0);  // next row (last: unused)
+      tv.y = word_from_draws<RULE>(tv.y, n1, c1, s1, side1, d1, p);
+      *reinterpret_cast<ulonglong2*>(tp) = tv;
+      if (r == 0 && p.halo_up) *reinterpret_cast<ulonglong2*>(p.halo_up + wc) = tv;
+      if (r == p.R - 1 && p.halo_dn) *reinterpret_cast<ulonglong2*>(p.halo_dn + wc) = tv;
+      if (OBS) {
+        obs_word(tv.x, n0, c0, s0, side0, obs_up, obs_anti);
+        obs_word(tv.y, n1, c1, s1, side1, obs_up, obs_anti);
+      }
+    }
+  } else
+#endif
 #pragma unroll kRowUnroll
   for (int rr = 0; rr < nrows; ++rr, tp += W) {
     const int r = ra + rr;
