@@ -430,19 +430,27 @@ def link_bandwidth(dev: int) -> dict:
     return best
 
 
-def e2e_run(lat, N: int, M: int, rows: int, n: int, steps: int, R: Ranks) -> float:
+def e2e_run(lat, N: int, M: int, rows: int, n: int, steps: int, R: Ranks, bits: bool = False) -> float:
     """Wall seconds (max over ranks) of: write_lattice(own rows from pinned host memory);
-    `steps` x ising_sweep_measure_async(1, 1) with the host one step behind; read_lattice."""
+    `steps` x ising_sweep_measure_async(1, 1) with the host one step behind; read_lattice.
+    bits: the same through the bit-packed calls (one bit per spin on the host)."""
     import torch
 
-    slab = torch.empty((rows, M), dtype=torch.int8, pin_memory=True)
-    lat.read_lattice(slab.numpy() if n > 1 else slab.numpy().reshape(N, M))
-    out = torch.empty((rows, M), dtype=torch.int8, pin_memory=True)
+    if bits:
+        slab = torch.empty(rows * M // 8, dtype=torch.uint8, pin_memory=True)
+        out = torch.empty(rows * M // 8, dtype=torch.uint8, pin_memory=True)
+        lat.read_lattice_bits(slab.numpy())
+        write, read = lat.write_lattice_bits, lat.read_lattice_bits
+    else:
+        slab = torch.empty((rows, M), dtype=torch.int8, pin_memory=True)
+        out = torch.empty((rows, M), dtype=torch.int8, pin_memory=True)
+        lat.read_lattice(slab.numpy() if n > 1 else slab.numpy().reshape(N, M))
+        write, read = lat.write_lattice, lat.read_lattice
     ups = torch.zeros(steps, dtype=torch.int64, pin_memory=True).numpy()
     Es = torch.zeros(steps, dtype=torch.int64, pin_memory=True).numpy()
     R.barrier()
     t0 = time.perf_counter()
-    lat.write_lattice(slab.numpy(), t=0)
+    write(slab.numpy(), t=0)
     prev = None
     for k in range(steps):
         ticket = lat.measure_async(1, 1, ups[k:k + 1], Es[k:k + 1])
@@ -450,7 +458,7 @@ def e2e_run(lat, N: int, M: int, rows: int, n: int, steps: int, R: Ranks) -> flo
             lat.measure_wait(prev)
         prev = ticket
     lat.measure_wait(prev)
-    lat.read_lattice(out.numpy())
+    read(out.numpy())
     R.barrier()
     return R.allmax(time.perf_counter() - t0)
 
@@ -573,7 +581,12 @@ def run_ours(args):
         e2e_s = e2e_run(lat, N, M, rows, n, args.steps, R)
         link = link_bandwidth(dev)
         copy_s = rows * M / (link["h2d_gbs"] * 1e9) + rows * M / (link["d2h_gbs"] * 1e9)
-        roof = N * M * args.steps / ((copy_s + args.steps * ms / args.steps * 1e-3) * 1e9)
+        roof = N * M * args.steps / ((copy_s + ms * 1e-3) * 1e9)
+        # the same through the bit-packed host format (1 bit per spin: 1/8 of the copy bytes)
+        bits_s = None
+        if not basic:
+            e2e_run(lat, N, M, rows, n, min(args.steps, 2), R, bits=True)
+            bits_s = e2e_run(lat, N, M, rows, n, args.steps, R, bits=True)
         e2e = {
             "value": N * M * args.steps / (e2e_s * 1e9),
             "unit": "flips/ns",
@@ -590,6 +603,13 @@ def run_ours(args):
                    "rank mode, 16 B copied to pinned host memory per step, the host waiting one "
                    "step behind); read_lattice(own rows, pinned int8); wall clock, max over "
                    "ranks; bytes summed over ranks; after one untimed warm-up pass",
+            "bitpacked": None if bits_s is None else {
+                "value": N * M * args.steps / (bits_s * 1e9),
+                "h2d_bytes_per_step": N * M // 8 // args.steps,
+                "d2h_bytes_per_step": N * M // 8 // args.steps + 16 * n,
+                "roof": N * M * args.steps / ((copy_s / 8 + ms * 1e-3) * 1e9),
+                "how": "the same calls with ising_write_lattice_bits / ising_read_lattice_bits "
+                       "(host lattice one bit per spin, pinned)"},
         }
     lat.close()
 

@@ -162,6 +162,17 @@ int ising_init_cold(ising_t h);
  * Collective in rank mode. */
 int ising_write_lattice(ising_t h, const int8_t* in, int64_t in_len, uint64_t t);
 
+/* The same two calls in the bit-packed host format: spin (i, J) is bit (J & 7) of byte
+ * (i*L_cols + J) / 8, 1 for +1 (row-major, least significant bit first: numpy's
+ * packbits(..., bitorder="little") of the +1 mask).  L_cols / 8 bytes per row, 8x less host
+ * memory and PCIe traffic than the +-1 bytes (checkpoints of the 2^40-spin lattice: 128 GiB
+ * instead of 1 TiB).  in_len / out_len >= L_rows*L_cols/8 (else RANGE); rank mode (world > 1)
+ * also takes exactly this rank's R*L_cols/8 bytes, as for the byte format.  Every bit pattern
+ * is a valid lattice.  Multi-spin handles only (ARG for ising_create_basic handles).
+ * ising_write_lattice_bits is collective in rank mode. */
+int ising_write_lattice_bits(ising_t h, const uint8_t* in, int64_t in_len, uint64_t t);
+int ising_read_lattice_bits(ising_t h, uint8_t* out, int64_t out_len);
+
 /* Run n >= 0 full sweeps (black then white), t += n.  STATE if set_beta or an
  * init/write has not happened; RANGE if t + n > 2^32 - 1.  Returns after
  * completion.  Collective in rank mode. */

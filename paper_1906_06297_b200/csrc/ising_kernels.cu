@@ -1580,6 +1580,68 @@ __global__ void k_unpack(const UnpackParams p) {
   }
 }
 
+// ------------------------------------------------------ bit-packed host format
+// 32 full columns J0 .. J0 + 31 (J0 = 32 w) of row i are plane columns 16 w .. 16 w + 15 of
+// both colours — exactly word w of each plane row; even columns have colour i & 1 (R1).
+// part1by1 moves bit p to bit 2p, compact1by1 is its inverse: the even-column bits (at 2k)
+// land on nibble lane k (bit 4k) and back.
+__device__ __forceinline__ uint64_t part1by1(uint64_t x) {
+  x &= 0x00000000FFFFFFFFull;
+  x = (x | (x << 16)) & 0x0000FFFF0000FFFFull;
+  x = (x | (x << 8)) & 0x00FF00FF00FF00FFull;
+  x = (x | (x << 4)) & 0x0F0F0F0F0F0F0F0Full;
+  x = (x | (x << 2)) & 0x3333333333333333ull;
+  x = (x | (x << 1)) & 0x5555555555555555ull;
+  return x;
+}
+__device__ __forceinline__ uint64_t compact1by1(uint64_t x) {
+  x &= 0x5555555555555555ull;
+  x = (x | (x >> 1)) & 0x3333333333333333ull;
+  x = (x | (x >> 2)) & 0x0F0F0F0F0F0F0F0Full;
+  x = (x | (x >> 4)) & 0x00FF00FF00FF00FFull;
+  x = (x | (x >> 8)) & 0x0000FFFF0000FFFFull;
+  x = (x | (x >> 16)) & 0x00000000FFFFFFFFull;
+  return x;
+}
+
+__global__ void k_pack_bits(const PackBitsParams p) {
+  const int64_t total = (int64_t)(p.rb - p.ra) * p.W;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t lr = idx / p.W, w = idx - lr * p.W;
+    const int64_t r = p.ra + lr;  // padded local row (-1 .. R)
+    int64_t gi = (p.row0 + r) % p.N;
+    if (gi < 0) gi += p.N;
+    const uint64_t x = p.bits[idx];
+    const uint64_t even = part1by1(x & 0x55555555u), odd = part1by1((x >> 1) & 0x55555555u);
+    const int ce = (int)(gi & 1);  // colour of the even columns
+    p.plane[ce][(r + 1) * p.W + w] = even;
+    p.plane[1 - ce][(r + 1) * p.W + w] = odd;
+  }
+}
+
+__global__ void k_unpack_bits(const UnpackBitsParams p) {
+  const int64_t total = (int64_t)(p.rb - p.ra) * p.W;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t lr = idx / p.W, w = idx - lr * p.W;
+    const int64_t r = p.ra + lr;
+    const int ce = (int)((p.row0 + r) & 1);
+    const uint64_t even = p.plane[ce][(r + 1) * p.W + w] & 0x1111111111111111ull;
+    const uint64_t odd = p.plane[1 - ce][(r + 1) * p.W + w] & 0x1111111111111111ull;
+    p.bits[idx] = (uint32_t)(compact1by1(even) | (compact1by1(odd) << 1));
+  }
+}
+
+cudaError_t launch_pack_bits(int grid, cudaStream_t st, const PackBitsParams& p) {
+  k_pack_bits<<<grid, 256, 0, st>>>(p);
+  return cudaGetLastError();
+}
+cudaError_t launch_unpack_bits(int grid, cudaStream_t st, const UnpackBitsParams& p) {
+  k_unpack_bits<<<grid, 256, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
 }  // namespace ising
 
 namespace ising {
@@ -1613,7 +1675,8 @@ cudaError_t preload_kernels() {
   cudaFuncAttributes a;
   const void* others[] = {(const void*)k_sync,      (const void*)k_gather, (const void*)k_set_u32,
                           (const void*)k_zero_u64,  (const void*)k_copy_u64, (const void*)k_init,
-                          (const void*)k_observables, (const void*)k_pack,  (const void*)k_unpack};
+                          (const void*)k_observables, (const void*)k_pack,  (const void*)k_unpack,
+                          (const void*)k_pack_bits, (const void*)k_unpack_bits};
   for (const void* f : others)
     if ((e = cudaFuncGetAttributes(&a, f)) != cudaSuccess) return e;
   return cudaSuccess;

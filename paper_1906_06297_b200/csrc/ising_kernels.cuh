@@ -150,6 +150,29 @@ struct PackParams {
   unsigned int* bad;      // set to 1 if a value is not -1/+1
 };
 
+// Bit-packed host format (ising_write_lattice_bits / ising_read_lattice_bits): bit (J & 7) of
+// byte (i L_cols + J) / 8 is 1 for spin +1; staging rows of L_cols / 8 bytes.  One thread per
+// 32 full columns = one 64-bit word of each colour plane.
+struct PackBitsParams {
+  uint64_t* plane[2];
+  const uint32_t* bits;   // staging: rows [ra, rb) of the padded row range, W 32-bit words each
+  int64_t W;
+  int64_t row0;
+  int64_t N;
+  int32_t ra;             // first padded local row in staging (may be -1)
+  int32_t rb;
+};
+struct UnpackBitsParams {
+  const uint64_t* plane[2];
+  uint32_t* bits;         // staging: rows [ra, rb) of the slab (interior rows only)
+  int64_t W;
+  int64_t row0;
+  int32_t ra;
+  int32_t rb;
+};
+cudaError_t launch_pack_bits(int grid, cudaStream_t st, const PackBitsParams& p);
+cudaError_t launch_unpack_bits(int grid, cudaStream_t st, const UnpackBitsParams& p);
+
 struct UnpackParams {
   const uint64_t* plane[2];
   int8_t* full;           // staging: rows [ra, rb) of the slab (interior rows only)

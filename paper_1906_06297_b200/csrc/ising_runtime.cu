@@ -957,13 +957,14 @@ int run_init(ising_ctx* h, int cold) {
 }
 
 // Copy global rows [g, g + n) (wrapping mod N) of the host lattice to dst.
-int h2d_rows(ising_ctx* h, int8_t* dst, const int8_t* in, int64_t g, int64_t n, cudaStream_t st) {
+int h2d_rows(ising_ctx* h, int8_t* dst, const int8_t* in, int64_t g, int64_t n, cudaStream_t st,
+             int64_t row_bytes) {
   g %= h->N;
   if (g < 0) g += h->N;
   while (n > 0) {
     const int64_t run = std::min(n, h->N - g);
-    CU(cudaMemcpyAsync(dst, in + g * h->M, (size_t)(run * h->M), cudaMemcpyHostToDevice, st));
-    dst += run * h->M;
+    CU(cudaMemcpyAsync(dst, in + g * row_bytes, (size_t)(run * row_bytes), cudaMemcpyHostToDevice, st));
+    dst += run * row_bytes;
     n -= run;
     g = 0;
   }
@@ -1085,11 +1086,13 @@ int enqueue_observables(ising_ctx* h, const std::vector<unsigned long long*>& ou
 
 // Unpack local rows [la, lb) of slab s into host rows at dst (row-major, M bytes each):
 // unpack of chunk k + 1 overlaps the D2H copy of chunk k (pipeline_out).
-int unpack_rows_to_host(ising_ctx* h, Slab& s, int64_t la, int64_t lb, int8_t* dst) {
+int unpack_rows_to_host(ising_ctx* h, Slab& s, int64_t la, int64_t lb, int8_t* dst,
+                        bool bits = false) {
   Device& d = h->devs[s.devi];
   CU(cudaSetDevice(d.dev));
-  TRY(ensure_staging(d, h->M));
-  const int64_t rpc = staging_rows(d, h->M);
+  const int64_t row_bytes = bits ? h->M / 8 : h->M;
+  TRY(ensure_staging(d, row_bytes));
+  const int64_t rpc = staging_rows(d, row_bytes);
   auto span = [&](int64_t k, int64_t* ra, int64_t* rb) {
     *ra = la + k * rpc;
     *rb = std::min<int64_t>(*ra + rpc, lb);
@@ -1097,6 +1100,20 @@ int unpack_rows_to_host(ising_ctx* h, Slab& s, int64_t la, int64_t lb, int8_t* d
   auto kern = [&](int64_t k, int8_t* buf, cudaStream_t st) -> int {
     int64_t ra, rb;
     span(k, &ra, &rb);
+    if (bits) {
+      UnpackBitsParams p;
+      p.plane[0] = s.plane[0];
+      p.plane[1] = s.plane[1];
+      p.bits = reinterpret_cast<uint32_t*>(buf);
+      p.W = h->W;
+      p.row0 = s.row0;
+      p.ra = (int32_t)ra;
+      p.rb = (int32_t)rb;
+      const int64_t total = (rb - ra) * h->W;
+      CU(launch_unpack_bits((int)std::min<int64_t>((total + 255) / 256, (int64_t)d.sms * 64), st, p));
+      ++h->launch_count;
+      return ISING_OK;
+    }
     UnpackParams p;
     p.plane[0] = s.plane[0];
     p.plane[1] = s.plane[1];
@@ -1116,7 +1133,7 @@ int unpack_rows_to_host(ising_ctx* h, Slab& s, int64_t la, int64_t lb, int8_t* d
   auto copy = [&](int64_t k, int8_t* buf, cudaStream_t st) -> int {
     int64_t ra, rb;
     span(k, &ra, &rb);
-    CU(cudaMemcpyAsync(dst + (ra - la) * h->M, buf, (size_t)((rb - ra) * h->M),
+    CU(cudaMemcpyAsync(dst + (ra - la) * row_bytes, buf, (size_t)((rb - ra) * row_bytes),
                        cudaMemcpyDeviceToHost, st));
     return ISING_OK;
   };
@@ -1574,20 +1591,27 @@ int ising_init_cold(ising_t h) {
   return h->basic ? basic_init(h, 1) : run_init(h, 1);
 }
 
-int ising_write_lattice(ising_t h, const int8_t* in, int64_t in_len, uint64_t t) {
+// Load the lattice from host memory: +-1 bytes (row_bytes = M) or the bit-packed format
+// (bits: row_bytes = M / 8).  Rank mode takes either the full lattice (its rows and halo rows
+// are packed straight from it) or exactly its own R rows (then the halo rows are exchanged on
+// device).
+static int write_impl(ising_t h, const int8_t* in, int64_t in_len, uint64_t t, bool bits) {
   if (!h || !in) return ISING_ERR_ARG;
   if (t > 0xffffffffull) return ISING_ERR_RANGE;
-  // Rank mode takes either the full lattice (its rows and halo rows are packed straight
-  // from it) or exactly its own R x M rows (then the halo rows are exchanged on device).
   if (h->basic) {
+    if (bits) {
+      g_last_error = "bit-packed lattice I/O is for the multi-spin layout";
+      return ISING_ERR_ARG;
+    }
     if (in_len < h->N * h->M) return ISING_ERR_RANGE;
     TRY(basic_convert(h, const_cast<int8_t*>(in), false));
     h->t = t;
     h->state_set = true;
     return ISING_OK;
   }
-  const bool slab_only = h->rank_mode && h->world > 1 && in_len == h->slabs[0].R * h->M;
-  if (!slab_only && in_len < h->N * h->M) return ISING_ERR_RANGE;
+  const int64_t row_bytes = bits ? h->M / 8 : h->M;
+  const bool slab_only = h->rank_mode && h->world > 1 && in_len == h->slabs[0].R * row_bytes;
+  if (!slab_only && in_len < h->N * row_bytes) return ISING_ERR_RANGE;
   if (h->p2p && h->world > 1 && !h->connected) return ISING_ERR_STATE;
   if (p2p_flags(h)) {
     // wait (by polling the stream, not inside a copy) until the neighbours are done with
@@ -1599,10 +1623,10 @@ int ising_write_lattice(ising_t h, const int8_t* in, int64_t in_len, uint64_t t)
   for (auto& s : h->slabs) {
     Device& d = h->devs[s.devi];
     CU(cudaSetDevice(d.dev));
-    TRY(ensure_staging(d, h->M));
+    TRY(ensure_staging(d, row_bytes));
     CU(launch_zero_u64(d.stream, d.red, 4));  // a kernel, not a memset (see launch_zero_u64)
     ++h->launch_count;
-    const int64_t rpc = staging_rows(d, h->M);
+    const int64_t rpc = staging_rows(d, row_bytes);
     const int64_t r_lo = slab_only ? 0 : -1, r_hi = slab_only ? s.R : s.R + 1;
     const int64_t nchunks = (r_hi - r_lo + rpc - 1) / rpc;
     auto span = [&](int64_t k, int64_t* ra, int64_t* rb) {
@@ -1614,15 +1638,30 @@ int ising_write_lattice(ising_t h, const int8_t* in, int64_t in_len, uint64_t t)
       int64_t ra, rb;
       span(k, &ra, &rb);
       if (slab_only)
-        CU(cudaMemcpyAsync(buf, in + ra * h->M, (size_t)((rb - ra) * h->M),
+        CU(cudaMemcpyAsync(buf, in + ra * row_bytes, (size_t)((rb - ra) * row_bytes),
                            cudaMemcpyHostToDevice, st));
       else
-        TRY(h2d_rows(h, buf, in, s.row0 + ra, rb - ra, st));
+        TRY(h2d_rows(h, buf, in, s.row0 + ra, rb - ra, st, row_bytes));
       return ISING_OK;
     };
     auto kern = [&](int64_t k, int8_t* buf, cudaStream_t st) -> int {
       int64_t ra, rb;
       span(k, &ra, &rb);
+      if (bits) {  // every bit pattern is a valid lattice: nothing to validate
+        PackBitsParams p;
+        p.plane[0] = s.plane[0];
+        p.plane[1] = s.plane[1];
+        p.bits = reinterpret_cast<const uint32_t*>(buf);
+        p.W = h->W;
+        p.row0 = s.row0;
+        p.N = h->N;
+        p.ra = (int32_t)ra;
+        p.rb = (int32_t)rb;
+        const int64_t total = (rb - ra) * h->W;
+        CU(launch_pack_bits((int)std::min<int64_t>((total + 255) / 256, (int64_t)d.sms * 64), st, p));
+        ++h->launch_count;
+        return ISING_OK;
+      }
       PackParams p;
       p.plane[0] = s.plane[0];
       p.plane[1] = s.plane[1];
@@ -1659,6 +1698,14 @@ int ising_write_lattice(ising_t h, const int8_t* in, int64_t in_len, uint64_t t)
   h->t = t;
   h->state_set = true;
   return ISING_OK;
+}
+
+int ising_write_lattice(ising_t h, const int8_t* in, int64_t in_len, uint64_t t) {
+  return write_impl(h, in, in_len, t, false);
+}
+
+int ising_write_lattice_bits(ising_t h, const uint8_t* in, int64_t in_len, uint64_t t) {
+  return write_impl(h, reinterpret_cast<const int8_t*>(in), in_len, t, true);
 }
 
 int ising_sweep(ising_t h, int64_t n) {
@@ -1701,19 +1748,32 @@ int ising_sweep(ising_t h, int64_t n) {
   return ISING_OK;
 }
 
-int ising_read_lattice(ising_t h, int8_t* out, int64_t out_len) {
+static int read_impl(ising_t h, int8_t* out, int64_t out_len, bool bits) {
   if (!h || !out) return ISING_ERR_ARG;
-  // rank mode: a buffer of exactly R x M receives this rank's rows at offset 0
-  const bool slab_only = h->rank_mode && h->world > 1 && out_len == h->slabs[0].R * h->M;
-  if (!slab_only && out_len < h->N * h->M) return ISING_ERR_RANGE;
+  if (bits && h->basic) {
+    g_last_error = "bit-packed lattice I/O is for the multi-spin layout";
+    return ISING_ERR_ARG;
+  }
+  const int64_t row_bytes = bits ? h->M / 8 : h->M;
+  // rank mode: a buffer of exactly R rows receives this rank's rows at offset 0
+  const bool slab_only = h->rank_mode && h->world > 1 && out_len == h->slabs[0].R * row_bytes;
+  if (!slab_only && out_len < h->N * row_bytes) return ISING_ERR_RANGE;
   if (!h->state_set) return ISING_ERR_STATE;
   if (h->basic) return basic_convert(h, out, true);
   for (auto& s : h->slabs) {
     // local rows [0, R) of this slab -> host rows starting at its global row (or at 0)
-    TRY(unpack_rows_to_host(h, s, 0, s.R, out + (slab_only ? 0 : s.row0) * h->M));
+    TRY(unpack_rows_to_host(h, s, 0, s.R, out + (slab_only ? 0 : s.row0) * row_bytes, bits));
   }
   TRY(sync_all(h));
   return ISING_OK;
+}
+
+int ising_read_lattice(ising_t h, int8_t* out, int64_t out_len) {
+  return read_impl(h, out, out_len, false);
+}
+
+int ising_read_lattice_bits(ising_t h, uint8_t* out, int64_t out_len) {
+  return read_impl(h, reinterpret_cast<int8_t*>(out), out_len, true);
 }
 
 int ising_read_rows(ising_t h, int64_t row_begin, int64_t nrows, int8_t* out, int64_t out_len) {

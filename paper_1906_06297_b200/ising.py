@@ -48,6 +48,8 @@ SIGNATURES = {
     "ising_init_random": (_INT, [_VP]),
     "ising_init_cold": (_INT, [_VP]),
     "ising_write_lattice": (_INT, [_VP, _VP, _I64, _U64]),
+    "ising_write_lattice_bits": (_INT, [_VP, _VP, _I64, _U64]),
+    "ising_read_lattice_bits": (_INT, [_VP, _VP, _I64]),
     "ising_sweep": (_INT, [_VP, _I64]),
     "ising_read_lattice": (_INT, [_VP, _VP, _I64]),
     "ising_observables": (_INT, [_VP, _I64P, _I64P]),
@@ -103,11 +105,11 @@ def _check(status: int, call: str) -> None:
         raise IsingError(status, call)
 
 
-def _buf_ptr(buf, nbytes_needed: int, writable: bool):
-    """Pointer + length of a host int8 buffer (numpy array or CPU torch tensor)."""
+def _buf_ptr(buf, nbytes_needed: int, writable: bool, dtype=np.int8):
+    """Pointer + length of a host int8 (uint8: bit-packed) buffer (numpy array or CPU tensor)."""
     if isinstance(buf, np.ndarray):
-        if buf.dtype != np.int8 or not buf.flags["C_CONTIGUOUS"]:
-            raise ValueError("lattice buffers must be C-contiguous int8")
+        if buf.dtype != dtype or not buf.flags["C_CONTIGUOUS"]:
+            raise ValueError(f"lattice buffers must be C-contiguous {np.dtype(dtype).name}")
         if writable and not buf.flags["WRITEABLE"]:
             raise ValueError("output buffer is read-only")
         return buf.ctypes.data, buf.size
@@ -115,8 +117,9 @@ def _buf_ptr(buf, nbytes_needed: int, writable: bool):
     if hasattr(buf, "data_ptr"):
         import torch
 
-        if buf.dtype != torch.int8 or not buf.is_contiguous() or buf.is_cuda:
-            raise ValueError("lattice tensors must be contiguous int8 host tensors")
+        want = torch.int8 if dtype == np.int8 else torch.uint8
+        if buf.dtype != want or not buf.is_contiguous() or buf.is_cuda:
+            raise ValueError(f"lattice tensors must be contiguous {want} host tensors")
         return buf.data_ptr(), buf.numel()
     raise TypeError("expected a numpy int8 array or an int8 torch tensor")
 
@@ -205,6 +208,16 @@ def ising_init_cold(h: int) -> None:
 def ising_write_lattice(h: int, buf, t: int = 0) -> None:
     ptr, n = _buf_ptr(buf, 0, writable=False)
     _check(load().ising_write_lattice(h, ptr, n, int(t)), "ising_write_lattice")
+
+
+def ising_write_lattice_bits(h: int, buf, t: int = 0) -> None:
+    ptr, n = _buf_ptr(buf, 0, writable=False, dtype=np.uint8)
+    _check(load().ising_write_lattice_bits(h, ptr, n, int(t)), "ising_write_lattice_bits")
+
+
+def ising_read_lattice_bits(h: int, out) -> None:
+    ptr, n = _buf_ptr(out, 0, writable=True, dtype=np.uint8)
+    _check(load().ising_read_lattice_bits(h, ptr, n), "ising_read_lattice_bits")
 
 
 def ising_sweep(h: int, n: int) -> None:
@@ -468,6 +481,17 @@ class IsingLattice:
 
     def observables(self) -> tuple[int, int]:
         return ising_observables(self.h)
+
+    def write_lattice_bits(self, bits, t: int = 0):
+        """Load from the bit-packed format (np.packbits(lattice == 1, bitorder="little"))."""
+        ising_write_lattice_bits(self.h, bits, t)
+        return self
+
+    def read_lattice_bits(self, out=None) -> np.ndarray:
+        if out is None:
+            out = np.empty(self.N * self.M // 8, dtype=np.uint8)
+        ising_read_lattice_bits(self.h, out)
+        return out
 
     def read_rows(self, row_begin: int, nrows: int, out=None) -> np.ndarray:
         if out is None:

@@ -1,7 +1,10 @@
 """Small workloads for compute-sanitizer (memcheck / racecheck / synccheck / initcheck): C1,
 virtual slabs with R = 2, heat bath (0 / 1 / 2 "always" classes), draw-free, the TMA-staged
 kernel (shared memory + mbarrier, ragged band), both basic-layout kernels, measured chain,
-graph replay, the asynchronous measured chain, and (SANITIZE_BIG=1) the guided tail."""
+graph replay, the asynchronous measured chain, the rank transports in self-exchange form
+(p2p flags / fences, NCCL self send-recv), and (SANITIZE_BIG=1) the guided tail.  (Not the
+same-process rank groups: the sanitizer serialises kernels, and a rank's phase that waits on
+another rank's flags can then never see them.)"""
 import os
 import sys
 
@@ -45,6 +48,17 @@ t2 = a.measure_async(3, 1, bufs[2], bufs[3])
 a.measure_wait(t1)
 a.measure_wait(t2)
 print("async", bufs[1].tolist(), bufs[3].tolist(), "variant", h.kernel_variant())
+from paper_1906_06297_b200 import ising  # noqa: E402
+
+os.environ["ISING_SELF_EXCHANGE"] = "1"
+for name, mk in (("p2p-self", lambda: ising.ising_create_rank_p2p(96, 8192, 8, 0, 1, 0)),
+                 ("nccl-self", lambda: ising.ising_create_rank(96, 8192, 8, 0, 1, 0, None))):
+    x = IsingLattice(96, 8192, 8, _handle=mk()).set_beta(0.4406868).init_random()
+    x.sweep(2)
+    x.measure(2, 1)
+    print(name, x.observables())
+    x.close()
+os.environ.pop("ISING_SELF_EXCHANGE")
 if os.environ.get("SANITIZE_BIG"):  # >= 3 waves: the staged kernel's guided tail (memcheck)
     big = IsingLattice(7168, 32768, 9).set_beta(0.4406868).init_random()
     big.sweep(1)
