@@ -237,7 +237,21 @@ struct ising_ctx {
   int8_t* bplane[2] = {nullptr, nullptr};
   PendingMeasure pending[kMaxPending];
   int64_t next_ticket = 0;
+  // ISING_TRACE=file.csv: timing events around the pieces of the first kMaxTracedPhases
+  // half-sweeps (boundary rows, halo transfer on the comm stream, interior), written at
+  // destroy as "phase,name,stream,ms" relative to the first event — a timeline of the
+  // halo / interior overlap without a system profiler
+  std::string trace_path;
+  struct TraceEvent {
+    int64_t phase;
+    const char* name;
+    const char* stream;
+    cudaEvent_t ev;
+  };
+  std::vector<TraceEvent> trace;
+  int64_t traced_phases = 0;
 };
+constexpr int64_t kMaxTracedPhases = 64;
 
 namespace {
 
@@ -450,8 +464,11 @@ bool p2p_flags(const ising_ctx* h) { return h->p2p && (h->world > 1 || h->self_e
 // rank handle whose halos move by NCCL send / recv (neighbours, or itself)
 bool nccl_halos(const ising_ctx* h) { return h->rank_mode && !h->p2p && h->comm != nullptr; }
 
+void trace_dump(ising_ctx* h);
+
 void destroy_ctx(ising_ctx* h) {
   if (!h) return;
+  trace_dump(h);
   if (p2p_flags(h) && h->connected && !h->devs.empty()) {
     // the neighbours may still be storing into this slab's halo rows (their last phase):
     // wait for them before the memory goes away (best effort: errors are ignored here)
@@ -638,6 +655,33 @@ int ensure_prof_events(ising_ctx* h, int64_t n_sweeps) {
   return ISING_OK;
 }
 
+// Record a timing event of the trace (no-op unless ISING_TRACE is set).
+int trace_mark(ising_ctx* h, const char* name, cudaStream_t st, const char* stream_name) {
+  if (h->trace_path.empty() || h->traced_phases >= kMaxTracedPhases) return ISING_OK;
+  cudaEvent_t e;
+  CU(cudaEventCreate(&e));
+  h->trace.push_back({h->traced_phases, name, stream_name, e});
+  CU(cudaEventRecord(e, st));
+  return ISING_OK;
+}
+
+void trace_dump(ising_ctx* h) {
+  if (h->trace.empty()) return;
+  cudaDeviceSynchronize();
+  FILE* f = fopen(h->trace_path.c_str(), "w");
+  if (f) {
+    fprintf(f, "phase,name,stream,ms\n");
+    for (auto& t : h->trace) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, h->trace[0].ev, t.ev);
+      fprintf(f, "%lld,%s,%s,%.6f\n", (long long)t.phase, t.name, t.stream, ms);
+    }
+    fclose(f);
+  }
+  for (auto& t : h->trace) cudaEventDestroy(t.ev);
+  h->trace.clear();
+}
+
 // One colour phase, LOCAL mode.
 int phase_local(ising_ctx* h, int c, uint32_t t, bool t_from_dev = false,
                 const std::vector<unsigned long long*>* obs = nullptr, bool slot_from_dev = false) {
@@ -686,10 +730,13 @@ int phase_rank(ising_ctx* h, int c, uint32_t t) {
   Device& d = h->devs[0];
   const int R = (int)s.R;
   const size_t W = (size_t)h->W;
+  TRY(trace_mark(h, "boundary_start", d.stream, "compute"));
   TRY(run_halfsweep(h, s, c, 0, 1, nullptr, nullptr, t));
   if (R > 1) TRY(run_halfsweep(h, s, c, R - 1, R, nullptr, nullptr, t));
+  TRY(trace_mark(h, "boundary_end", d.stream, "compute"));
   CU(cudaEventRecord(d.ev_bnd, d.stream));
   CU(cudaStreamWaitEvent(d.comm, d.ev_bnd, 0));
+  TRY(trace_mark(h, "halo_start", d.comm, "comm"));
   const int up = (h->rank + h->world - 1) % h->world, dn = (h->rank + 1) % h->world;
   uint64_t* pl = s.plane[c];
   NC(ncclGroupStart());
@@ -698,9 +745,13 @@ int phase_rank(ising_ctx* h, int c, uint32_t t) {
   NC(ncclSend(pl + (size_t)R * W, W, ncclUint64, dn, h->comm, d.comm)); // row R-1 -> dn's top halo
   NC(ncclRecv(pl, W, ncclUint64, up, h->comm, d.comm));
   NC(ncclGroupEnd());
+  TRY(trace_mark(h, "halo_end", d.comm, "comm"));
   CU(cudaEventRecord(d.ev_comm, d.comm));
+  TRY(trace_mark(h, "interior_start", d.stream, "compute"));
   TRY(run_halfsweep(h, s, c, 1, R - 1, nullptr, nullptr, t));
+  TRY(trace_mark(h, "interior_end", d.stream, "compute"));
   CU(cudaStreamWaitEvent(d.stream, d.ev_comm, 0));
+  if (!h->trace_path.empty()) ++h->traced_phases;
   return ISING_OK;
 }
 
@@ -710,8 +761,11 @@ int phase_rank(ising_ctx* h, int c, uint32_t t) {
 int phase_p2p(ising_ctx* h, int c, uint32_t t, unsigned long long* obs = nullptr) {
   NvtxRange range("half-sweep p2p c=%lld t=%lld", c, t);
   Slab& s = h->slabs[0];
+  TRY(trace_mark(h, "phase_start", h->devs[0].stream, "compute"));
   TRY(run_halfsweep(h, s, c, 0, (int)s.R, h->up_plane[c] + (s.R + 1) * h->W, h->dn_plane[c], t,
                     false, obs));
+  TRY(trace_mark(h, "phase_end", h->devs[0].stream, "compute"));
+  if (!h->trace_path.empty()) ++h->traced_phases;
   ++h->phase;
   return ISING_OK;
 }
@@ -875,6 +929,7 @@ int enable_peers(ising_ctx* h) {
 
 // Experiment / test knobs read once at creation (every handle type).
 void read_env_knobs(ising_ctx* h) {
+  if (const char* tr = getenv("ISING_TRACE")) h->trace_path = tr;
   const char* env = getenv("ISING_ROWS_PER_ITEM");
   if (env) h->rows_per_item_override = atoi(env);
   if (env_is_zero("ISING_GRAPHS")) h->graphs_enabled = false;
