@@ -290,6 +290,8 @@ def self_exchange_lattice(N: int, M: int, dev: int, transport: str):
     try:
         if transport == "p2p":
             h = ising.ising_create_rank_p2p(N, M, SEED, 0, 1, dev)
+        elif transport == "lsa":
+            h = ising.ising_create_rank_lsa(N, M, SEED, 0, 1, dev, None)
         else:
             h = ising.ising_create_rank(N, M, SEED, 0, 1, dev, None)
     finally:
@@ -619,7 +621,7 @@ def run_ours(args):
     if main_legs and n == 1:
         # the multi-GPU transports' per-GPU cost, each rank its own neighbour
         transports = {"local": {"value": value, "ms_per_step": ms / args.steps}}
-        for tname in ("p2p", "nccl"):
+        for tname in ("p2p", "lsa", "nccl"):
             try:
                 tl = self_exchange_lattice(N, M, dev, tname)
                 tms = timed_sweeps(tl, args.steps, 2, R)
@@ -633,14 +635,18 @@ def run_ours(args):
         invariance = invariance_check(n, None, R)
         if main_legs:
             transports = {"p2p": {"value": value, "ms_per_step": ms / args.steps}}
-            if same_dev:
-                transports["nccl"] = {"skipped": "NCCL rejects two ranks on one device "
-                                                 "(same-device functional run)"}
-            else:
-                nl = leg("c3_nccl", N, M, n, args.steps, 2, R, transport="nccl")
-                transports["nccl"] = {"value": nl["value"], "ms_per_step": nl["ms_per_step"],
-                                      "transport": nl["transport"],
-                                      "invariance": invariance_check(n, "nccl", R)}
+            for tname in ("lsa", "nccl"):
+                if same_dev:
+                    transports[tname] = {"skipped": "NCCL rejects two ranks on one device "
+                                                    "(same-device functional run)"}
+                    continue
+                try:
+                    nl = leg("c3_" + tname, N, M, n, args.steps, 2, R, transport=tname)
+                    transports[tname] = {"value": nl["value"], "ms_per_step": nl["ms_per_step"],
+                                         "transport": nl["transport"],
+                                         "invariance": invariance_check(n, tname, R)}
+                except Exception as e:  # reported, not hidden (every rank raises alike)
+                    transports[tname] = {"error": repr(e)}
     if main_legs:
         legs["c4_strong"] = scaling_leg("c4_strong", "strong", n, max(4, min(args.steps, 32)), 2, R)
         legs["c5_weak"] = scaling_leg("c5_weak", "weak", n, max(2, min(args.steps, 8)), 1, R)

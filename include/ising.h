@@ -105,6 +105,17 @@ int ising_create_rank_p2p(ising_t* out, int64_t L_rows, int64_t L_cols, uint64_t
 int ising_ipc_handle(ising_t h, void* blob, size_t len);            /* len >= 256 */
 int ising_ipc_connect(ising_t h, const void* blobs, size_t len);    /* world * 256 bytes */
 
+/* One process per GPU, the rank-p2p kernel protocol (fused peer stores + flags in peer
+ * memory) over NCCL 2.28 symmetric memory instead of CUDA IPC (SURVEY §8(f) row f4's NCCL
+ * device API): the planes and the flag area are allocated with ncclMemAlloc and registered as
+ * symmetric windows (ncclCommWindowRegister, NCCL_WIN_COLL_SYMMETRIC), and the neighbours'
+ * addresses come from ncclGetLsaPointer on the device.  Arguments as ising_create_rank (the
+ * NCCL unique id from rank 0; world == 1: nccl_id may be NULL; ISING_SELF_EXCHANGE=1 as for
+ * rank-p2p).  Every rank must be in the others' load/store-accessible (LSA) team — one
+ * NVLink domain — else NCCL error.  world <= 8.  Collective: create and destroy. */
+int ising_create_rank_lsa(ising_t* out, int64_t L_rows, int64_t L_cols, uint64_t seed, int rank,
+                          int world, int device, const void* nccl_id, size_t id_len);
+
 /* Connect the n rank-p2p handles of one lattice that live in THIS process (handles[r] =
  * rank r, all created with world = n) through their device pointers instead of CUDA IPC:
  * one process drives every rank, one host thread per handle (calls on different handles may

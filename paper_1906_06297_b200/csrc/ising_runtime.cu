@@ -24,6 +24,7 @@
 // byte-per-spin layout (ising_create_basic, §3.1) has its own kernels.
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nccl_device.h>
 #include <nvtx3/nvToolsExt.h>
 #include <sched.h>
 
@@ -212,6 +213,11 @@ struct ising_ctx {
   uint64_t* dn_plane[2] = {nullptr, nullptr};
   unsigned long long* peer_sync[kMaxRanks] = {};
   std::vector<void*> opened;               // IPC mappings to close
+  // rank-lsa transport (ising_create_rank_lsa): the planes and the flag area live in NCCL
+  // symmetric memory (ncclMemAlloc + ncclCommWindowRegister) and the neighbours' addresses
+  // come from the NCCL device API (ncclGetLsaPointer) instead of CUDA IPC
+  bool lsa = false;
+  ncclWindow_t win[3] = {nullptr, nullptr, nullptr};  // plane 0, plane 1, sync
   unsigned long long phase = 0;            // completed phases (init/write count as one)
   unsigned long long gather_epoch = 0;
   // CUDA graph of kGraphSweeps sweeps for small lattices (launch-bound), single device
@@ -379,6 +385,38 @@ int alloc_slabs(ising_ctx* h) {
   return ISING_OK;
 }
 
+// The neighbours' plane addresses and every rank's flag area in this rank's address space,
+// from the NCCL device API (LSA pointers of symmetric windows); out[0..1] up planes,
+// out[2..3] down planes, out[4 + q] rank q's sync area.
+__global__ void k_lsa_pointers(ncclWindow_t w0, ncclWindow_t w1, ncclWindow_t ws, int up, int dn,
+                               const int* lsa_rank, int world, void** out) {
+  out[0] = ncclGetLsaPointer(w0, 0, up);
+  out[1] = ncclGetLsaPointer(w1, 0, up);
+  out[2] = ncclGetLsaPointer(w0, 0, dn);
+  out[3] = ncclGetLsaPointer(w1, 0, dn);
+  for (int q = 0; q < world; ++q) out[4 + q] = ncclGetLsaPointer(ws, 0, lsa_rank[q]);
+}
+
+cudaError_t lsa_peer_pointers(cudaStream_t st, const ncclWindow_t win[3], int up, int dn,
+                              const int* lsa_rank, int world, void** host_out) {
+  int* d_rank = nullptr;
+  void** d_out = nullptr;
+  cudaError_t e = cudaMalloc(&d_rank, sizeof(int) * kMaxRanks);
+  if (e == cudaSuccess) e = cudaMalloc(&d_out, sizeof(void*) * (4 + kMaxRanks));
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(d_rank, lsa_rank, sizeof(int) * world, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) {
+    k_lsa_pointers<<<1, 1, 0, st>>>(win[0], win[1], win[2], up, dn, d_rank, world, d_out);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(host_out, d_out, sizeof(void*) * (4 + world), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (d_rank) cudaFree(d_rank);
+  if (d_out) cudaFree(d_out);
+  return e;
+}
+
 // Release every resource of a Device (streams, events, buffers); safe on a partial setup.
 void teardown_device(Device& d) {
   if (d.dev < 0) return;
@@ -475,6 +513,17 @@ void destroy_ctx(ising_ctx* h) {
     cudaSetDevice(h->devs[0].dev);
     if (p2p_wait(h) == ISING_OK) cudaStreamSynchronize(h->devs[0].stream);
     cudaGetLastError();
+  }
+  if (h->lsa) {  // symmetric memory: deregister (collective) and free through NCCL
+    if (!h->devs.empty()) cudaSetDevice(h->devs[0].dev);
+    for (auto& w : h->win)
+      if (w && h->comm) ncclCommWindowDeregister(h->comm, w);
+    for (auto& s : h->slabs)
+      for (int c = 0; c < 2; ++c)
+        if (s.plane[c]) ncclMemFree(s.plane[c]);
+    if (h->sync) ncclMemFree(h->sync);
+    for (auto& s : h->slabs) s.plane[0] = s.plane[1] = nullptr;
+    h->sync = nullptr;
   }
   for (auto& s : h->slabs) {
     if (s.devi < (int)h->devs.size()) cudaSetDevice(h->devs[s.devi].dev);
@@ -1435,6 +1484,92 @@ int ising_create_rank_p2p(ising_t* out, int64_t L_rows, int64_t L_cols, uint64_t
     h->self_exchange = env_is_one("ISING_SELF_EXCHANGE");
     h->connected = true;
   }
+  read_env_knobs(h);
+  *out = h;
+  return ISING_OK;
+}
+
+int ising_create_rank_lsa(ising_t* out, int64_t L_rows, int64_t L_cols, uint64_t seed, int rank,
+                          int world, int device, const void* nccl_id, size_t id_len) {
+  if (!out || world < 1 || world > kMaxRanks || rank < 0 || rank >= world) return ISING_ERR_ARG;
+  if (world > 1 && (!nccl_id || id_len < sizeof(ncclUniqueId))) return ISING_ERR_ARG;
+  *out = nullptr;
+  TRY(check_shape(L_rows, L_cols, world));
+  ising_ctx* h = new (std::nothrow) ising_ctx;
+  if (!h) return ISING_ERR_OOM;
+  h->N = L_rows;
+  h->M = L_cols;
+  h->W = L_cols / 32;
+  h->seed = seed;
+  h->rank_mode = true;
+  h->p2p = true;  // the same fused peer-store + flag protocol as rank-p2p
+  h->lsa = true;
+  h->rank = rank;
+  h->world = world;
+  make_keys(seed, &h->keys);
+  h->devs.emplace_back();
+  auto fail = [&](int st) {
+    destroy_ctx(h);
+    return st;
+  };
+  int st = setup_device(h->devs[0], device);
+  if (st != ISING_OK) return fail(st);
+  Device& d = h->devs[0];
+  {
+    ncclUniqueId u;
+    ncclResult_t r = ncclSuccess;
+    if (world > 1)
+      memcpy(&u, nccl_id, sizeof u);
+    else
+      r = ncclGetUniqueId(&u);
+    if (r == ncclSuccess) r = ncclCommInitRank(&h->comm, world, u, rank);
+    if (r != ncclSuccess) return fail(fail_nccl(r, "ncclCommInitRank", __LINE__));
+  }
+  Slab sl;
+  sl.devi = 0;
+  sl.R = L_rows / world;
+  sl.row0 = rank * sl.R;
+  h->slabs.push_back(sl);
+  Slab& s = h->slabs[0];
+  const size_t bytes = (size_t)(s.R + 2) * (size_t)h->W * sizeof(uint64_t);
+  // symmetric allocations and windows, in the same order on every rank (collective)
+  ncclResult_t r = ncclSuccess;
+  for (int c = 0; c < 2 && r == ncclSuccess; ++c) r = ncclMemAlloc((void**)&s.plane[c], bytes);
+  if (r == ncclSuccess) r = ncclMemAlloc((void**)&h->sync, kSyncBytes);
+  if (r != ncclSuccess) return fail(fail_nccl(r, "ncclMemAlloc", __LINE__));
+  cudaError_t e = cudaSuccess;
+  for (int c = 0; c < 2 && e == cudaSuccess; ++c) e = cudaMemsetAsync(s.plane[c], 0, bytes, d.stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(h->sync, 0, kSyncBytes, d.stream);
+  if (e == cudaSuccess) e = cudaMalloc(&h->done_counter, sizeof(unsigned int));
+  if (e == cudaSuccess) e = cudaMemsetAsync(h->done_counter, 0, sizeof(unsigned int), d.stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(d.stream);
+  if (e != cudaSuccess) return fail(fail_cuda(e, "rank-lsa buffers", __LINE__));
+  for (int c = 0; c < 2 && r == ncclSuccess; ++c)
+    r = ncclCommWindowRegister(h->comm, s.plane[c], bytes, &h->win[c], NCCL_WIN_COLL_SYMMETRIC);
+  if (r == ncclSuccess)
+    r = ncclCommWindowRegister(h->comm, h->sync, kSyncBytes, &h->win[2], NCCL_WIN_COLL_SYMMETRIC);
+  if (r != ncclSuccess) return fail(fail_nccl(r, "ncclCommWindowRegister", __LINE__));
+  // every rank must be reachable by load / store (one NVLink domain): LSA rank of each rank
+  const ncclTeam_t wt = ncclTeamWorld(h->comm), lt = ncclTeamLsa(h->comm);
+  int lsa_rank[kMaxRanks];
+  for (int q = 0; q < world; ++q) {
+    if (!ncclTeamRankIsMember(lt, wt, q)) {
+      g_last_error = "ising_create_rank_lsa: a rank is outside this rank's load/store (LSA) team";
+      return fail(ISING_ERR_NCCL);
+    }
+    lsa_rank[q] = ncclTeamRankToLsa(h->comm, wt, q);
+  }
+  void* ptrs[2 + 2 + kMaxRanks] = {};  // up planes, down planes, every rank's sync area
+  const int up = (rank + world - 1) % world, dn = (rank + 1) % world;
+  e = lsa_peer_pointers(d.stream, h->win, lsa_rank[up], lsa_rank[dn], lsa_rank, world, ptrs);
+  if (e != cudaSuccess) return fail(fail_cuda(e, "ncclGetLsaPointer", __LINE__));
+  for (int c = 0; c < 2; ++c) {
+    h->up_plane[c] = (uint64_t*)ptrs[c];
+    h->dn_plane[c] = (uint64_t*)ptrs[2 + c];
+  }
+  for (int q = 0; q < world; ++q) h->peer_sync[q] = (unsigned long long*)ptrs[4 + q];
+  h->self_exchange = world == 1 && env_is_one("ISING_SELF_EXCHANGE");
+  h->connected = true;
   read_env_knobs(h);
   *out = h;
   return ISING_OK;

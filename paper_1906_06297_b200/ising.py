@@ -38,6 +38,7 @@ SIGNATURES = {
     "ising_create_rank": (_INT, [ctypes.POINTER(_VP), _I64, _I64, _U64, _INT, _INT, _INT, _VP, _SZ]),
     "ising_nccl_unique_id": (_INT, [_VP, _SZ]),
     "ising_create_rank_p2p": (_INT, [ctypes.POINTER(_VP), _I64, _I64, _U64, _INT, _INT, _INT]),
+    "ising_create_rank_lsa": (_INT, [ctypes.POINTER(_VP), _I64, _I64, _U64, _INT, _INT, _INT, _VP, _SZ]),
     "ising_create_basic": (_INT, [ctypes.POINTER(_VP), _I64, _I64, _U64, _INT]),
     "ising_ipc_handle": (_INT, [_VP, _VP, _SZ]),
     "ising_ipc_connect": (_INT, [_VP, _VP, _SZ]),
@@ -159,6 +160,16 @@ def ising_create_rank_p2p(L_rows: int, L_cols: int, seed: int, rank: int, world:
     h = _VP()
     _check(load().ising_create_rank_p2p(ctypes.byref(h), L_rows, L_cols, seed, rank, world, device),
            "ising_create_rank_p2p")
+    return h.value
+
+
+def ising_create_rank_lsa(L_rows: int, L_cols: int, seed: int, rank: int, world: int, device: int,
+                          nccl_id: bytes | None) -> int:
+    h = _VP()
+    idbuf = ctypes.create_string_buffer(nccl_id, NCCL_ID_BYTES) if nccl_id else None
+    _check(load().ising_create_rank_lsa(ctypes.byref(h), L_rows, L_cols, seed, rank, world, device,
+                                        idbuf, NCCL_ID_BYTES if nccl_id else 0),
+           "ising_create_rank_lsa")
     return h.value
 
 
@@ -351,8 +362,9 @@ class IsingLattice:
 
         transport "p2p" (default): the half-sweep kernel stores halo rows into the
         neighbours' memory and synchronises through flags in peer memory
-        (ising_create_rank_p2p).  "nccl": ncclSend/ncclRecv of the halo rows on a comm
-        stream overlapped with the interior (ising_create_rank)."""
+        (ising_create_rank_p2p, CUDA IPC mappings).  "lsa": the same kernel protocol over NCCL
+        symmetric memory windows (ising_create_rank_lsa).  "nccl": ncclSend/ncclRecv of the
+        halo rows on a comm stream overlapped with the interior (ising_create_rank)."""
         import torch.distributed as dist
 
         transport = transport or os.environ.get("ISING_TRANSPORT", "p2p")
@@ -391,15 +403,16 @@ class IsingLattice:
 
             warnings.warn(f"rank-p2p transport unavailable ({err or 'on another rank'}); using NCCL")
             transport = "nccl"
-        if transport == "nccl":
+        if transport in ("nccl", "lsa"):
             obj = [ising_nccl_unique_id() if (rank == 0 and world > 1) else None]
             if world > 1:
                 dist.broadcast_object_list(obj, src=0)
-            h = ising_create_rank(L_rows, L_cols, seed, rank, world, device, obj[0])
+            create = ising_create_rank if transport == "nccl" else ising_create_rank_lsa
+            h = create(L_rows, L_cols, seed, rank, world, device, obj[0])
         else:
             raise ValueError(f"unknown transport {transport!r}")
         lat = cls(L_rows, L_cols, seed, _handle=h)
-        lat.transport = "nccl"
+        lat.transport = transport
         return lat
 
     @classmethod

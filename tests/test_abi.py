@@ -84,6 +84,9 @@ def test_shapes_beyond_the_draw_counter_or_int32_slab_rows_are_rejected():
         with pytest.raises(ising.IsingError) as ei:
             ising.ising_create_rank(N, M, 1, 0, 1, 0, None)
         assert ei.value.status == ising.ISING_ERR_ARG, (N, M)
+        with pytest.raises(ising.IsingError) as ei:
+            ising.ising_create_rank_lsa(N, M, 1, 0, 1, 0, None)
+        assert ei.value.status == ising.ISING_ERR_ARG, (N, M)
     # 2^32 rows in 4 slabs of 2^30 is within every limit: it gets past the shape check and
     # fails only at the device (none here)
     with pytest.raises(ising.IsingError) as ei:

@@ -7,7 +7,8 @@
   sweeps in one call per rank, the ranks coupled only through the flags in peer memory) are
   compared with the oracle bit for bit (reading R19).
 * Self exchange (ISING_SELF_EXCHANGE=1, world 1): the rank is its own neighbour through the
-  whole protocol — the rank-p2p flags / fences / peer-store path, and the NCCL transport's
+  whole protocol — the rank-p2p flags / fences / peer-store path (over CUDA IPC mappings, and
+  over NCCL symmetric-memory windows: ising_create_rank_lsa), and the NCCL transport's
   boundary-rows-first, ncclSend/ncclRecv-on-a-comm-stream, interior-overlap path
   (PAPER.md:224), which NCCL does not allow for two ranks on one GPU.
 """
@@ -117,12 +118,14 @@ def self_exchange(monkeypatch):
     monkeypatch.setenv("ISING_SELF_EXCHANGE", "1")
 
 
-@pytest.mark.parametrize("transport", ["p2p", "nccl"])
+@pytest.mark.parametrize("transport", ["p2p", "nccl", "lsa"])
 @pytest.mark.parametrize("N,M", [(64, 64), (130, 192), (2, 64), (96, 8192), (7168, 32768)])
 def test_self_exchange_transport_matches_oracle(self_exchange, transport, N, M):
     seed = 2
     if transport == "p2p":
         h = ising.ising_create_rank_p2p(N, M, seed, 0, 1, 0)
+    elif transport == "lsa":  # the p2p kernel protocol over NCCL symmetric-memory windows
+        h = ising.ising_create_rank_lsa(N, M, seed, 0, 1, 0, None)
     else:
         h = ising.ising_create_rank(N, M, seed, 0, 1, 0, None)
     g = IsingLattice(N, M, seed, _handle=h)
