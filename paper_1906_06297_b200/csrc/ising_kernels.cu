@@ -465,8 +465,7 @@ __device__ __forceinline__ void philox8(uint32_t t, uint32_t c1base, uint32_t co
   }
 #pragma unroll
   for (int b = 0; b < 8; ++b) out[b] = make_uint4(c0[b], c1[b], c2[b], c3[b]);
-  return;
-#endif
+#else
 #pragma unroll
   for (int b = 0; b < 8; ++b) {
     c0[b] = t;
@@ -490,6 +489,7 @@ __device__ __forceinline__ void philox8(uint32_t t, uint32_t c1base, uint32_t co
   }
 #pragma unroll
   for (int b = 0; b < 8; ++b) out[b] = make_uint4(c0[b], c1[b], c2[b], c3[b]);
+#endif
 }
 
 // Experiment (ISING_SEL1): one compare per lane against the threshold the lane's class needs.

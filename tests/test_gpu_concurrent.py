@@ -163,3 +163,28 @@ def test_profiling_survives_measured_chains():
             assert g.kernel_stats()[1] == 10
         finally:
             g.close()
+
+
+def test_trace_timeline_of_the_nccl_transport(self_exchange, monkeypatch, tmp_path):
+    """ISING_TRACE: every traced half-sweep records its boundary rows, the halo group on the
+    comm stream and the interior, in stream order, and the result stays bit-exact."""
+    import csv
+
+    path = tmp_path / "trace.csv"
+    monkeypatch.setenv("ISING_TRACE", str(path))
+    N, M, seed = 96, 8192, 3
+    g = IsingLattice(N, M, seed, _handle=ising.ising_create_rank(N, M, seed, 0, 1, 0, None))
+    g.set_beta(BETA).init_random().sweep(3)
+    got = g.read_lattice()
+    g.close()  # writes the trace
+    o = oracle.Lattice(N, M, seed).init_random().set_beta(BETA).sweep(3)
+    assert np.array_equal(got, o.full())
+    rows = list(csv.DictReader(open(path)))
+    phases = sorted({int(r["phase"]) for r in rows})
+    assert phases == list(range(6))
+    for p in phases:
+        ev = {r["name"]: float(r["ms"]) for r in rows if int(r["phase"]) == p}
+        assert set(ev) == {"boundary_start", "boundary_end", "halo_start", "halo_end",
+                           "interior_start", "interior_end"}
+        assert ev["boundary_start"] <= ev["boundary_end"] <= ev["halo_start"] <= ev["halo_end"]
+        assert ev["boundary_end"] <= ev["interior_start"] <= ev["interior_end"]
