@@ -1088,6 +1088,11 @@ __global__ void __launch_bounds__(kStageThreads, staged_minb(RULE)) k_halfsweep_
     ra = p.r_begin + p.tail_row4 + (band - p.tail_band4) * p.tail_h2;
     rb = min(ra + p.tail_h2, p.r_end);
   }
+  if (p.mirror) {  // same band heights, rows mirrored within [r_begin, r_end)
+    const int a = ra;
+    ra = p.r_begin + p.r_end - rb;
+    rb = p.r_begin + p.r_end - a;
+  }
   const int nrows = rb - ra;
   // rank-p2p: only the bands at the slab edges depend on the neighbours — they read the halo
   // rows the neighbours stored in the previous phase and store rows 0 / R - 1 into halo rows

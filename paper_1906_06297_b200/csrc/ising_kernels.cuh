@@ -53,6 +53,8 @@ struct HalfSweepParams {
   int32_t tail_row4;      //   first row (relative to r_begin) of the 4-row bands
   int32_t tail_h1, tail_h2;  // tail band heights (8, 4)
   int32_t pdl;            // staged kernel launched as a programmatic dependent launch
+  int32_t mirror;         // staged kernel: bands walk the rows bottom-up (row r -> r_begin +
+                          // r_end - 1 - r): the first wave reads what the previous phase wrote last
   uint32_t t;             // sweep index (>= 1), or the offset added to *t_dev
   const uint32_t* t_dev;  // graph replays: device-resident sweep base (null otherwise)
   uint32_t colour;        // 0 black, 1 white

@@ -233,6 +233,9 @@ struct ising_ctx {
   bool staged = true;                      // TMA-staged half-sweep (ISING_STAGED=0: off)
   bool guided_tail = !env_is_zero("ISING_TAIL");  // staged kernel: 8- / 4-row last waves
   bool pdl = !env_is_zero("ISING_PDL");  // staged kernel: programmatic dependent launch
+  // staged kernel: white phases walk the bands bottom-up (ISING_MIRROR=0: off); C3 1552 ->
+  // 1567, 16384 x 32768 1515 -> 1542 flips/ns (profiles/r02_ncu_halfsweep.md)
+  bool mirror = !env_is_zero("ISING_MIRROR");
   // heat-bath variant 7 (ISING_HB_SYMMETRIC=0: off, for every handle type)
   bool symmetric_hb_enabled = !env_is_zero("ISING_HB_SYMMETRIC");
   bool draw_free_enabled = true;           // beta in {0, inf}: skip Philox (ISING_DRAW_FREE=0)
@@ -632,6 +635,10 @@ int run_halfsweep(ising_ctx* h, Slab& s, int c, int r_begin, int r_end, uint64_t
                     (size_t)(2 * h->kernel_launches + 1) < h->prof_events.size();
   if (prof) CU(cudaEventRecord(h->prof_events[2 * h->kernel_launches], d.stream));
   p.pdl = h->pdl ? 1 : 0;
+  // Alternate the band order between phases, so each phase's first wave reads the rows the
+  // previous phase wrote last (still in L2).  (Rank-p2p: the edge bands stay first in the grid;
+  // mirroring swaps which rows the first and last logical band hold, both still edge rows.)
+  p.mirror = (h->mirror && c == 1) ? 1 : 0;
   if (h->staged && h->W % kStageWords == 0) {
     CU(launch_halfsweep_staged(kernel_variant(h),
                                h->guided_tail ? (int64_t)d.sms * d.staged_blocks_per_sm : 0, d.stream, p));
