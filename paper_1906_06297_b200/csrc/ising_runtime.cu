@@ -182,6 +182,7 @@ struct ising_ctx {
   bool rank_mode = false;
   int rank = 0, world = 1;
   ncclComm_t comm = nullptr;
+  bool comm_aborted = false;  // an asynchronous NCCL error aborted comm: every later call fails
   std::vector<Device> devs;
   std::vector<Slab> slabs;
   std::vector<int> slab_of_rank;  // unused in local mode
@@ -503,7 +504,9 @@ int p2p_wait(ising_ctx* h);
 // rank-p2p handle whose half-sweeps run the flag protocol (neighbours, or itself)
 bool p2p_flags(const ising_ctx* h) { return h->p2p && (h->world > 1 || h->self_exchange); }
 // rank handle whose halos move by NCCL send / recv (neighbours, or itself)
-bool nccl_halos(const ising_ctx* h) { return h->rank_mode && !h->p2p && h->comm != nullptr; }
+bool nccl_halos(const ising_ctx* h) {
+  return h->rank_mode && !h->p2p && (h->comm != nullptr || h->comm_aborted);
+}
 
 void trace_dump(ising_ctx* h);
 
@@ -520,7 +523,7 @@ void destroy_ctx(ising_ctx* h) {
   if (h->lsa) {  // symmetric memory: deregister (collective) and free through NCCL
     if (!h->devs.empty()) cudaSetDevice(h->devs[0].dev);
     for (auto& w : h->win)
-      if (w && h->comm) ncclCommWindowDeregister(h->comm, w);
+      if (w && h->comm && !h->comm_aborted) ncclCommWindowDeregister(h->comm, w);
     for (auto& s : h->slabs)
       for (int c = 0; c < 2; ++c)
         if (s.plane[c]) ncclMemFree(s.plane[c]);
@@ -533,7 +536,7 @@ void destroy_ctx(ising_ctx* h) {
     for (int c = 0; c < 2; ++c)
       if (s.plane[c]) cudaFree(s.plane[c]);
   }
-  if (h->comm) ncclCommDestroy(h->comm);
+  if (h->comm && !h->comm_aborted) ncclCommDestroy(h->comm);
   for (void* ptr : h->opened) cudaIpcCloseMemHandle(ptr);
   if (h->sync) cudaFree(h->sync);
   if (h->done_counter) cudaFree(h->done_counter);
@@ -657,13 +660,18 @@ int run_halfsweep(ising_ctx* h, Slab& s, int c, int r_begin, int r_end, uint64_t
 // error state (SURVEY §5 failure detection).  On an error the communicator is aborted, so a
 // stream blocked in an NCCL kernel does not hang the process.
 int nccl_poll(ising_ctx* h) {
+  if (h->comm_aborted) {
+    g_last_error = "NCCL communicator aborted after an asynchronous error";
+    return ISING_ERR_NCCL;
+  }
   if (!h->comm) return ISING_OK;
   ncclResult_t ae = ncclSuccess;
   NC(ncclCommGetAsyncError(h->comm, &ae));
   if (ae != ncclSuccess && ae != ncclInProgress) {
     const int st = fail_nccl(ae, "NCCL asynchronous error (communicator aborted)", __LINE__);
-    ncclCommAbort(h->comm);
+    ncclCommAbort(h->comm);  // frees the communicator; the handle is unusable from here on
     h->comm = nullptr;
+    h->comm_aborted = true;
     return st;
   }
   return ISING_OK;
@@ -673,7 +681,7 @@ int nccl_poll(ising_ctx* h) {
 int wait_stream(ising_ctx* h, cudaStream_t st) {
   if (!h->comm) {
     CU(cudaStreamSynchronize(st));
-    return ISING_OK;
+    return h->comm_aborted ? nccl_poll(h) : ISING_OK;
   }
   for (;;) {
     const cudaError_t e = cudaStreamQuery(st);
@@ -1907,6 +1915,7 @@ int ising_write_lattice_bits(ising_t h, const uint8_t* in, int64_t in_len, uint6
 
 int ising_sweep(ising_t h, int64_t n) {
   if (!h || n < 0) return ISING_ERR_ARG;
+  if (h->comm_aborted) return nccl_poll(h);
   if (!h->beta_set || !h->state_set) return ISING_ERR_STATE;
   if (h->p2p && h->world > 1 && !h->connected) return ISING_ERR_STATE;
   if (h->t + (uint64_t)n > 0xffffffffull) return ISING_ERR_RANGE;
@@ -2016,6 +2025,7 @@ int ising_read_rows(ising_t h, int64_t row_begin, int64_t nrows, int8_t* out, in
 
 int ising_observables(ising_t h, int64_t* up_count, int64_t* bond_energy) {
   if (!h || !up_count || !bond_energy) return ISING_ERR_ARG;
+  if (h->comm_aborted) return nccl_poll(h);
   if (!h->state_set) return ISING_ERR_STATE;
   if (h->basic) return basic_observables(h, up_count, bond_energy);
   TRY(p2p_wait(h));  // the neighbours' last phase wrote this slab's white halo rows
