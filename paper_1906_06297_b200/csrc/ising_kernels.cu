@@ -523,45 +523,6 @@ __device__ __forceinline__ uint32_t sel1_half(uint32_t t, uint32_t n, uint32_t c
   return t ^ ((x >> 3) & kLane0);
 }
 
-// philox8 with round 1 precomputed by the caller: for counter {t, c1base + b, colour, row}
-// round 1 gives c0 = u0 ^ (c1base + b), c1 = l1, c2 = h0 ^ row, c3 = l0, with
-// u0 = hi(M1 colour) ^ k0[0], l1 = lo(M1 colour), h0 = hi(M0 t) ^ k1[0], l0 = lo(M0 t) — values a
-// caller whose t and colour vary per work item (k_sweeps_wavefront) computes once per item.
-struct PhiloxRound1 {
-  uint32_t u0, l1, h0, l0;
-};
-__device__ __forceinline__ PhiloxRound1 philox_round1(uint32_t t, uint32_t colour, const PhiloxKeys& K) {
-  const uint64_t p0 = (uint64_t)t * kPhiloxM0, p1 = (uint64_t)colour * kPhiloxM1;
-  return {(uint32_t)(p1 >> 32) ^ K.k0[0], (uint32_t)p1, (uint32_t)(p0 >> 32) ^ K.k1[0], (uint32_t)p0};
-}
-__device__ __forceinline__ void philox8_r1(const PhiloxRound1& q, uint32_t c1base, uint32_t row,
-                                           const PhiloxKeys& K, uint4 (&out)[8]) {
-  uint32_t c0[8], c1[8], c2[8], c3[8];
-#pragma unroll
-  for (int b = 0; b < 8; ++b) {
-    c0[b] = q.u0 ^ (c1base + b);
-    c1[b] = q.l1;
-    c2[b] = q.h0 ^ row;
-    c3[b] = q.l0;
-  }
-#pragma unroll
-  for (int r = 1; r < 10; ++r) {
-#pragma unroll
-    for (int b = 0; b < 8; ++b) {
-      const uint64_t p0 = (uint64_t)c0[b] * kPhiloxM0;
-      const uint64_t p1 = (uint64_t)c2[b] * kPhiloxM1;
-      const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1[b] ^ K.k0[r];
-      const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3[b] ^ K.k1[r];
-      c1[b] = (uint32_t)p1;
-      c3[b] = (uint32_t)p0;
-      c0[b] = n0;
-      c2[b] = n2;
-    }
-  }
-#pragma unroll
-  for (int b = 0; b < 8; ++b) out[b] = make_uint4(c0[b], c1[b], c2[b], c3[b]);
-}
-
 // NB Philox blocks (counter word 1 = c1base + b) advanced in lockstep: philox8's form for
 // the four blocks of one word.
 template <int NB>
@@ -1345,220 +1306,6 @@ cudaError_t launch_halfsweep_staged(int rule, int64_t slots, cudaStream_t st, Ha
   });
 }
 
-// ------------------------------------------------------- temporally fused sweeps
-#ifndef ISING_WF_RELEASE
-#define ISING_WF_RELEASE 1
-#endif
-#ifndef ISING_WF_LAG_MUL
-#define ISING_WF_LAG_MUL 3  // lag = window * MUL / 2 + 2 ticks
-#endif
-#ifndef ISING_WF_STATIC
-#define ISING_WF_STATIC 1
-#endif
-
-__device__ __forceinline__ void spin_until_u32(const unsigned int* flag, unsigned int v) {
-  unsigned long long t0 = 0;
-  for (;;) {
-    unsigned int x;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(x) : "l"(flag) : "memory");
-    if (x >= v) return;
-    __nanosleep(32);
-    const unsigned long long now = global_ns();
-    if (t0 == 0) t0 = now;
-    if (now - t0 > 30000000000ull) {
-      printf("ising: wavefront dependency wait timed out (counter %u, want %u)\n", x, v);
-      __trap();
-    }
-  }
-}
-
-template <int RULE>
-__global__ void __launch_bounds__(kStageThreads, staged_minb(RULE))
-    k_sweeps_wavefront(const WavefrontParams P) {
-  constexpr int kRows = stage_rows(RULE);
-  __shared__ alignas(128) uint64_t tile[kRows + 2][kStageWords];
-  __shared__ uint64_t edge[kRows + 2][2];
-  __shared__ alignas(8) uint64_t mbar;
-  __shared__ long long s_item;
-  const int64_t W = P.ph[0].W;
-  const int bpr = (int)(W / kStageWords);
-  const int R = P.ph[0].R;
-  const int64_t per_tick = 2 * (int64_t)bpr;
-  const int64_t nbn = (int64_t)P.nb * P.n;  // band-phases per colour in this launch
-  const uint32_t bar = smem_u32(&mbar);
-  const int tid = threadIdx.x;
-  if (tid == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  uint32_t parity = 0;
-#if ISING_WF_STATIC
-  // static round-robin assignment (co-resident grid: cooperative launch): item k of this block
-  // is blockIdx.x + k gridDim.x; every item waits only on items with smaller indices, which
-  // their blocks reach first, so progress is guaranteed without a shared fetch counter
-  for (long long item = blockIdx.x; item < P.total; item += gridDim.x) {
-#else
-  for (;;) {
-    if (tid == 0) s_item = (long long)atomicAdd(P.next_item, 1ull);
-    __syncthreads();
-    // broadcast from lane 0 so the compiler can treat the item — and the sweep, colour and
-    // row derived from it — as warp-uniform (uniform datapath for the Philox words that do not
-    // vary across the warp, as in the per-phase kernel)
-    const long long item = (long long)__reduce_max_sync(0xffffffffu, (unsigned int)s_item);
-    __syncthreads();  // s_item is rewritten by the next fetch
-    if (item >= P.total) break;
-#endif
-    const int64_t tick = item / per_tick;
-    const int rem = (int)(item - tick * per_tick);
-    const int c = rem >= bpr ? 1 : 0;
-    const int span = c ? rem - bpr : rem;
-    const int64_t j = c ? tick - P.lag : tick;
-    if (j < 0 || j >= nbn) continue;  // the white front's lead-in / the black front's run-out
-    const int s = (int)(j / P.nb);
-    const int b = (int)(j - (int64_t)s * P.nb);
-    // colour-dependent pointers by select; keys, thresholds and flags from ph[0] (identical for
-    // both colours) so the Philox / acceptance code keeps constant-bank operands at fixed
-    // offsets instead of indexed loads
-    const HalfSweepParams& p = P.ph[0];
-    const uint64_t* src_plane = c ? P.ph[1].src : P.ph[0].src;
-    uint64_t* tgt_plane = c ? P.ph[1].tgt : P.ph[0].tgt;
-    uint64_t* halo_up = c ? P.ph[1].halo_up : P.ph[0].halo_up;
-    uint64_t* halo_dn = c ? P.ph[1].halo_dn : P.ph[0].halo_dn;
-    const uint32_t colour = (uint32_t)c;
-    // black (s, b) reads the white rows of bands b-1 .. b+1 written in sweep s - 1 and
-    // overwrites black rows they read; white (s, b) likewise against black of sweep s
-    if (tid == 0) {
-      const unsigned int need = (unsigned int)((c == 0 ? s : s + 1) * bpr);
-      const unsigned int* d = P.done + (1 - c) * P.nb;
-      const int bm = b == 0 ? P.nb - 1 : b - 1, bp = b == P.nb - 1 ? 0 : b + 1;
-      // the three counters read together (one round trip); the usual case is done
-      unsigned int x0, x1, x2;
-      asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(x0) : "l"(d + bm) : "memory");
-      asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(x1) : "l"(d + b) : "memory");
-      asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(x2) : "l"(d + bp) : "memory");
-      if (min(x0, min(x1, x2)) < need) {
-        spin_until_u32(d + bm, need);
-        spin_until_u32(d + b, need);
-        spin_until_u32(d + bp, need);
-      }
-      asm volatile("fence.acq_rel.gpu;" ::: "memory");  // the relaxed reads become acquire
-      // other blocks wrote those rows with generic stores; the bulk copies read them through
-      // the async proxy
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-    }
-    __syncthreads();
-    const int ra = b * kRows;
-    const int rb = min(ra + kRows, R);
-    const int nrows = rb - ra;
-    const int64_t w0 = (int64_t)span * kStageWords;
-    const uint64_t* src = src_plane + W;
-    if (tid == 0) {
-      const uint32_t bytes = (uint32_t)(nrows + 2) * kStageWords * 8;
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
-                   : "memory");
-      for (int rr = 0; rr < nrows + 2; ++rr) {
-        const uint64_t* g = src + (int64_t)(ra - 1 + rr) * W + w0;
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-            ::"r"(smem_u32(&tile[rr][0])), "l"(g), "r"((uint32_t)(kStageWords * 8)), "r"(bar)
-            : "memory");
-      }
-    }
-    if (tid >= 32 && tid < 32 + 2 * nrows) {
-      const int e = tid - 32;
-      const int rr = e >> 1;
-      const int64_t col = (e & 1) ? ((w0 + kStageWords == W) ? 0 : w0 + kStageWords)
-                                  : ((w0 == 0) ? W - 1 : w0 - 1);
-      edge[rr + 1][e & 1] =
-          __ldcg(reinterpret_cast<const unsigned long long*>(src + (int64_t)(ra + rr) * W + col));
-    }
-    __syncthreads();
-    {
-      uint32_t ready = 0;
-      while (!ready)
-        asm volatile(
-            "{\n\t.reg .pred q;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, q;\n\t}"
-            : "=r"(ready)
-            : "r"(bar), "r"(parity)
-            : "memory");
-    }
-    parity ^= 1u;
-    const uint32_t t = P.t0 + (uint32_t)s + 1u;
-    const PhiloxRound1 q1 = philox_round1(t, colour, p.keys);  // once per item
-    const int64_t wc = w0 + 2 * tid;
-    uint64_t* tp = tgt_plane + W + (int64_t)ra * W + wc;
-    for (int rr = 0; rr < nrows; ++rr, tp += W) {
-      const int r = ra + rr;
-      const int64_t gi = p.row0 + r;
-      const bool west = ((gi & 1) == 0) == (colour == 0);
-      const uint64_t n0 = tile[rr][2 * tid], n1 = tile[rr][2 * tid + 1];
-      const uint64_t c0 = tile[rr + 1][2 * tid], c1 = tile[rr + 1][2 * tid + 1];
-      const uint64_t s0 = tile[rr + 2][2 * tid], s1 = tile[rr + 2][2 * tid + 1];
-      uint64_t side0, side1;
-      if (west) {
-        const uint64_t wl = tid == 0 ? edge[rr + 1][0] : tile[rr + 1][2 * tid - 1];
-        side0 = splice_west(c0, wl);
-        side1 = splice_west(c1, c0);
-      } else {
-        const uint64_t er = tid == kStageThreads - 1 ? edge[rr + 1][1] : tile[rr + 1][2 * tid + 2];
-        side0 = splice_east(c0, c1);
-        side1 = splice_east(c1, er);
-      }
-      ulonglong2 tv = __ldcg(reinterpret_cast<const ulonglong2*>(tp));
-      const uint32_t ctr0 = (uint32_t)(4 * wc);
-      if constexpr (lockstep_rule(RULE)) {
-        uint4 rbk[8];
-        philox8_r1(q1, ctr0, (uint32_t)gi, p.keys, rbk);
-        tv.x = word_from_draws<RULE>(tv.x, n0, c0, s0, side0, rbk, p);
-        tv.y = word_from_draws<RULE>(tv.y, n1, c1, s1, side1, rbk + 4, p);
-      } else {
-        tv.x = update_word<RULE>(tv.x, n0, c0, s0, side0, ctr0, (uint32_t)gi, t, P.ph[c]);
-        tv.y = update_word<RULE>(tv.y, n1, c1, s1, side1, ctr0 + 4, (uint32_t)gi, t, P.ph[c]);
-      }
-      *reinterpret_cast<ulonglong2*>(tp) = tv;
-      if (r == 0) *reinterpret_cast<ulonglong2*>(halo_up + wc) = tv;
-      if (r == R - 1) *reinterpret_cast<ulonglong2*>(halo_dn + wc) = tv;
-    }
-    __syncthreads();  // every thread's stores issued and its tile reads done
-    if (tid == 0) {
-#if ISING_WF_RELEASE == 0
-      __threadfence();  // release: this band's stores before the count
-      atomicAdd(P.done + c * P.nb + b, 1u);
-#elif ISING_WF_RELEASE == 1
-      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(P.done + c * P.nb + b) : "memory");
-#elif ISING_WF_RELEASE == 2
-      asm volatile("fence.acq_rel.gpu;" ::: "memory");
-      atomicAdd(P.done + c * P.nb + b, 1u);
-#else  // measurement only: no release (not a correct protocol)
-      atomicAdd(P.done + c * P.nb + b, 1u);
-#endif
-    }
-  }
-}
-
-int wavefront_band_rows(int rule) { return stage_rows(rule); }
-
-cudaError_t launch_wavefront(int rule, int grid, cudaStream_t st, const WavefrontParams& P) {
-  return dispatch_rule(rule, false, [&](auto R, auto) {
-#if ISING_WF_STATIC
-    void* args[] = {const_cast<WavefrontParams*>(&P)};
-    return cudaLaunchCooperativeKernel((const void*)k_sweeps_wavefront<decltype(R)::value>,
-                                       dim3(grid), dim3(kStageThreads), args, 0, st);
-#else
-    k_sweeps_wavefront<decltype(R)::value><<<grid, kStageThreads, 0, st>>>(P);
-    return cudaGetLastError();
-#endif
-  });
-}
-
-cudaError_t wavefront_occupancy(int* blocks_per_sm) {
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_sweeps_wavefront<0>,
-                                                       kStageThreads, 0);
-}
-
 cudaError_t staged_occupancy(int* blocks_per_sm) {
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_halfsweep_staged<0>,
                                                        kStageThreads, 0);
@@ -1917,7 +1664,6 @@ static cudaError_t preload_rule() {
   if ((e = cudaFuncGetAttributes(&a, k_halfsweep<R, false>)) != cudaSuccess) return e;
   if ((e = cudaFuncGetAttributes(&a, k_halfsweep<R, true>)) != cudaSuccess) return e;
   if ((e = cudaFuncGetAttributes(&a, k_halfsweep_staged<R, false>)) != cudaSuccess) return e;
-  if ((e = cudaFuncGetAttributes(&a, k_sweeps_wavefront<R>)) != cudaSuccess) return e;
   return cudaFuncGetAttributes(&a, k_halfsweep_staged<R, true>);
 }
 

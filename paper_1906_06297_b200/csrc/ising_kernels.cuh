@@ -90,26 +90,6 @@ struct PersistentParams {
   uint32_t every;
 };
 
-// Temporally fused sweeps for one large slab (k_sweeps_wavefront): work item = (band of
-// stage_rows rows, 256-word span) of one colour phase; items are taken in a fixed order from a
-// global counter — tick j holds the black items of band j (mod nb) and the white items of band
-// j - lag — and each waits only for the three neighbouring bands of the other colour
-// (done[] counters, acquire / release), so consecutive phases and sweeps overlap with no
-// kernel boundary and no grid barrier.
-struct WavefrontParams {
-  HalfSweepParams ph[2];           // black and white phase parameters (one slab, own halos)
-  uint32_t t0;                     // sweeps t0 + 1 .. t0 + n
-  uint32_t n;
-  int32_t nb;                      // bands per phase
-  int32_t lag;                     // white front behind the black front, in bands
-  long long total;                 // items (including the empty ones of the first / last ticks)
-  unsigned long long* next_item;   // zeroed before the launch
-  unsigned int* done;              // [2][nb] completed spans per band, zeroed before the launch
-};
-cudaError_t launch_wavefront(int rule, int grid, cudaStream_t st, const WavefrontParams& P);
-cudaError_t wavefront_occupancy(int* blocks_per_sm);
-int wavefront_band_rows(int rule);
-
 // Rank-p2p synchronisation helpers (one thread each).
 struct SyncParams {
   const unsigned long long* wait_flags;  // spin until all wait_count flags >= wait_value

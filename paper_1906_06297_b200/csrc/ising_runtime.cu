@@ -135,7 +135,6 @@ struct Device {
   int sms = 0;
   int hs_blocks_per_sm = 0;  // occupancy of k_halfsweep<0>
   int staged_blocks_per_sm = 0;  // occupancy of k_halfsweep_staged<0>
-  int wavefront_blocks_per_sm = 0;  // occupancy of k_sweeps_wavefront<0>
   cudaStream_t stream = nullptr;
   cudaStream_t comm = nullptr;
   cudaEvent_t ev_phase = nullptr;  // end of the latest phase on this device
@@ -238,11 +237,6 @@ struct ising_ctx {
   // staged kernel: white phases walk the bands bottom-up (ISING_MIRROR=0: off); C3 1552 ->
   // 1567, 16384 x 32768 1515 -> 1542 flips/ns (profiles/r02_ncu_halfsweep.md)
   bool mirror = !env_is_zero("ISING_MIRROR");
-  // one slab on one device, widths of the staged kernel, enough bands: sweeps run as one
-  // temporally fused launch (k_sweeps_wavefront; ISING_WAVEFRONT=0: per-phase launches)
-  bool wavefront = env_is_one("ISING_WAVEFRONT");  // opt-in: measured slower (see profiles)
-  unsigned long long* wf_buf = nullptr;  // [0] item counter, then 2 * nb uint32 done counters
-  size_t wf_bytes = 0;
   // heat-bath variant 7 (ISING_HB_SYMMETRIC=0: off, for every handle type)
   bool symmetric_hb_enabled = !env_is_zero("ISING_HB_SYMMETRIC");
   bool draw_free_enabled = true;           // beta in {0, inf}: skip Philox (ISING_DRAW_FREE=0)
@@ -366,8 +360,6 @@ int setup_device(Device& d, int dev) {
   if (d.hs_blocks_per_sm < 1) d.hs_blocks_per_sm = 1;
   CU(staged_occupancy(&d.staged_blocks_per_sm));
   if (d.staged_blocks_per_sm < 1) d.staged_blocks_per_sm = 1;
-  CU(wavefront_occupancy(&d.wavefront_blocks_per_sm));
-  if (d.wavefront_blocks_per_sm < 1) d.wavefront_blocks_per_sm = 1;
   {  // once per device and process (see preload_kernels)
     static std::mutex mu;
     static std::vector<bool> loaded;
@@ -561,7 +553,6 @@ void destroy_ctx(ising_ctx* h) {
   if (h->t_dev) cudaFree(h->t_dev);
   if (h->gexec_meas) cudaGraphExecDestroy(h->gexec_meas);
   if (h->bar) cudaFree(h->bar);
-  if (h->wf_buf) cudaFree(h->wf_buf);
   delete h;
 }
 
@@ -1159,93 +1150,8 @@ int run_persistent(ising_ctx* h, int64_t n, unsigned long long* obs_base, int64_
 // Enqueue sweeps t+1 .. t+n on the handle's streams (no synchronisation); t += n.  With
 // obs (LOCAL mode), the white phase of sweep t+n also reduces the observables of the state
 // it produces into obs[device][0..1] (fused; no extra pass).
-// Temporally fused sweeps (k_sweeps_wavefront): geometry, eligibility and launch.  The white
-// front trails the black one (and the next sweep's black front the white one) by `lag` bands,
-// more than the items in flight (one per resident block), so an item's three neighbour bands
-// of the other colour are normally complete when it is taken and its wait is a single check.
-struct WavefrontGeometry {
-  int bpr = 0, nb = 0, lag = 0, grid = 0;
-};
-
-bool wavefront_geometry(const ising_ctx* h, WavefrontGeometry* g) {
-  if (!h->wavefront || h->rank_mode || h->basic || h->devs.size() != 1 || h->slabs.size() != 1 ||
-      !h->staged || h->W % kStageWords != 0)
-    return false;
-  const Device& d = h->devs[0];
-  const Slab& s = h->slabs[0];
-  const int rows = wavefront_band_rows(kernel_variant(h));
-  g->bpr = (int)(h->W / kStageWords);
-  g->nb = (int)((s.R + rows - 1) / rows);
-  g->grid = d.sms * d.wavefront_blocks_per_sm;
-  const int window = (g->grid + 2 * g->bpr - 1) / (2 * g->bpr);  // ticks in flight
-#ifndef ISING_WF_LAG_MUL
-#define ISING_WF_LAG_MUL 3
-#endif
-  g->lag = window * ISING_WF_LAG_MUL / 2 + 2;
-  return g->nb >= 2 * g->lag + window;
-}
-
-int run_wavefront(ising_ctx* h, int64_t n, const WavefrontGeometry& g) {
-  Device& d = h->devs[0];
-  Slab& s = h->slabs[0];
-  CU(cudaSetDevice(d.dev));
-  const size_t bytes = sizeof(unsigned long long) + 2 * sizeof(unsigned int) * (size_t)g.nb;
-  if (h->wf_bytes < bytes) {
-    if (h->wf_buf) CU(cudaFree(h->wf_buf));
-    h->wf_buf = nullptr;
-    h->wf_bytes = 0;
-    CU(cudaMalloc(&h->wf_buf, bytes));
-    h->wf_bytes = bytes;
-  }
-  CU(cudaMemsetAsync(h->wf_buf, 0, bytes, d.stream));
-  WavefrontParams P{};
-  for (int c = 0; c < 2; ++c) {
-    HalfSweepParams& p = P.ph[c];
-    p.tgt = s.plane[c];
-    p.src = s.plane[1 - c];
-    p.halo_up = s.plane[c] + (s.R + 1) * h->W;  // one slab: its own halo rows
-    p.halo_dn = s.plane[c];
-    p.W = h->W;
-    p.row0 = s.row0;
-    p.R = (int32_t)s.R;
-    p.r_begin = 0;
-    p.r_end = (int32_t)s.R;
-    p.colour = (uint32_t)c;
-    p.keys = h->keys;
-    p.acc = h->acc;
-  }
-  P.t0 = (uint32_t)h->t;
-  P.n = (uint32_t)n;
-  P.nb = g.nb;
-  P.lag = g.lag;
-  P.total = ((long long)n * g.nb + g.lag) * 2 * g.bpr;
-  P.next_item = h->wf_buf;
-  P.done = reinterpret_cast<unsigned int*>(h->wf_buf + 1);
-  const bool prof = h->prof_active && (size_t)(2 * h->kernel_launches + 1) < h->prof_events.size();
-  if (prof) CU(cudaEventRecord(h->prof_events[2 * h->kernel_launches], d.stream));
-  CU(launch_wavefront(kernel_variant(h), g.grid, d.stream, P));
-  if (prof) {
-    CU(cudaEventRecord(h->prof_events[2 * h->kernel_launches + 1], d.stream));
-    ++h->kernel_launches;
-  }
-  ++h->launch_count;
-  h->t += (uint64_t)n;
-  return ISING_OK;
-}
-
 int enqueue_sweeps(ising_ctx* h, int64_t n, const std::vector<unsigned long long*>* obs = nullptr) {
   if (n > 0 && persistent_eligible(h)) return run_persistent(h, n, obs ? (*obs)[0] : nullptr, n);
-  WavefrontGeometry wg;
-  const int64_t n_fused = obs ? n - 1 : n;  // a measured sweep is launched by phases
-  if (n_fused > 0 && wavefront_geometry(h, &wg)) {
-    TRY(run_wavefront(h, n_fused, wg));
-    if (!obs) return ISING_OK;
-    h->t -= (uint64_t)n_fused;  // (the phase loop below counts from the enqueue's base)
-    for (int c = 0; c < 2; ++c)
-      TRY(phase_local(h, c, (uint32_t)(h->t + (uint64_t)n), false, obs));
-    h->t += (uint64_t)n;
-    return ISING_OK;
-  }
   int64_t k0 = 1;
   const int64_t n_graph = obs ? n - 1 : n;  // the measured sweep is launched directly
   if (graph_eligible(h) && n_graph >= kGraphSweeps) {
