@@ -412,60 +412,9 @@ __device__ __forceinline__ uint64_t update_word<1>(uint64_t tgt, uint64_t n, uin
 #ifndef ISING_PROBE8
 #define ISING_PROBE8 1  // the probe advances eight blocks in lockstep, like the kernels (1899 -> 2005 draws/ns)
 #endif
-// Experiment (ISING_R2DECOMP): the second round's only per-thread product, M0 x c0, has
-// c0 = U ^ (c1base + b) with U warp-uniform and c1base a multiple of 8 (b = 0..7), so
-// c0 = Y + d_b with Y = c1base ^ (U & ~7) per thread and d_b = (b ^ U) & 7 warp-uniform:
-// M0 c0 = M0 Y + M0 d_b — one IMAD.WIDE and eight 64-bit adds of uniform constants instead of
-// eight IMAD.WIDE (exact: same 64-bit products).
-#ifndef ISING_R2DECOMP
-#define ISING_R2DECOMP 0
-#endif
 __device__ __forceinline__ void philox8(uint32_t t, uint32_t c1base, uint32_t colour, uint32_t row,
                                         const PhiloxKeys& K, uint4 (&out)[8]) {
   uint32_t c0[8], c1[8], c2[8], c3[8];
-#if ISING_R2DECOMP
-  {
-    const uint64_t p0u = (uint64_t)t * kPhiloxM0, p1u = (uint64_t)colour * kPhiloxM1;  // round 1
-    const uint32_t U = (uint32_t)(p1u >> 32) ^ K.k0[0];  // round-1 c0 = U ^ (c1base + b)
-    const uint32_t c1u = (uint32_t)p1u;
-    const uint32_t c2u = (uint32_t)(p0u >> 32) ^ row ^ K.k1[0];
-    const uint32_t c3u = (uint32_t)p0u;
-    const uint64_t q1 = (uint64_t)c2u * kPhiloxM1;  // round 2, uniform product
-    const uint32_t n0 = (uint32_t)(q1 >> 32) ^ c1u ^ K.k0[1];
-    const uint64_t Q = (uint64_t)(c1base ^ (U & ~7u)) * kPhiloxM0;  // round 2, per thread
-#pragma unroll
-    for (int b = 0; b < 8; ++b) {
-      const uint64_t C = (uint64_t)((b ^ U) & 7u) * kPhiloxM0;  // warp-uniform
-      uint64_t P;  // Q + C as two ALU adds (ptxas would re-fuse a plain add into IMAD.WIDE)
-      asm("{\n\t.reg .u32 ql, qh, cl, ch, pl, ph;\n\t"
-          "mov.b64 {ql, qh}, %1;\n\tmov.b64 {cl, ch}, %2;\n\t"
-          "add.cc.u32 pl, ql, cl;\n\taddc.u32 ph, qh, ch;\n\t"
-          "mov.b64 %0, {pl, ph};\n\t}"
-          : "=l"(P)
-          : "l"(Q), "l"(C));
-      c0[b] = n0;
-      c1[b] = (uint32_t)q1;
-      c2[b] = (uint32_t)(P >> 32) ^ c3u ^ K.k1[1];
-      c3[b] = (uint32_t)P;
-    }
-  }
-#pragma unroll
-  for (int r = 2; r < 10; ++r) {
-#pragma unroll
-    for (int b = 0; b < 8; ++b) {
-      const uint64_t p0 = (uint64_t)c0[b] * kPhiloxM0;
-      const uint64_t p1 = (uint64_t)c2[b] * kPhiloxM1;
-      const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1[b] ^ K.k0[r];
-      const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3[b] ^ K.k1[r];
-      c1[b] = (uint32_t)p1;
-      c3[b] = (uint32_t)p0;
-      c0[b] = n0;
-      c2[b] = n2;
-    }
-  }
-#pragma unroll
-  for (int b = 0; b < 8; ++b) out[b] = make_uint4(c0[b], c1[b], c2[b], c3[b]);
-#else
 #pragma unroll
   for (int b = 0; b < 8; ++b) {
     c0[b] = t;
@@ -489,69 +438,6 @@ __device__ __forceinline__ void philox8(uint32_t t, uint32_t c1base, uint32_t co
   }
 #pragma unroll
   for (int b = 0; b < 8; ++b) out[b] = make_uint4(c0[b], c1[b], c2[b], c3[b]);
-#endif
-}
-
-// Experiment (ISING_SEL1): one compare per lane against the threshold the lane's class needs.
-// With b = anti-aligned neighbours, flip iff b >= 2, or b = 1 and r < T3, or b = 0 and r < T4;
-// with thr = (b >= 1 ? T3 : T4) and c = [r >= thr], that is b - 2c >= 0 for every b.  One
-// compare and one insert per lane (plus the threshold select) instead of two of each.
-#ifndef ISING_SEL1
-#define ISING_SEL1 0
-#endif
-__device__ __forceinline__ void c_step(uint32_t& a, uint32_t r, uint32_t thr) {
-  asm("{\n\t.reg .u32 d;\n\t"
-      "sub.cc.u32 d, %1, %2;\n\t"
-      "madc.lo.u32 %0, %0, 16, 0;\n\t}"
-      : "+r"(a)
-      : "r"(r), "r"(thr));
-}
-
-__device__ __forceinline__ uint32_t sel1_half(uint32_t t, uint32_t n, uint32_t c, uint32_t s,
-                                              uint32_t side, const uint32_t (&d)[8], uint32_t t3,
-                                              uint32_t t4) {
-  const uint32_t b = anti8(t, n, c, s, side);  // 0..4 per lane
-  const uint32_t y = b + 0x77777777u;          // bit 3 of a lane: b >= 1
-  uint32_t acc = 0;
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {  // d[q] serves lane 7 - q (descending Horner order)
-    const int lane = 7 - q;
-    const uint32_t thr = (y >> (4 * lane + 3)) & 1u ? t3 : t4;
-    c_step(acc, d[q], thr);
-  }
-  const uint32_t x = b + 0x88888888u - (acc << 1);
-  return t ^ ((x >> 3) & kLane0);
-}
-
-// NB Philox blocks (counter word 1 = c1base + b) advanced in lockstep: philox8's form for
-// the four blocks of one word.
-template <int NB>
-__device__ __forceinline__ void philox_n(uint32_t t, uint32_t c1base, uint32_t colour, uint32_t row,
-                                         const PhiloxKeys& K, uint4 (&out)[NB]) {
-  uint32_t c0[NB], c1[NB], c2[NB], c3[NB];
-#pragma unroll
-  for (int b = 0; b < NB; ++b) {
-    c0[b] = t;
-    c1[b] = c1base + b;
-    c2[b] = colour;
-    c3[b] = row;
-  }
-#pragma unroll
-  for (int r = 0; r < 10; ++r) {
-#pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      const uint64_t p0 = (uint64_t)c0[b] * kPhiloxM0;
-      const uint64_t p1 = (uint64_t)c2[b] * kPhiloxM1;
-      const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1[b] ^ K.k0[r];
-      const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3[b] ^ K.k1[r];
-      c1[b] = (uint32_t)p1;
-      c3[b] = (uint32_t)p0;
-      c0[b] = n0;
-      c2[b] = n2;
-    }
-  }
-#pragma unroll
-  for (int b = 0; b < NB; ++b) out[b] = make_uint4(c0[b], c1[b], c2[b], c3[b]);
 }
 
 // Metropolis (RULE 0) acceptance of one word from its four precomputed blocks rb[0..3]
@@ -560,32 +446,6 @@ template <int RULE>
 __device__ __forceinline__ uint64_t metropolis_from_draws(uint64_t tgt, uint64_t n, uint64_t c,
                                                           uint64_t s, uint64_t side,
                                                           const uint4* rb, const HalfSweepParams& p) {
-#if ISING_SEL1 == 1
-  if constexpr (RULE == 0) {
-    const uint32_t dl[8] = {rb[1].w, rb[1].z, rb[1].y, rb[1].x, rb[0].w, rb[0].z, rb[0].y, rb[0].x};
-    const uint32_t dh[8] = {rb[3].w, rb[3].z, rb[3].y, rb[3].x, rb[2].w, rb[2].z, rb[2].y, rb[2].x};
-    const uint32_t lo = sel1_half((uint32_t)tgt, (uint32_t)n, (uint32_t)c, (uint32_t)s,
-                                  (uint32_t)side, dl, p.acc.thr[3], p.acc.thr[4]);
-    const uint32_t hi = sel1_half((uint32_t)(tgt >> 32), (uint32_t)(n >> 32), (uint32_t)(c >> 32),
-                                  (uint32_t)(s >> 32), (uint32_t)(side >> 32), dh, p.acc.thr[3],
-                                  p.acc.thr[4]);
-    return ((uint64_t)hi << 32) | lo;
-  }
-#elif ISING_SEL1 == 2  // the low half of each word only (the balance point between the pipes)
-  if constexpr (RULE == 0) {
-    const uint32_t dl[8] = {rb[1].w, rb[1].z, rb[1].y, rb[1].x, rb[0].w, rb[0].z, rb[0].y, rb[0].x};
-    const uint32_t dh[8] = {rb[3].w, rb[3].z, rb[3].y, rb[3].x, rb[2].w, rb[2].z, rb[2].y, rb[2].x};
-    const uint32_t lo = sel1_half((uint32_t)tgt, (uint32_t)n, (uint32_t)c, (uint32_t)s,
-                                  (uint32_t)side, dl, p.acc.thr[3], p.acc.thr[4]);
-    const uint32_t sum_hi =
-        (uint32_t)(n >> 32) + (uint32_t)(c >> 32) + (uint32_t)(s >> 32) + (uint32_t)(side >> 32);
-    uint32_t a3hi = 0, a4hi = 0;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) nc_step(a3hi, a4hi, dh[q], p.acc.thr[3], p.acc.thr[4]);
-    const uint32_t hi = accept8((uint32_t)(tgt >> 32), sum_hi, a3hi + a4hi);
-    return ((uint64_t)hi << 32) | lo;
-  }
-#endif
   const uint32_t sum_lo = (uint32_t)n + (uint32_t)c + (uint32_t)s + (uint32_t)side;
   const uint32_t sum_hi =
       (uint32_t)(n >> 32) + (uint32_t)(c >> 32) + (uint32_t)(s >> 32) + (uint32_t)(side >> 32);
@@ -1026,9 +886,6 @@ constexpr int kRowUnroll = ISING_ROW_UNROLL;  // staged row loop unroll factor
 #ifndef ISING_STAGED_MINB
 #define ISING_STAGED_MINB 3
 #endif
-#ifndef ISING_PIPE
-#define ISING_PIPE 0
-#endif
 #ifndef ISING_STAGED_MINB_DRAWFREE
 #define ISING_STAGED_MINB_DRAWFREE 4
 #endif
@@ -1157,48 +1014,6 @@ __global__ void __launch_bounds__(kStageThreads, staged_minb(RULE)) k_halfsweep_
   const int64_t wc = w0 + 2 * tid;
   uint32_t obs_up = 0, obs_anti = 0;
   uint64_t* tp = tgt + (int64_t)ra * W + wc;  // target chunk of row r, advanced by W per row
-#if ISING_PIPE
-  // Experiment: software-pipelined draws.  The four blocks of a row's second word are drawn
-  // while its first word is accepted, and the next row's first word while the second is
-  // accepted, so the Philox multiplies (FMA-heavy pipe) and the acceptance (ALU) of one warp
-  // interleave instead of alternating.
-  if constexpr (lockstep_rule(RULE)) {
-    uint4 d0[4];
-    philox_n<4>(t, (uint32_t)(4 * wc), p.colour, (uint32_t)(p.row0 + ra), p.keys, d0);
-    for (int rr = 0; rr < nrows; ++rr, tp += W) {
-      const int r = ra + rr;
-      const int64_t gi = p.row0 + r;
-      const bool west = ((gi & 1) == 0) == (p.colour == 0);
-      const uint64_t n0 = tile[rr][2 * tid], n1 = tile[rr][2 * tid + 1];
-      const uint64_t c0 = tile[rr + 1][2 * tid], c1 = tile[rr + 1][2 * tid + 1];
-      const uint64_t s0 = tile[rr + 2][2 * tid], s1 = tile[rr + 2][2 * tid + 1];
-      uint64_t side0, side1;
-      if (west) {
-        const uint64_t wl = tid == 0 ? edge[rr + 1][0] : tile[rr + 1][2 * tid - 1];
-        side0 = splice_west(c0, wl);
-        side1 = splice_west(c1, c0);
-      } else {
-        const uint64_t er = tid == kStageThreads - 1 ? edge[rr + 1][1] : tile[rr + 1][2 * tid + 2];
-        side0 = splice_east(c0, c1);
-        side1 = splice_east(c1, er);
-      }
-      ulonglong2 tv = __ldcg(reinterpret_cast<const ulonglong2*>(tp));
-      const uint32_t ctr0 = (uint32_t)(4 * wc);
-      uint4 d1[4];
-      philox_n<4>(t, ctr0 + 4, p.colour, (uint32_t)gi, p.keys, d1);
-      tv.x = word_from_draws<RULE>(tv.x, n0, c0, s0, side0, d0, p);
-      philox_n<4>(t, ctr0, p.colour, (uint32_t)(gi + 1), p.keys, d0);  // next row (last: unused)
-      tv.y = word_from_draws<RULE>(tv.y, n1, c1, s1, side1, d1, p);
-      *reinterpret_cast<ulonglong2*>(tp) = tv;
-      if (r == 0 && p.halo_up) *reinterpret_cast<ulonglong2*>(p.halo_up + wc) = tv;
-      if (r == p.R - 1 && p.halo_dn) *reinterpret_cast<ulonglong2*>(p.halo_dn + wc) = tv;
-      if (OBS) {
-        obs_word(tv.x, n0, c0, s0, side0, obs_up, obs_anti);
-        obs_word(tv.y, n1, c1, s1, side1, obs_up, obs_anti);
-      }
-    }
-  } else
-#endif
 #pragma unroll kRowUnroll
   for (int rr = 0; rr < nrows; ++rr, tp += W) {
     const int r = ra + rr;
