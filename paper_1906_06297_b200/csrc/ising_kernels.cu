@@ -1098,7 +1098,13 @@ cudaError_t launch_halfsweep_staged(int rule, int64_t slots, cudaStream_t st, Ha
   const int64_t per_wave = slots / spans;  // bands per wave
   // measured on C3 (profiles/r01_ncu_halfsweep.md): heights 8/4, 8/2, 4/2, 12/6 and one or
   // two waves each all land within 0.3 % of each other
-  constexpr int h1 = 8, h2 = 4, w1 = 1, w2 = 1;
+#ifndef ISING_TAIL_H1
+#define ISING_TAIL_H1 8
+#endif
+#ifndef ISING_TAIL_H2
+#define ISING_TAIL_H2 4
+#endif
+  constexpr int h1 = ISING_TAIL_H1, h2 = ISING_TAIL_H2, w1 = 1, w2 = 1;
   if (per_wave > 0 && bands * spans >= 3 * slots && bands * spans < 64 * slots) {
     const int64_t row4 = rows - (int64_t)h2 * w2 * per_wave;
     const int64_t row8 = ((row4 - (int64_t)h1 * w1 * per_wave) / kStageRows) * kStageRows;
