@@ -10,7 +10,7 @@ import os, sys, numpy as np
 sys.path.insert(0, os.environ["ROOT"])
 from paper_1906_06297_b200.ising import IsingLattice, ising_probe_philox
 import oracle
-N, M = 130, 192
+N, M = int(os.environ.get("PN", 130)), int(os.environ.get("PM", 8192))
 g = IsingLattice(N, M, 3).set_beta(0.4406868).init_random(); g.sweep(50)
 o = oracle.Lattice(N, M, 3).set_beta(0.4406868).init_random(); o.sweep(50)
 ok = np.array_equal(g.read_lattice(), o.full())
