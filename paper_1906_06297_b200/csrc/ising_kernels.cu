@@ -440,67 +440,6 @@ __device__ __forceinline__ void philox8(uint32_t t, uint32_t c1base, uint32_t co
   for (int b = 0; b < 8; ++b) out[b] = make_uint4(c0[b], c1[b], c2[b], c3[b]);
 }
 
-// Base-3 acceptance digits (RULE 0, staged kernel).  Per draw the two compares stay on the
-// carry chain, but both carries go into ONE three-input add, acc = 3 acc + [r >= T3] +
-// [r >= T4] (ptxas: IADD3.X acc, acc, acc, acc, P, P' — ALU pipe), instead of two nibble
-// inserts acc = 16 acc + carry (IMAD.X, FMA-heavy pipe, which the Philox multiplies
-// saturate).  The digit of a lane is nc = [r >= T3] + [r >= T4] in {0, 1, 2}; the four
-// digits of one Philox block (elements x, y, z, w = lanes 4q + 0..3, Horner order w z y x,
-// so element e has weight 3^e) form an index < 81 into a shared table of their nibble
-// patterns: b3tab[i] = sum_e digit_e(i) << 4e, b3tab[81 + i] = the same << 16.
-#ifndef ISING_B3
-#define ISING_B3 0  // measured slower (profiles/r02_ncu_halfsweep.md): off
-#endif
-constexpr int kB3Entries = 81;
-__device__ __forceinline__ void b3_step(uint32_t& acc, uint32_t r, uint32_t t3, uint32_t t4) {
-  asm("{\n\t.reg .u32 d, x;\n\t"
-      "sub.cc.u32 d, %1, %2;\n\t"
-      "addc.u32 x, %0, %0;\n\t"
-      "sub.cc.u32 d, %1, %3;\n\t"
-      "addc.u32 %0, x, %0;\n\t}"
-      : "+r"(acc)
-      : "r"(r), "r"(t3), "r"(t4));
-}
-__device__ __forceinline__ void b3_table_init(uint32_t* tab) {
-  for (int i = threadIdx.x; i < 2 * kB3Entries; i += blockDim.x) {
-    const int idx = i % kB3Entries;
-    uint32_t pat = 0;
-    for (int e = 0, v = idx; e < 4; ++e, v /= 3) pat |= (uint32_t)(v % 3) << (4 * e);
-    tab[i] = i < kB3Entries ? pat : pat << 16;
-  }
-}
-__device__ __forceinline__ uint32_t b3_index(const uint4& b, uint32_t zero, uint32_t t3, uint32_t t4) {
-  uint32_t acc = zero;
-  b3_step(acc, b.w, t3, t4);
-  b3_step(acc, b.z, t3, t4);
-  b3_step(acc, b.y, t3, t4);
-  b3_step(acc, b.x, t3, t4);
-  return acc;
-}
-__device__ __forceinline__ uint64_t metropolis_b3(uint64_t tgt, uint64_t n, uint64_t c, uint64_t s,
-                                                  uint64_t side, const uint4* rb,
-                                                  const HalfSweepParams& p, const uint32_t* tab) {
-  const uint32_t sum_lo = (uint32_t)n + (uint32_t)c + (uint32_t)s + (uint32_t)side;
-  const uint32_t sum_hi =
-      (uint32_t)(n >> 32) + (uint32_t)(c >> 32) + (uint32_t)(s >> 32) + (uint32_t)(side >> 32);
-  const uint32_t t3 = p.acc.thr[3], t4 = p.acc.thr[4], z = p.acc.zero;
-  const uint32_t i0 = b3_index(rb[0], z, t3, t4), i1 = b3_index(rb[1], z, t3, t4);
-  const uint32_t nclo = tab[i0] + tab[kB3Entries + i1];
-#if ISING_B3 == 2  // hybrid: the high half keeps the nibble inserts (balances the two pipes)
-  uint32_t a3hi = 0, a4hi = 0;
-  const uint32_t dh[8] = {rb[3].w, rb[3].z, rb[3].y, rb[3].x, rb[2].w, rb[2].z, rb[2].y, rb[2].x};
-#pragma unroll
-  for (int q = 0; q < 8; ++q) nc_step(a3hi, a4hi, dh[q], t3, t4);
-  const uint32_t nchi = a3hi + a4hi;
-#else
-  const uint32_t i2 = b3_index(rb[2], z, t3, t4), i3 = b3_index(rb[3], z, t3, t4);
-  const uint32_t nchi = tab[i2] + tab[kB3Entries + i3];
-#endif
-  const uint32_t lo = accept8((uint32_t)tgt, sum_lo, nclo);
-  const uint32_t hi = accept8((uint32_t)(tgt >> 32), sum_hi, nchi);
-  return ((uint64_t)hi << 32) | lo;
-}
-
 // Metropolis (RULE 0) acceptance of one word from its four precomputed blocks rb[0..3]
 // (block q serves lanes 4q .. 4q + 3), same Horner order as update_word_metropolis.
 template <int RULE>
@@ -982,10 +921,6 @@ __global__ void __launch_bounds__(kStageThreads, staged_minb(RULE)) k_halfsweep_
   __shared__ alignas(128) uint64_t tile[kRows + 2][kStageWords];
   __shared__ uint64_t edge[kRows + 2][2];
   __shared__ alignas(8) uint64_t mbar;
-#if ISING_B3
-  __shared__ uint32_t b3tab[RULE == 0 ? 2 * kB3Entries : 1];
-  if constexpr (RULE == 0) b3_table_init(b3tab);  // ordered by the start-up barrier below
-#endif
   const int64_t W = p.W;
   const int64_t bpr = W / kStageWords;  // blocks per band
   const int pband = (int)(blockIdx.x / bpr);
@@ -1103,16 +1038,8 @@ __global__ void __launch_bounds__(kStageThreads, staged_minb(RULE)) k_halfsweep_
     if constexpr (lockstep_rule(RULE)) {
       uint4 rb[8];
       philox8(t, ctr0, p.colour, (uint32_t)gi, p.keys, rb);
-#if ISING_B3
-      if constexpr (RULE == 0) {
-        tv.x = metropolis_b3(tv.x, n0, c0, s0, side0, rb, p, &b3tab[0]);
-        tv.y = metropolis_b3(tv.y, n1, c1, s1, side1, rb + 4, p, &b3tab[0]);
-      } else
-#endif
-      {
-        tv.x = word_from_draws<RULE>(tv.x, n0, c0, s0, side0, rb, p);
-        tv.y = word_from_draws<RULE>(tv.y, n1, c1, s1, side1, rb + 4, p);
-      }
+      tv.x = word_from_draws<RULE>(tv.x, n0, c0, s0, side0, rb, p);
+      tv.y = word_from_draws<RULE>(tv.y, n1, c1, s1, side1, rb + 4, p);
     } else
 #endif
     {

@@ -34,7 +34,6 @@ struct Accept {
   uint32_t always_mask;
   uint32_t keep3, keep4;  // Metropolis: 0 if T[a=3] / T[a=4] is 2^32, else ~0
   uint32_t nc_const;      // RULE 4: [r >= T3] + [r >= T4] per lane (draw-independent)
-  uint32_t zero;          // always 0: an accumulator start ptxas cannot constant-fold
 };
 
 struct HalfSweepParams {
