@@ -96,7 +96,9 @@ int ising_create_rank(ising_t* out, int64_t L_rows, int64_t L_cols, uint64_t see
  * "read access to the memory of the two GPUs that handle the slabs on top and bottom",
  * PAPER.md:227).  After creation every rank exports ising_ipc_handle, the caller
  * all-gathers the blobs in rank order (e.g. torch.distributed) and passes them to
- * ising_ipc_connect.  world <= 8.  Ranks may share a device (for testing).  With world == 1
+ * ising_ipc_connect.  world <= 8.  Ranks may share a device (for testing; the blobs carry the
+ * device UUID and ranks that share one run without programmatic dependent launch, as in
+ * ising_p2p_connect_local — under MPS their kernels run concurrently).  With world == 1
  * the rank is its own neighbour; ISING_SELF_EXCHANGE=1 in the environment makes it run the
  * whole flag protocol with itself (the protocol's per-GPU cost, measurable on one device). */
 #define ISING_IPC_BLOB_BYTES 256

@@ -118,6 +118,7 @@ struct IpcBlob {  // ising_ipc_handle payload (<= ISING_IPC_BLOB_BYTES)
   int64_t R, W;
   cudaIpcMemHandle_t plane[2];
   cudaIpcMemHandle_t sync;
+  unsigned char uuid[16];  // the exporting rank's GPU (ranks of several processes may share one)
 };
 static_assert(sizeof(IpcBlob) <= ISING_IPC_BLOB_BYTES, "IPC blob too large");
 
@@ -1643,6 +1644,9 @@ int ising_ipc_handle(ising_t h, void* blob, size_t len) {
   CU(cudaIpcGetMemHandle(&b.plane[0], h->slabs[0].plane[0]));
   CU(cudaIpcGetMemHandle(&b.plane[1], h->slabs[0].plane[1]));
   CU(cudaIpcGetMemHandle(&b.sync, h->sync));
+  cudaDeviceProp prop;
+  CU(cudaGetDeviceProperties(&prop, h->devs[0].dev));
+  memcpy(b.uuid, prop.uuid.bytes, sizeof b.uuid);
   memset(blob, 0, ISING_IPC_BLOB_BYTES);
   memcpy(blob, &b, sizeof b);
   return ISING_OK;
@@ -1662,6 +1666,11 @@ int ising_ipc_connect(ising_t h, const void* blobs, size_t len) {
       return ISING_ERR_ARG;
     }
   }
+  // Ranks of several processes on one GPU (testing; with MPS their kernels run concurrently):
+  // no programmatic dependent launch, for the reason given in ising_p2p_connect_local.
+  for (int r = 0; r < h->world; ++r)
+    if (r != h->rank && memcmp(all[r].uuid, all[h->rank].uuid, sizeof all[r].uuid) == 0)
+      h->pdl = false;
   for (int r = 0; r < h->world; ++r) {
     if (r == h->rank) {
       h->peer_sync[r] = h->sync;

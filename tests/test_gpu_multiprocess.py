@@ -71,6 +71,68 @@ def _worker(rank, world, port, N, M, seed, beta, plan, transport, q):
         dist.destroy_process_group()
 
 
+def _chain_worker(rank, world, port, N, M, seed, beta, sweeps, q):
+    """One call of `sweeps` sweeps per rank: 2 x sweeps phases coupled only through the
+    flags in peer memory (with MPS the ranks' kernels overlap in time)."""
+    import sys
+    import time
+
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    from paper_1906_06297_b200.ising import IsingLattice
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        lat = IsingLattice.distributed(N, M, seed, device=0, transport="p2p")
+        row0, rows = lat.slab_info()
+        lat.set_beta(beta).init_random()
+        t0 = time.perf_counter()
+        lat.sweep(sweeps)
+        wall = time.perf_counter() - t0
+        mine = np.empty((rows, M), dtype=np.int8)
+        lat.read_lattice(mine)
+        parts = [torch.zeros((rows, M), dtype=torch.int8) for _ in range(world)]
+        dist.all_gather(parts, torch.from_numpy(mine))
+        obs = lat.observables()
+        lat.close()
+        if rank == 0:
+            q.put(("ok", (obs, torch.cat(parts).numpy(), wall)))
+    except Exception as e:  # pragma: no cover - reported to the parent
+        q.put(("error", f"rank {rank}: {e!r}"))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,N,M,sweeps", [(4, 128, 8192, 500), (2, 64, 128, 300),
+                                              (3, 96, 16384, 200)])
+def test_rank_p2p_long_chain_separate_processes(world, N, M, sweeps):
+    """Separate processes (CUDA IPC mappings, not the in-process local groups), one long call
+    each; run under MPS (tools/gpu_mps.sh) the processes' kernels are concurrent."""
+    import oracle
+
+    seed, beta = 13, 0.4406868
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_chain_worker, args=(r, world, port, N, M, seed, beta, sweeps, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    status, payload = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+    assert status == "ok", payload
+    obs, full, wall = payload
+    o = oracle.Lattice(N, M, seed).init_random().set_beta(beta).sweep(sweeps)
+    assert np.array_equal(full, o.full()), f"{int((full != o.full()).sum())} sites differ"
+    assert obs == o.observables()
+    print(f"world {world} {N}x{M}: {sweeps} sweeps in {wall:.3f} s "
+          f"(MPS: {os.environ.get('CUDA_MPS_PIPE_DIRECTORY') is not None})")
+
+
 # (x, 8192) widths run the TMA-staged kernel, whose interior bands skip the neighbour wait
 @pytest.mark.parametrize("world,N,M", [(2, 64, 128), (4, 128, 64), (2, 4, 64), (2, 128, 8192),
                                       (4, 48, 8192)])
