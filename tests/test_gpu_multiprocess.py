@@ -107,7 +107,7 @@ def _chain_worker(rank, world, port, N, M, seed, beta, sweeps, q):
 
 
 @pytest.mark.parametrize("world,N,M,sweeps", [(4, 128, 8192, 500), (2, 64, 128, 300),
-                                              (3, 96, 16384, 200)])
+                                              (3, 96, 16384, 200), (8, 64, 8192, 300)])
 def test_rank_p2p_long_chain_separate_processes(world, N, M, sweeps):
     """Separate processes (CUDA IPC mappings, not the in-process local groups), one long call
     each; run under MPS (tools/gpu_mps.sh) the processes' kernels are concurrent."""

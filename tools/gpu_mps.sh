@@ -13,7 +13,7 @@ timeout 900 python -m pytest tests/test_gpu_multiprocess.py -q -s --timeout 600 
 echo "pytest (MPS): $(tail -1 gpurun_out/mps_pytest.txt)"; grep -E "^world" gpurun_out/mps_pytest.txt
 echo "MPS servers: $(echo get_server_list | nvidia-cuda-mps-control)"
 for n in ${MPS_BENCH_N:-2 4}; do
-  ISING_BENCH_SAME_DEVICE=1 timeout 900 python bench.py --gpus $n --steps 20 --warmup 5 --no-legs \
+  ISING_BENCH_SAME_DEVICE=1 timeout 900 python bench.py --gpus $n --steps 20 --warmup 5 ${MPS_BENCH_ARGS---no-legs} \
     > gpurun_out/mps_bench_n$n.json 2> gpurun_out/mps_bench_n$n.err
   echo "bench n=$n rc=$? $(python -c "import json,sys; d=json.load(open('gpurun_out/mps_bench_n$n.json')); print(d['value'], d['config']['transport'], d['invariance'])" 2>&1 | tail -1)"
 done
