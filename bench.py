@@ -41,7 +41,10 @@ BETA = 0.4406868
 SEED = 1
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 BYTES_PER_FLIP = 1.5  # 4-bit spins: read target + read source + write target
-MULWIDE_PER_FLIP = 4.0  # per-thread 32x32->64 multiplies per draw (16 per Philox block / 4, R6)
+# per-thread 32x32->64 multiplies per attempted flip in the staged kernel's row loop: 114
+# IMAD.WIDE.U32 per 32 flips (SASS, tools/sass_loops.py; 16 per Philox block / 4 = 4, less the
+# row-invariant round-2 products ptxas hoists out of the row loop)
+MULWIDE_PER_FLIP = 114 / 32
 IMADWIDE_PER_CLK_SM = 27.65  # measured IMAD.WIDE.U32 issue rate (profiles/r01_pipes_microbench.txt)
 TRAFFIC_FILE = os.path.join(ROOT, "profiles", "ncu_traffic.json")
 JSON_OUT = sys.stdout  # the bench line's stream (run_ours keeps the real stdout for it)
@@ -737,11 +740,12 @@ def run_ours(args):
                 "kernel": "k_basic_halfsweep<0>" if basic else ("k_halfsweep_staged<0>" if (M // 32) % 256 == 0 else "k_halfsweep<0>"),
                 "peak_source": "measured live: ising_probe_philox (Philox4x32-10-only draws/ns of "
                                "the kernels' device function, eight blocks per thread in "
-                               "lockstep); one draw per attempted flip (reading R6)",
+                               "lockstep, a fixed column chunk per thread walking the rows as "
+                               "the half-sweeps do); one draw per attempted flip (reading R6)",
                 "derived_peak": {"value": derived_peak, "unit": "flips/ns",
                                  "how": f"{sms} SMs x {IMADWIDE_PER_CLK_SM} IMAD.WIDE.U32/clk/SM "
                                         f"(measured, profiles/r01_pipes_microbench.txt) x "
-                                        f"{clk_mhz:.0f} MHz / {MULWIDE_PER_FLIP} per-thread "
+                                        f"{clk_mhz:.0f} MHz / {MULWIDE_PER_FLIP:.4f} per-thread "
                                         "mul.wide per flip (DESIGN.md §5)",
                                  "frac": flips_per_ns_kernel / derived_peak},
                 "hbm_roof_flips_per_ns": hbm_roof_flips,

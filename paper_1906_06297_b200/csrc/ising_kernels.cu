@@ -410,7 +410,11 @@ __device__ __forceinline__ uint64_t update_word<1>(uint64_t tgt, uint64_t n, uin
 #define ISING_PHILOX8 1
 #endif
 #ifndef ISING_PROBE8
-#define ISING_PROBE8 1  // the probe advances eight blocks in lockstep, like the kernels (1899 -> 2005 draws/ns)
+// 1: the probe advances eight blocks per thread in lockstep, like the kernels (1899 -> 2005
+// draws/ns); 2: and walks rows with a fixed column chunk per thread, as the half-sweeps do —
+// the products that do not depend on the row (round 2's per-block c0 * M0) leave the loop
+// there too, so the probe does the same per-draw multiply work as the kernels
+#define ISING_PROBE8 2
 #endif
 __device__ __forceinline__ void philox8(uint32_t t, uint32_t c1base, uint32_t colour, uint32_t row,
                                         const PhiloxKeys& K, uint4 (&out)[8]) {
@@ -1215,7 +1219,17 @@ __global__ void __launch_bounds__(128) k_philox_probe(PhiloxKeys K, uint32_t blo
                                                       uint32_t t, unsigned int* sink) {
   uint32_t acc = 0;
   const uint32_t row = blockIdx.x;
-#if ISING_PROBE8
+#if ISING_PROBE8 == 2
+  // a thread owns one 128-bit column chunk (counter word 1 = c1base + 0..7) and walks
+  // blocks_per_thread / 8 rows down it
+  const uint32_t c1base = 8 * (blockIdx.x * blockDim.x + threadIdx.x);
+  for (uint32_t b = 0; b < blocks_per_thread; b += 8) {
+    uint4 r[8];
+    philox8(t, c1base, 1u, row + b / 8, K, r);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc ^= r[q].x ^ r[q].y ^ r[q].z ^ r[q].w;
+  }
+#elif ISING_PROBE8
   for (uint32_t b = 0; b < blocks_per_thread; b += 8) {  // eight blocks in lockstep
     uint4 r[8];
     philox8(t, 8 * (b * blockDim.x / 8 + threadIdx.x), 1u, row, K, r);
