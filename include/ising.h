@@ -85,7 +85,11 @@ int ising_create_slabs(ising_t* out, int64_t L_rows, int64_t L_cols, uint64_t se
  * With world == 1 nccl_id may be NULL; the handle then behaves as one slab, unless the
  * environment sets ISING_SELF_EXCHANGE=1: a one-rank communicator is created and every
  * half-sweep exchanges its halo rows with itself by ncclSend/ncclRecv (the transport's
- * per-GPU cost, measurable on one device).  Collective: all ranks must call it. */
+ * per-GPU cost, measurable on one device).  Collective: all ranks must call it.
+ * Failure detection: while a call waits for its streams it polls ncclCommGetAsyncError; on an
+ * asynchronous error, or when the streams make no progress for ISING_NCCL_TIMEOUT_S seconds
+ * (environment, default 300), the communicator is aborted and this and every later call on
+ * the handle returns ISING_ERR_NCCL (destroy it). */
 int ising_create_rank(ising_t* out, int64_t L_rows, int64_t L_cols, uint64_t seed, int rank,
                       int world, int device, const void* nccl_id, size_t id_len);
 

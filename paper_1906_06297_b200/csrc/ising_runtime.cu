@@ -29,6 +29,7 @@
 #include <sched.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -678,17 +679,35 @@ int nccl_poll(ising_ctx* h) {
   return ISING_OK;
 }
 
+// A stream that makes no progress for this long in NCCL rank mode is a hung peer that reported
+// no error (ISING_NCCL_TIMEOUT_S, default 300 s): the communicator is aborted and the call
+// fails with ISING_ERR_NCCL instead of blocking the process forever.
+double nccl_timeout_s() {
+  const char* v = getenv("ISING_NCCL_TIMEOUT_S");
+  const double t = v ? atof(v) : 300.0;
+  return t > 0 ? t : 300.0;
+}
+
 // Wait for a stream; in NCCL rank mode by polling, checking the communicator meanwhile.
 int wait_stream(ising_ctx* h, cudaStream_t st) {
   if (!h->comm) {
     CU(cudaStreamSynchronize(st));
     return h->comm_aborted ? nccl_poll(h) : ISING_OK;
   }
+  const auto t0 = std::chrono::steady_clock::now();
+  const double limit = nccl_timeout_s();
   for (;;) {
     const cudaError_t e = cudaStreamQuery(st);
     if (e == cudaSuccess) return nccl_poll(h);
     if (e != cudaErrorNotReady) return fail_cuda(e, "cudaStreamQuery", __LINE__);
     TRY(nccl_poll(h));
+    if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > limit) {
+      ncclCommAbort(h->comm);
+      h->comm = nullptr;
+      h->comm_aborted = true;
+      g_last_error = "NCCL rank mode: no progress within ISING_NCCL_TIMEOUT_S (communicator aborted)";
+      return ISING_ERR_NCCL;
+    }
     nvtx_yield();
   }
 }
