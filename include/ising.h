@@ -275,6 +275,39 @@ int ising_launch_count(ising_t h, int64_t* launches);
  * measured ALU roofline of the path (every attempted flip consumes one draw). */
 int ising_probe_philox(int device, double* draws_per_ns);
 
+/* ----------------------------------------------------------- lattice batches
+ * n independent L_rows x L_cols lattices on one device, each with its own seed and beta
+ * (temperature scans and the Binder-cumulant analysis, PAPER.md:414-421,
+ * run many small lattices, which one-lattice handles leave launch-bound).  One CTA per lattice
+ * keeps both colour planes in shared memory for up to 4096 sweeps per launch.  Every lattice
+ * follows exactly the contract of a one-lattice handle with the same seed and beta (same
+ * draws, thresholds and update order): bit-identical results.  Limits: L_rows even,
+ * L_cols % 64 == 0, L_rows * L_cols <= 409600 (e.g. 640 x 640), 1 <= n <= 65535; else ARG.
+ * The handle owns its device memory; calls synchronise before returning; not thread-safe. */
+typedef struct ising_batch* ising_batch_t;
+/* seeds: n values (lattice k draws with seeds[k]); device: CUDA device index. */
+int ising_batch_create(ising_batch_t* out, int64_t L_rows, int64_t L_cols, int n_lattices,
+                       const uint64_t* seeds, int device);
+int ising_batch_destroy(ising_batch_t b);                 /* NULL is a no-op */
+/* betas: n values (each as ising_set_beta: >= 0 or +inf, NaN -> ARG); rule:
+ * ISING_RULE_METROPOLIS or ISING_RULE_HEATBATH for every lattice of the batch. */
+int ising_batch_set_beta(ising_batch_t b, const double* betas, int rule);
+int ising_batch_init_random(ising_batch_t b);             /* every lattice; t := 0 */
+int ising_batch_init_cold(ising_batch_t b);
+/* n >= 0 sweeps of every lattice; STATE / RANGE as ising_sweep. */
+int ising_batch_sweep(ising_batch_t b, int64_t n);
+/* n_samples x every sweeps; after every `every` sweeps each lattice's (up count, bond
+ * energy) — as ising_observables — into up_counts / bond_energies[k * n_samples + s]
+ * (n * n_samples entries each, caller-owned). */
+int ising_batch_sweep_measure(ising_batch_t b, int64_t n_samples, int64_t every,
+                              int64_t* up_counts, int64_t* bond_energies);
+/* Current (up count, bond energy) of every lattice (n entries each). */
+int ising_batch_observables(ising_batch_t b, int64_t* up_counts, int64_t* bond_energies);
+/* Lattice `lattice` as +-1 bytes, row-major; out_len >= L_rows * L_cols (else RANGE). */
+int ising_batch_read_lattice(ising_batch_t b, int lattice, int8_t* out, int64_t out_len);
+int ising_batch_last_sweep_ms(ising_batch_t b, double* device_ms);  /* last sweep call */
+int ising_batch_get_sweep(ising_batch_t b, uint64_t* t);
+
 const char* ising_strerror(int status);
 
 /* Message of the last CUDA/NCCL error seen by this thread ("" if none). */

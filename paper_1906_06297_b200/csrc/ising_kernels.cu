@@ -1492,6 +1492,188 @@ namespace ising {
 // several ranks share one process (ising_p2p_connect_local), a rank whose half-sweep spins on
 // another rank's flags then blocks that other rank's first launch of a kernel — a deadlock
 // (observed: the flag-wait timeout fired).  cudaFuncGetAttributes forces the load.
+// ------------------------------------------------------------- lattice batches
+// One CTA per lattice, the lattice in shared memory for the whole chunk of sweeps (row f2).
+// The update is the same as the half-sweep kernels' — the same counter-based draws (reading
+// R6 with this lattice's seed), side-word splices and acceptance — so every lattice of a
+// batch is bit-identical to a one-lattice handle and to the oracle.  Metropolis runs the
+// generic lockstep form (RULE 2: any beta, thresholds at 2^32 masked), heat bath the generic
+// per-lane form (RULE 1).
+// MR: Metropolis variant of the lockstep acceptance — 0 when every lattice of the batch has
+// both thresholds below 2^32 (the fast path of the big kernels), else 2 (generic).
+template <bool HB, int MR = 2>
+__global__ void __launch_bounds__(kBatchMaxThreads) k_batch_sweeps(const BatchParams P) {
+  extern __shared__ uint4 batch_smem[];
+  uint64_t* sm = reinterpret_cast<uint64_t*>(batch_smem);
+  __shared__ BatchLattice L;
+  __shared__ unsigned long long red[2];
+  const int k = blockIdx.x;
+  const int N = P.N, W = P.W;
+  const int plane_words = N * W;
+  uint64_t* g = P.planes + (size_t)k * 2 * plane_words;
+  for (int i = threadIdx.x; i < plane_words; i += blockDim.x) {  // both planes, 128-bit
+    reinterpret_cast<uint4*>(sm)[i] = __ldcg(reinterpret_cast<const uint4*>(g) + i);
+  }
+  if (threadIdx.x == 0) {
+    L = P.lat[k];
+    red[0] = red[1] = 0;
+  }
+  __syncthreads();
+  HalfSweepParams p{};
+  p.acc = L.acc;
+  if constexpr (HB) p.keys = L.keys;
+  const int half = W / 2;  // a thread updates two words (one 128-bit chunk) per item
+  const int items = N * half;
+  const uint32_t total = P.measure_only ? 1u : P.sweeps;
+  for (uint32_t s = 1; s <= total; ++s) {
+    const uint32_t t = P.t0 + s;
+    const bool measure = P.obs && (P.measure_only || (P.every && (P.s_base + s) % P.every == 0));
+    uint32_t up = 0, anti = 0;
+    for (int c = 0; c < 2; ++c) {
+      uint64_t* tgt = sm + c * plane_words;
+      const uint64_t* src = sm + (1 - c) * plane_words;
+      if (P.measure_only && c == 0) continue;
+      for (int it = threadIdx.x; it < items; it += blockDim.x) {
+        const int i = it / half;
+        const int w = 2 * (it - i * half);
+        const int im = i == 0 ? N - 1 : i - 1, ip = i == N - 1 ? 0 : i + 1;
+        const uint64_t n0 = src[im * W + w], n1 = src[im * W + w + 1];
+        const uint64_t c0 = src[i * W + w], c1 = src[i * W + w + 1];
+        const uint64_t s0 = src[ip * W + w], s1 = src[ip * W + w + 1];
+        const bool west = ((i & 1) == 0) == (c == 0);  // reading R2
+        uint64_t side0, side1;
+        if (west) {
+          side0 = splice_west(c0, src[i * W + (w == 0 ? W - 1 : w - 1)]);
+          side1 = splice_west(c1, c0);
+        } else {
+          side0 = splice_east(c0, c1);
+          side1 = splice_east(c1, src[i * W + (w + 2 == W ? 0 : w + 2)]);
+        }
+        uint64_t t0w = tgt[i * W + w], t1w = tgt[i * W + w + 1];
+        if (!P.measure_only) {
+          const uint32_t ctr0 = (uint32_t)(4 * w);
+          if constexpr (HB) {
+            p.colour = (uint32_t)c;
+            t0w = update_word<1>(t0w, n0, c0, s0, side0, ctr0, (uint32_t)i, t, p);
+            t1w = update_word<1>(t1w, n1, c1, s1, side1, ctr0 + 4, (uint32_t)i, t, p);
+          } else {
+            uint4 rb[8];
+            philox8(t, ctr0, (uint32_t)c, (uint32_t)i, L.keys, rb);
+            t0w = word_from_draws<MR>(t0w, n0, c0, s0, side0, rb, p);
+            t1w = word_from_draws<MR>(t1w, n1, c1, s1, side1, rb + 4, p);
+          }
+          tgt[i * W + w] = t0w;
+          tgt[i * W + w + 1] = t1w;
+        }
+        if (c == 1 && measure) {  // every bond has exactly one white end (row a8)
+          obs_word(t0w, n0, c0, s0, side0, up, anti);
+          obs_word(t1w, n1, c1, s1, side1, up, anti);
+        }
+      }
+      __syncthreads();
+    }
+    if (measure) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        up += __shfl_xor_sync(0xffffffffu, up, off);
+        anti += __shfl_xor_sync(0xffffffffu, anti, off);
+      }
+      if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&red[0], (unsigned long long)up);
+        atomicAdd(&red[1], (unsigned long long)anti);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const uint32_t slot = P.measure_only ? 0u : (P.s_base + s) / P.every - 1;
+        unsigned long long* o = P.obs + 2 * ((size_t)k * P.n_samples + slot);
+        o[0] = red[0];
+        o[1] = red[1];
+        red[0] = red[1] = 0;
+      }
+      __syncthreads();
+    }
+  }
+  if (!P.measure_only)
+    for (int i = threadIdx.x; i < plane_words; i += blockDim.x)
+      __stcg(reinterpret_cast<uint4*>(g) + i, reinterpret_cast<const uint4*>(sm)[i]);
+}
+
+template <bool HB, int MR>
+static cudaError_t batch_launch(int n_lattices, int threads, size_t smem, cudaStream_t st,
+                                const BatchParams& p) {
+  cudaError_t e = cudaFuncSetAttribute((const void*)k_batch_sweeps<HB, MR>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_batch_sweeps<HB, MR><<<n_lattices, threads, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_batch_sweeps(bool heat_bath, bool fast, int n_lattices, int threads, size_t smem,
+                                cudaStream_t st, const BatchParams& p) {
+  if (heat_bath) return batch_launch<true, 2>(n_lattices, threads, smem, st, p);
+  return fast ? batch_launch<false, 0>(n_lattices, threads, smem, st, p)
+              : batch_launch<false, 2>(n_lattices, threads, smem, st, p);
+}
+
+// Random / cold start of every lattice of a batch (row a3 with each lattice's seed): spin +1
+// iff r(seed_k, 0, c, i, j) < 2^31 — the same draws k_init takes for a one-lattice handle.
+__global__ void k_batch_init(const BatchParams P, int cold) {
+  const int64_t plane_words = (int64_t)P.N * P.W;
+  const int64_t total = 2 * plane_words;
+  const int k = blockIdx.y;
+  const BatchLattice& L = P.lat[k];
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(idx / plane_words);
+    const int64_t rem = idx - c * plane_words;
+    const int i = (int)(rem / P.W);
+    const int w = (int)(rem - (int64_t)i * P.W);
+    uint64_t word = 0x1111111111111111ull;
+    if (!cold) {
+      word = 0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const uint4 r = philox4x32_10(0u, (uint32_t)(4 * w + b), (uint32_t)c, (uint32_t)i, L.keys);
+        const uint32_t rr[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (rr[q] < 0x80000000u) word |= 1ull << (4 * (4 * b + q));
+      }
+    }
+    P.planes[(size_t)k * total + idx] = word;
+  }
+}
+
+cudaError_t launch_batch_init(int n_lattices, int cold, cudaStream_t st, const BatchParams& p) {
+  const int64_t total = 2 * (int64_t)p.N * p.W;
+  const int gx = (int)std::min<int64_t>((total + 255) / 256, 1024);
+  k_batch_init<<<dim3(gx, n_lattices), 256, 0, st>>>(p, cold);
+  return cudaGetLastError();
+}
+
+// Lattice k as the +-1 byte full lattice (row a9): site (i, J) is plane (i + J) & 1, plane
+// column J / 2 = lane (J / 2) % 16 of word J / 32.
+__global__ void k_batch_unpack(const BatchParams P, int k, int8_t* full) {
+  const int64_t M = (int64_t)P.W * 32;
+  const int64_t total = (int64_t)P.N * M;
+  const uint64_t* g = P.planes + (size_t)k * 2 * P.N * P.W;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx / M, J = idx - i * M;
+    const int c = (int)((i + J) & 1);
+    const int64_t j = J >> 1;
+    const uint64_t word = g[(size_t)c * P.N * P.W + i * P.W + (j >> 4)];
+    full[idx] = ((word >> (4 * (j & 15))) & 1) ? 1 : -1;
+  }
+}
+
+cudaError_t launch_batch_unpack(int lattice, cudaStream_t st, const BatchParams& p, int8_t* full) {
+  const int64_t total = (int64_t)p.N * p.W * 32;
+  const int grid = (int)std::min<int64_t>((total + 255) / 256, 4096);
+  k_batch_unpack<<<grid, 256, 0, st>>>(p, lattice, full);
+  return cudaGetLastError();
+}
+
 template <int R>
 static cudaError_t preload_rule() {
   cudaFuncAttributes a;

@@ -208,6 +208,35 @@ cudaError_t launch_basic_convert(int grid, cudaStream_t st, int8_t* black, int8_
                                  int8_t* full, int64_t ny, int64_t r0, int64_t rows, int to_full,
                                  unsigned int* bad);
 
+// Batches of small lattices (ising_batch_*: temperature scans and the
+// Binder analysis run many independent small lattices, which one-lattice launches leave
+// launch-bound).  One CTA per lattice: both colour planes (N x W words each, no halo rows —
+// the wrap is modular indexing) live in shared memory for a whole chunk of sweeps.
+struct BatchLattice {
+  PhiloxKeys keys;  // this lattice's seed
+  Accept acc;       // this lattice's beta (thresholds as Accept of the generic kernels)
+};
+struct BatchParams {
+  uint64_t* planes;                // lattice k: planes + k * 2 * N * W (black, then white)
+  const BatchLattice* lat;         // one per lattice
+  int32_t N, W;                    // rows, words per plane row
+  uint32_t t0;                     // sweeps t0 + 1 .. t0 + sweeps
+  uint32_t sweeps;
+  uint32_t every;                  // > 0: observables after every `every` sweeps
+  uint32_t n_samples;              // slots per lattice in obs
+  uint32_t s_base;                 // sweeps of the call done before this launch: sample slot
+                                   // of local sweep s is (s_base + s) / every - 1
+  unsigned long long* obs;         // [lattice][sample][up, antiparallel] or null
+  int32_t measure_only;            // 1: no sweeps, observables of the current state
+};
+constexpr int kBatchMaxThreads = 512;
+constexpr size_t kBatchMaxSmem = 200 * 1024;  // both planes, bytes
+// fast: every lattice has both Metropolis thresholds below 2^32 (kernel variant 0)
+cudaError_t launch_batch_sweeps(bool heat_bath, bool fast, int n_lattices, int threads, size_t smem,
+                                cudaStream_t st, const BatchParams& p);
+cudaError_t launch_batch_init(int n_lattices, int cold, cudaStream_t st, const BatchParams& p);
+cudaError_t launch_batch_unpack(int lattice, cudaStream_t st, const BatchParams& p, int8_t* full);
+
 // Host-side launchers (defined in ising_kernels.cu).
 cudaError_t launch_sync(cudaStream_t st, const SyncParams& p);
 cudaError_t launch_halfsweep_staged(int rule, int64_t slots, cudaStream_t st, HalfSweepParams p);

@@ -298,6 +298,26 @@ void compute_thresholds(double beta, int rule, uint64_t T[5]) {
   }
 }
 
+// The kernels' form of a threshold table: low 32 bits, "always" (2^32) classes as a mask
+// (and, for Metropolis, as keep masks of the generic kernel).
+Accept make_accept(const uint64_t T[5]) {
+  Accept acc{};
+  acc.keep3 = acc.keep4 = 0xffffffffu;
+  for (int a = 0; a < 5; ++a) {
+    if (T[a] >= (uint64_t(1) << 32)) {
+      acc.always_mask |= 1u << a;
+      acc.thr[a] = 0xffffffffu;
+      if (a == 3) acc.keep3 = 0;
+      if (a == 4) acc.keep4 = 0;
+    } else {
+      acc.thr[a] = (uint32_t)T[a];
+    }
+  }
+  // draw-free Metropolis (beta = 0 or inf): T = 0 contributes one "no flip" per class
+  acc.nc_const = (T[3] == 0 ? 0x11111111u : 0u) + (T[4] == 0 ? 0x11111111u : 0u);
+  return acc;
+}
+
 void make_keys(uint64_t seed, PhiloxKeys* K) {
   uint32_t k0 = (uint32_t)(seed & 0xffffffffu), k1 = (uint32_t)(seed >> 32);
   for (int r = 0; r < 10; ++r) {
@@ -1796,21 +1816,7 @@ int ising_set_beta(ising_t h, double beta) {
     h->gexec_meas = nullptr;
   }
   compute_thresholds(beta, h->rule, h->T);
-  h->acc.always_mask = 0;
-  h->acc.keep3 = h->acc.keep4 = 0xffffffffu;
-  h->acc.nc_const = 0;
-  for (int a = 0; a < 5; ++a) {
-    if (h->T[a] >= (uint64_t(1) << 32)) {
-      h->acc.always_mask |= 1u << a;
-      h->acc.thr[a] = 0xffffffffu;
-      if (a == 3) h->acc.keep3 = 0;
-      if (a == 4) h->acc.keep4 = 0;
-    } else {
-      h->acc.thr[a] = (uint32_t)h->T[a];
-    }
-  }
-  // draw-free Metropolis (beta = 0 or inf): T = 0 contributes one "no flip" per class
-  h->acc.nc_const = (h->T[3] == 0 ? 0x11111111u : 0u) + (h->T[4] == 0 ? 0x11111111u : 0u);
+  h->acc = make_accept(h->T);
   h->beta_set = true;
   return ISING_OK;
 }
@@ -2397,6 +2403,257 @@ int ising_probe_philox(int device, double* draws_per_ns) {
   cudaFree(sink);
   teardown_device(d);
   *draws_per_ns = best;
+  return ISING_OK;
+}
+
+// ------------------------------------------------------------- lattice batches
+// ising_batch_*: n independent L_rows x L_cols lattices on one device, each with its own seed
+// and beta, one CTA per lattice holding it in shared memory for a chunk of sweeps
+// (k_batch_sweeps).  SURVEY §8(f) row f2 (temperature scans / Binder analysis on small L).
+struct ising_batch {
+  int64_t N = 0, M = 0, W = 0;
+  int n = 0;
+  Device d;
+  uint64_t* planes = nullptr;
+  BatchLattice* lat_dev = nullptr;
+  std::vector<BatchLattice> lat;
+  int rule = ISING_RULE_METROPOLIS;
+  bool fast = false;  // Metropolis, every lattice's T3, T4 < 2^32: kernel variant 0
+  bool beta_set = false, state_set = false;
+  uint64_t t = 0;
+  double last_ms = 0;
+  int threads = 0;
+  size_t smem = 0;
+  unsigned long long* obs = nullptr;
+  size_t obs_cap = 0;  // u64 entries
+  int8_t* full = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+};
+
+namespace {
+constexpr uint32_t kBatchSweepsPerLaunch = 4096;
+
+void batch_free(ising_batch* b) {
+  if (!b) return;
+  if (b->d.dev >= 0) {
+    cudaSetDevice(b->d.dev);
+    cudaDeviceSynchronize();
+    for (void* p : {(void*)b->planes, (void*)b->lat_dev, (void*)b->obs, (void*)b->full})
+      if (p) cudaFree(p);
+    if (b->e0) cudaEventDestroy(b->e0);
+    if (b->e1) cudaEventDestroy(b->e1);
+    teardown_device(b->d);
+  }
+  delete b;
+}
+
+BatchParams batch_params(const ising_batch* b) {
+  BatchParams p{};
+  p.planes = b->planes;
+  p.lat = b->lat_dev;
+  p.N = (int32_t)b->N;
+  p.W = (int32_t)b->W;
+  p.t0 = (uint32_t)b->t;
+  return p;
+}
+
+int batch_ensure_obs(ising_batch* b, size_t entries) {
+  if (b->obs_cap >= entries) return ISING_OK;
+  if (b->obs) cudaFree(b->obs);
+  b->obs = nullptr;
+  b->obs_cap = 0;
+  CU(cudaMalloc(&b->obs, entries * sizeof(unsigned long long)));
+  b->obs_cap = entries;
+  return ISING_OK;
+}
+
+// sweeps t + 1 .. t + n (every > 0: observables after every `every` sweeps into slots
+// sample0.., n_samples per lattice), in launches of at most kBatchSweepsPerLaunch sweeps
+int batch_run(ising_batch* b, int64_t n, int64_t every, int64_t n_samples) {
+  NvtxRange r("ising_batch_sweeps %lld x %lld lattices", (long long)n, (long long)b->n);
+  CU(cudaSetDevice(b->d.dev));
+  CU(cudaEventRecord(b->e0, b->d.stream));
+  int64_t done = 0;
+  const bool heat = b->rule == ISING_RULE_HEATBATH;
+  while (done < n) {
+    const int64_t chunk = std::min<int64_t>(n - done, kBatchSweepsPerLaunch);
+    BatchParams p = batch_params(b);
+    p.t0 = (uint32_t)(b->t + done);
+    p.sweeps = (uint32_t)chunk;
+    if (every > 0) {
+      p.every = (uint32_t)every;
+      p.n_samples = (uint32_t)n_samples;
+      p.s_base = (uint32_t)done;
+      p.obs = b->obs;
+    }
+    CU(launch_batch_sweeps(heat, b->fast, b->n, b->threads, b->smem, b->d.stream, p));
+    done += chunk;
+  }
+  CU(cudaEventRecord(b->e1, b->d.stream));
+  CU(cudaEventSynchronize(b->e1));
+  float ms = 0;
+  CU(cudaEventElapsedTime(&ms, b->e0, b->e1));
+  b->last_ms = ms;
+  b->t += (uint64_t)n;
+  return ISING_OK;
+}
+}  // namespace
+
+int ising_batch_create(ising_batch_t* out, int64_t L_rows, int64_t L_cols, int n_lattices,
+                       const uint64_t* seeds, int device) {
+  if (!out || !seeds) return ISING_ERR_ARG;
+  *out = nullptr;
+  if (L_rows < 2 || (L_rows & 1) || L_cols < 64 || L_cols % 64 != 0 || n_lattices < 1 ||
+      n_lattices > 65535 || L_rows * L_cols / 2 > (int64_t)kBatchMaxSmem) {
+    g_last_error = "ising_batch_create: need L_rows even, L_cols % 64 == 0, L_rows * L_cols <= "
+                   "409600 (both planes in one CTA's shared memory), 1 <= n <= 65535";
+    return ISING_ERR_ARG;
+  }
+  ising_batch* b = new (std::nothrow) ising_batch;
+  if (!b) return ISING_ERR_OOM;
+  b->N = L_rows;
+  b->M = L_cols;
+  b->W = L_cols / 32;
+  b->n = n_lattices;
+  int st = setup_device(b->d, device);
+  if (st != ISING_OK) {
+    batch_free(b);
+    return st;
+  }
+  auto fail = [&](int s) {
+    batch_free(b);
+    return s;
+  };
+  b->lat.resize(n_lattices);
+  for (int k = 0; k < n_lattices; ++k) {
+    make_keys(seeds[k], &b->lat[k].keys);
+    b->lat[k].acc = Accept{};
+  }
+  const size_t words = (size_t)n_lattices * 2 * b->N * b->W;
+  cudaError_t e = cudaMalloc(&b->planes, words * sizeof(uint64_t));
+  if (e == cudaSuccess) e = cudaMalloc(&b->lat_dev, sizeof(BatchLattice) * n_lattices);
+  if (e == cudaSuccess) e = cudaMalloc(&b->full, (size_t)(b->N * b->M));
+  if (e == cudaSuccess) e = cudaEventCreate(&b->e0);
+  if (e == cudaSuccess) e = cudaEventCreate(&b->e1);
+  if (e != cudaSuccess) return fail(fail_cuda(e, "ising_batch_create", __LINE__));
+  const int64_t items = b->N * b->W / 2;
+  b->threads = (int)std::min<int64_t>(kBatchMaxThreads, (items + 31) / 32 * 32);
+  b->smem = (size_t)(2 * b->N * b->W) * sizeof(uint64_t);
+  *out = b;
+  return ISING_OK;
+}
+
+int ising_batch_destroy(ising_batch_t b) {
+  batch_free(b);
+  return ISING_OK;
+}
+
+int ising_batch_set_beta(ising_batch_t b, const double* betas, int rule) {
+  if (!b || !betas || (rule != ISING_RULE_METROPOLIS && rule != ISING_RULE_HEATBATH))
+    return ISING_ERR_ARG;
+  for (int k = 0; k < b->n; ++k)
+    if (std::isnan(betas[k]) || betas[k] < 0) return ISING_ERR_ARG;
+  bool fast = rule == ISING_RULE_METROPOLIS;
+  for (int k = 0; k < b->n; ++k) {
+    uint64_t T[5];
+    compute_thresholds(betas[k], rule, T);
+    b->lat[k].acc = make_accept(T);
+    fast = fast && (b->lat[k].acc.keep3 & b->lat[k].acc.keep4) == 0xffffffffu;
+  }
+  b->fast = fast;
+  CU(cudaSetDevice(b->d.dev));
+  CU(cudaMemcpyAsync(b->lat_dev, b->lat.data(), sizeof(BatchLattice) * b->n,
+                     cudaMemcpyHostToDevice, b->d.stream));
+  CU(cudaStreamSynchronize(b->d.stream));
+  b->rule = rule;
+  b->beta_set = true;
+  return ISING_OK;
+}
+
+static int batch_init(ising_batch_t b, int cold) {
+  if (!b) return ISING_ERR_ARG;
+  CU(cudaSetDevice(b->d.dev));
+  if (!b->beta_set) {  // the keys must be on the device for the random start
+    CU(cudaMemcpyAsync(b->lat_dev, b->lat.data(), sizeof(BatchLattice) * b->n,
+                       cudaMemcpyHostToDevice, b->d.stream));
+  }
+  CU(launch_batch_init(b->n, cold, b->d.stream, batch_params(b)));
+  CU(cudaStreamSynchronize(b->d.stream));
+  b->t = 0;
+  b->state_set = true;
+  return ISING_OK;
+}
+int ising_batch_init_random(ising_batch_t b) { return batch_init(b, 0); }
+int ising_batch_init_cold(ising_batch_t b) { return batch_init(b, 1); }
+
+int ising_batch_sweep(ising_batch_t b, int64_t n) {
+  if (!b || n < 0) return ISING_ERR_ARG;
+  if (!b->beta_set || !b->state_set) return ISING_ERR_STATE;
+  if (b->t + (uint64_t)n > 0xffffffffull) return ISING_ERR_RANGE;
+  if (n == 0) return ISING_OK;
+  return batch_run(b, n, 0, 0);
+}
+
+int ising_batch_sweep_measure(ising_batch_t b, int64_t n_samples, int64_t every,
+                              int64_t* up_counts, int64_t* bond_energies) {
+  if (!b || n_samples < 0 || every < 1 || !up_counts || !bond_energies) return ISING_ERR_ARG;
+  if (!b->beta_set || !b->state_set) return ISING_ERR_STATE;
+  if (n_samples > 0 && every > (int64_t)0xffffffff / n_samples) return ISING_ERR_RANGE;
+  if (b->t + (uint64_t)(n_samples * every) > 0xffffffffull) return ISING_ERR_RANGE;
+  if (n_samples == 0) return ISING_OK;
+  const size_t entries = (size_t)b->n * n_samples * 2;
+  TRY(batch_ensure_obs(b, entries));
+  TRY(batch_run(b, n_samples * every, every, n_samples));
+  std::vector<unsigned long long> host(entries);
+  CU(cudaMemcpy(host.data(), b->obs, entries * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  for (size_t q = 0; q < (size_t)b->n * n_samples; ++q) {
+    up_counts[q] = (int64_t)host[2 * q];
+    bond_energies[q] = 2 * (int64_t)host[2 * q + 1] - 2 * b->N * b->M;
+  }
+  return ISING_OK;
+}
+
+int ising_batch_observables(ising_batch_t b, int64_t* up_counts, int64_t* bond_energies) {
+  if (!b || !up_counts || !bond_energies) return ISING_ERR_ARG;
+  if (!b->state_set) return ISING_ERR_STATE;
+  TRY(batch_ensure_obs(b, (size_t)b->n * 2));
+  CU(cudaSetDevice(b->d.dev));
+  BatchParams p = batch_params(b);
+  p.measure_only = 1;
+  p.n_samples = 1;
+  p.obs = b->obs;
+  CU(launch_batch_sweeps(false, false, b->n, b->threads, b->smem, b->d.stream, p));
+  std::vector<unsigned long long> host((size_t)b->n * 2);
+  CU(cudaMemcpyAsync(host.data(), b->obs, host.size() * sizeof(unsigned long long),
+                     cudaMemcpyDeviceToHost, b->d.stream));
+  CU(cudaStreamSynchronize(b->d.stream));
+  for (int k = 0; k < b->n; ++k) {
+    up_counts[k] = (int64_t)host[2 * k];
+    bond_energies[k] = 2 * (int64_t)host[2 * k + 1] - 2 * b->N * b->M;
+  }
+  return ISING_OK;
+}
+
+int ising_batch_read_lattice(ising_batch_t b, int lattice, int8_t* out, int64_t out_len) {
+  if (!b || !out || lattice < 0 || lattice >= b->n) return ISING_ERR_ARG;
+  if (!b->state_set) return ISING_ERR_STATE;
+  if (out_len < b->N * b->M) return ISING_ERR_RANGE;
+  CU(cudaSetDevice(b->d.dev));
+  CU(launch_batch_unpack(lattice, b->d.stream, batch_params(b), b->full));
+  CU(cudaMemcpyAsync(out, b->full, (size_t)(b->N * b->M), cudaMemcpyDeviceToHost, b->d.stream));
+  CU(cudaStreamSynchronize(b->d.stream));
+  return ISING_OK;
+}
+
+int ising_batch_last_sweep_ms(ising_batch_t b, double* device_ms) {
+  if (!b || !device_ms) return ISING_ERR_ARG;
+  *device_ms = b->last_ms;
+  return ISING_OK;
+}
+
+int ising_batch_get_sweep(ising_batch_t b, uint64_t* t) {
+  if (!b || !t) return ISING_ERR_ARG;
+  *t = b->t;
   return ISING_OK;
 }
 

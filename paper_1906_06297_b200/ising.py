@@ -67,6 +67,17 @@ SIGNATURES = {
     "ising_launch_count": (_INT, [_VP, _I64P]),
     "ising_kernel_variant": (_INT, [_VP, ctypes.POINTER(ctypes.c_int)]),
     "ising_probe_philox": (_INT, [_INT, _DBLP]),
+    "ising_batch_create": (_INT, [ctypes.POINTER(_VP), _I64, _I64, _INT, _U64P, _INT]),
+    "ising_batch_destroy": (_INT, [_VP]),
+    "ising_batch_set_beta": (_INT, [_VP, _DBLP, _INT]),
+    "ising_batch_init_random": (_INT, [_VP]),
+    "ising_batch_init_cold": (_INT, [_VP]),
+    "ising_batch_sweep": (_INT, [_VP, _I64]),
+    "ising_batch_sweep_measure": (_INT, [_VP, _I64, _I64, _I64P, _I64P]),
+    "ising_batch_observables": (_INT, [_VP, _I64P, _I64P]),
+    "ising_batch_read_lattice": (_INT, [_VP, _INT, _VP, _I64]),
+    "ising_batch_last_sweep_ms": (_INT, [_VP, _DBLP]),
+    "ising_batch_get_sweep": (_INT, [_VP, _U64P]),
     "ising_strerror": (ctypes.c_char_p, [_INT]),
     "ising_last_error": (ctypes.c_char_p, []),
 }
@@ -563,3 +574,89 @@ def run_ranks(lats, fn):
         r, e = errs[0]
         raise RuntimeError(f"rank {r}: {e!r}") from e
     return out
+
+
+# ------------------------------------------------------------ lattice batches
+class IsingBatch:
+    """n independent L_rows x L_cols lattices on one device (ising_batch_*): lattice k draws
+    with seeds[k] and runs at betas[k]; each is bit-identical to a one-lattice handle with the
+    same seed and beta.  For temperature scans / Binder analysis on small lattices."""
+
+    def __init__(self, L_rows: int, L_cols: int, seeds, device: int = 0):
+        self.N, self.M = int(L_rows), int(L_cols)
+        seeds = np.ascontiguousarray(np.asarray(seeds, dtype=np.uint64))
+        self.n = int(seeds.size)
+        h = _VP()
+        _check(load().ising_batch_create(ctypes.byref(h), self.N, self.M, self.n,
+                                         seeds.ctypes.data_as(_U64P), int(device)),
+               "ising_batch_create")
+        self.h = h.value
+
+    def close(self):
+        if getattr(self, "h", None):
+            load().ising_batch_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def set_beta(self, betas, rule: int = RULE_METROPOLIS):
+        b = np.ascontiguousarray(np.broadcast_to(np.asarray(betas, dtype=np.float64), (self.n,)))
+        _check(load().ising_batch_set_beta(self.h, b.ctypes.data_as(_DBLP), int(rule)),
+               "ising_batch_set_beta")
+        return self
+
+    def init_random(self):
+        _check(load().ising_batch_init_random(self.h), "ising_batch_init_random")
+        return self
+
+    def init_cold(self):
+        _check(load().ising_batch_init_cold(self.h), "ising_batch_init_cold")
+        return self
+
+    def sweep(self, n: int = 1):
+        _check(load().ising_batch_sweep(self.h, int(n)), "ising_batch_sweep")
+        return self
+
+    def measure(self, n_samples: int, every: int = 1) -> tuple[np.ndarray, np.ndarray]:
+        """(up counts, bond energies), each of shape (n_lattices, n_samples)."""
+        up = np.zeros((self.n, int(n_samples)), dtype=np.int64)
+        E = np.zeros((self.n, int(n_samples)), dtype=np.int64)
+        _check(load().ising_batch_sweep_measure(self.h, int(n_samples), int(every),
+                                                up.ctypes.data_as(_I64P), E.ctypes.data_as(_I64P)),
+               "ising_batch_sweep_measure")
+        return up, E
+
+    def observables(self) -> tuple[np.ndarray, np.ndarray]:
+        up = np.zeros(self.n, dtype=np.int64)
+        E = np.zeros(self.n, dtype=np.int64)
+        _check(load().ising_batch_observables(self.h, up.ctypes.data_as(_I64P), E.ctypes.data_as(_I64P)),
+               "ising_batch_observables")
+        return up, E
+
+    def read_lattice(self, k: int, out=None) -> np.ndarray:
+        if out is None:
+            out = np.empty((self.N, self.M), dtype=np.int8)
+        ptr, n = _buf_ptr(out, self.N * self.M, True)
+        _check(load().ising_batch_read_lattice(self.h, int(k), ptr, n), "ising_batch_read_lattice")
+        return out
+
+    def last_sweep_ms(self) -> float:
+        v = _DBL()
+        _check(load().ising_batch_last_sweep_ms(self.h, ctypes.byref(v)), "ising_batch_last_sweep_ms")
+        return v.value
+
+    @property
+    def t(self) -> int:
+        v = _U64()
+        _check(load().ising_batch_get_sweep(self.h, ctypes.byref(v)), "ising_batch_get_sweep")
+        return v.value
