@@ -230,6 +230,15 @@ struct BatchParams {
   int32_t measure_only;            // 1: no sweeps, observables of the current state
 };
 constexpr int kBatchMaxThreads = 512;
+// Row bands per lattice: a thread owns one 128-bit column pair of a band of consecutive rows,
+// W / 2 pairs per row, at most kBatchMaxThreads threads (the CTA: batch_threads).
+__host__ __device__ inline int batch_bands(int N, int W) {
+  const int per = kBatchMaxThreads / (W / 2);
+  return N < per ? N : per;
+}
+__host__ __device__ inline int batch_threads(int N, int W) {
+  return (batch_bands(N, W) * (W / 2) + 31) / 32 * 32;
+}
 constexpr size_t kBatchMaxSmem = 200 * 1024;  // both planes, bytes
 // fast: every lattice has both Metropolis thresholds below 2^32 (kernel variant 0)
 cudaError_t launch_batch_sweeps(bool heat_bath, bool fast, int n_lattices, int threads, size_t smem,

@@ -2536,8 +2536,7 @@ int ising_batch_create(ising_batch_t* out, int64_t L_rows, int64_t L_cols, int n
   if (e == cudaSuccess) e = cudaEventCreate(&b->e0);
   if (e == cudaSuccess) e = cudaEventCreate(&b->e1);
   if (e != cudaSuccess) return fail(fail_cuda(e, "ising_batch_create", __LINE__));
-  const int64_t items = b->N * b->W / 2;
-  b->threads = (int)std::min<int64_t>(kBatchMaxThreads, (items + 31) / 32 * 32);
+  b->threads = batch_threads((int)b->N, (int)b->W);
   b->smem = (size_t)(2 * b->N * b->W) * sizeof(uint64_t);
   *out = b;
   return ISING_OK;
