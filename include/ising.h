@@ -305,6 +305,12 @@ int ising_batch_sweep_measure(ising_batch_t b, int64_t n_samples, int64_t every,
 int ising_batch_observables(ising_batch_t b, int64_t* up_counts, int64_t* bond_energies);
 /* Lattice `lattice` as +-1 bytes, row-major; out_len >= L_rows * L_cols (else RANGE). */
 int ising_batch_read_lattice(ising_batch_t b, int lattice, int8_t* out, int64_t out_len);
+/* Load lattice `lattice` from +-1 bytes (in_len >= L_rows * L_cols, else RANGE; other values
+ * -> ARG) and set the batch's sweep counter to t (shared by all lattices: the next sweep is
+ * t + 1) — checkpoint / exact resume of a batch, lattice by lattice.  Lattices never
+ * initialised or written start cold. */
+int ising_batch_write_lattice(ising_batch_t b, int lattice, const int8_t* in, int64_t in_len,
+                              uint64_t t);
 int ising_batch_last_sweep_ms(ising_batch_t b, double* device_ms);  /* last sweep call */
 int ising_batch_get_sweep(ising_batch_t b, uint64_t* t);
 

@@ -1716,6 +1716,40 @@ __global__ void k_batch_unpack(const BatchParams P, int k, int8_t* full) {
   }
 }
 
+// Lattice k from the +-1 byte full lattice (the inverse of k_batch_unpack); *bad := 1 if a
+// value is not -1 / +1.
+__global__ void k_batch_pack(const BatchParams P, int k, const int8_t* full, unsigned int* bad) {
+  const int64_t plane_words = (int64_t)P.N * P.W;
+  const int64_t M = (int64_t)P.W * 32;
+  uint64_t* g = P.planes + (size_t)k * 2 * plane_words;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < 2 * plane_words;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(idx / plane_words);
+    const int64_t rem = idx - c * plane_words;
+    const int64_t i = rem / P.W, w = rem - i * P.W;
+    const int8_t* row = full + i * M;
+    uint64_t word = 0;
+    bool ok = true;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int64_t J = 2 * (16 * w + q) + ((i + c) & 1);  // reading R1
+      const int8_t v = row[J];
+      ok = ok && (v == 1 || v == -1);
+      word |= (uint64_t)(v == 1) << (4 * q);
+    }
+    if (!ok) atomicExch(bad, 1u);
+    g[idx] = word;
+  }
+}
+
+cudaError_t launch_batch_pack(int lattice, cudaStream_t st, const BatchParams& p, const int8_t* full,
+                              unsigned int* bad) {
+  const int64_t total = 2 * (int64_t)p.N * p.W;
+  const int grid = (int)std::min<int64_t>((total + 255) / 256, 4096);
+  k_batch_pack<<<grid, 256, 0, st>>>(p, lattice, full, bad);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_batch_unpack(int lattice, cudaStream_t st, const BatchParams& p, int8_t* full) {
   const int64_t total = (int64_t)p.N * p.W * 32;
   const int grid = (int)std::min<int64_t>((total + 255) / 256, 4096);

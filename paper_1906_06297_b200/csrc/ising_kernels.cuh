@@ -245,6 +245,8 @@ cudaError_t launch_batch_sweeps(bool heat_bath, bool fast, int n_lattices, int t
                                 cudaStream_t st, const BatchParams& p);
 cudaError_t launch_batch_init(int n_lattices, int cold, cudaStream_t st, const BatchParams& p);
 cudaError_t launch_batch_unpack(int lattice, cudaStream_t st, const BatchParams& p, int8_t* full);
+cudaError_t launch_batch_pack(int lattice, cudaStream_t st, const BatchParams& p, const int8_t* full,
+                              unsigned int* bad);
 
 // Host-side launchers (defined in ising_kernels.cu).
 cudaError_t launch_sync(cudaStream_t st, const SyncParams& p);

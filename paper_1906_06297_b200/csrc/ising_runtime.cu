@@ -2427,6 +2427,7 @@ struct ising_batch {
   unsigned long long* obs = nullptr;
   size_t obs_cap = 0;  // u64 entries
   int8_t* full = nullptr;
+  unsigned int* bad = nullptr;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
 };
 
@@ -2438,7 +2439,7 @@ void batch_free(ising_batch* b) {
   if (b->d.dev >= 0) {
     cudaSetDevice(b->d.dev);
     cudaDeviceSynchronize();
-    for (void* p : {(void*)b->planes, (void*)b->lat_dev, (void*)b->obs, (void*)b->full})
+    for (void* p : {(void*)b->planes, (void*)b->lat_dev, (void*)b->obs, (void*)b->full, (void*)b->bad})
       if (p) cudaFree(p);
     if (b->e0) cudaEventDestroy(b->e0);
     if (b->e1) cudaEventDestroy(b->e1);
@@ -2641,6 +2642,35 @@ int ising_batch_read_lattice(ising_batch_t b, int lattice, int8_t* out, int64_t 
   CU(launch_batch_unpack(lattice, b->d.stream, batch_params(b), b->full));
   CU(cudaMemcpyAsync(out, b->full, (size_t)(b->N * b->M), cudaMemcpyDeviceToHost, b->d.stream));
   CU(cudaStreamSynchronize(b->d.stream));
+  return ISING_OK;
+}
+
+int ising_batch_write_lattice(ising_batch_t b, int lattice, const int8_t* in, int64_t in_len,
+                              uint64_t t) {
+  if (!b || !in || lattice < 0 || lattice >= b->n) return ISING_ERR_ARG;
+  if (in_len < b->N * b->M) return ISING_ERR_RANGE;
+  if (t > 0xffffffffull) return ISING_ERR_RANGE;
+  CU(cudaSetDevice(b->d.dev));
+  if (!b->bad) CU(cudaMalloc(&b->bad, sizeof(unsigned int)));
+  CU(cudaMemsetAsync(b->bad, 0, sizeof(unsigned int), b->d.stream));
+  if (!b->beta_set) {  // the keys must be on the device before the first sweep
+    CU(cudaMemcpyAsync(b->lat_dev, b->lat.data(), sizeof(BatchLattice) * b->n,
+                       cudaMemcpyHostToDevice, b->d.stream));
+  }
+  if (!b->state_set) {  // the other lattices start cold until written
+    CU(launch_batch_init(b->n, 1, b->d.stream, batch_params(b)));
+    b->state_set = true;
+  }
+  CU(cudaMemcpyAsync(b->full, in, (size_t)(b->N * b->M), cudaMemcpyHostToDevice, b->d.stream));
+  CU(launch_batch_pack(lattice, b->d.stream, batch_params(b), b->full, b->bad));
+  unsigned int bad = 0;
+  CU(cudaMemcpyAsync(&bad, b->bad, sizeof bad, cudaMemcpyDeviceToHost, b->d.stream));
+  CU(cudaStreamSynchronize(b->d.stream));
+  if (bad) {
+    g_last_error = "ising_batch_write_lattice: values must be -1 or +1";
+    return ISING_ERR_ARG;
+  }
+  b->t = t;
   return ISING_OK;
 }
 

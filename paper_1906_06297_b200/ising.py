@@ -76,6 +76,7 @@ SIGNATURES = {
     "ising_batch_sweep_measure": (_INT, [_VP, _I64, _I64, _I64P, _I64P]),
     "ising_batch_observables": (_INT, [_VP, _I64P, _I64P]),
     "ising_batch_read_lattice": (_INT, [_VP, _INT, _VP, _I64]),
+    "ising_batch_write_lattice": (_INT, [_VP, _INT, _VP, _I64, _U64]),
     "ising_batch_last_sweep_ms": (_INT, [_VP, _DBLP]),
     "ising_batch_get_sweep": (_INT, [_VP, _U64P]),
     "ising_strerror": (ctypes.c_char_p, [_INT]),
@@ -649,6 +650,11 @@ class IsingBatch:
         ptr, n = _buf_ptr(out, self.N * self.M, True)
         _check(load().ising_batch_read_lattice(self.h, int(k), ptr, n), "ising_batch_read_lattice")
         return out
+
+    def write_lattice(self, k: int, full, t: int = 0):
+        ptr, n = _buf_ptr(full, self.N * self.M, False)
+        _check(load().ising_batch_write_lattice(self.h, int(k), ptr, n, int(t)), "ising_batch_write_lattice")
+        return self
 
     def last_sweep_ms(self) -> float:
         v = _DBL()

@@ -132,3 +132,34 @@ def test_batch_errors():
         assert up.tolist() == [64 * 64] * 2 and E.tolist() == [-2 * 64 * 64] * 2
     finally:
         b.close()
+
+
+@pytest.mark.gpu
+def test_batch_write_lattice_resume_matches_oracle():
+    # checkpoint / exact resume: lattices loaded from +-1 bytes at t = 123, then swept
+    N, M, n = 96, 192, 3
+    rng = np.random.default_rng(42)
+    seeds = [5, 6, 7]
+    betas = [0.3, cases.BETA_TC, 0.6]
+    starts = [cases.random_pm1(rng, N, M, p) for p in (0.2, 0.5, 0.9)]
+    b = IsingBatch(N, M, seeds).set_beta(betas)
+    try:
+        for k in range(n):
+            b.write_lattice(k, starts[k], t=123)
+        assert b.t == 123
+        for k in range(n):
+            assert np.array_equal(b.read_lattice(k), starts[k])
+        up, E = b.measure(4, 5)
+        for k in range(n):
+            o = oracle.Lattice(N, M, seeds[k]).set_beta(betas[k]).load_full(starts[k], t=123)
+            ou, oE = o.chain(20)
+            assert up[k].tolist() == [int(x) for x in ou[4::5]]
+            assert E[k].tolist() == [int(x) for x in oE[4::5]]
+            assert np.array_equal(b.read_lattice(k), o.full())
+        bad = starts[0].copy()
+        bad[3, 5] = 0
+        with pytest.raises(ising.IsingError) as e:
+            b.write_lattice(0, bad)
+        assert e.value.status == ising.ISING_ERR_ARG
+    finally:
+        b.close()
