@@ -4,6 +4,8 @@
  *     -> line 1: "up E t sum" after `sweeps` sweeps (and the +-1 bytes, row-major, written
  *        to lattice.bin when given)
  *        line 2: "up E" of 2 x 3 samples, one every 2 sweeps, via ising_sweep_measure_async
+ *        line 3: a lattice batch of 3 copies of the lattice (seeds seed, seed+1, seed+2; betas
+ *        beta, beta/2, 2 beta): "up E" of each after `sweeps` sweeps (ising_batch_*)
  * Built by __graft_entry__.build(); tests/test_gpu_capi.py runs it against the oracle. */
 #include <stdio.h>
 #include <stdlib.h>
@@ -62,5 +64,20 @@ int main(int argc, char** argv) {
     for (int k = 0; k < 3; ++k) printf("%lld %lld ", (long long)ups[c][k], (long long)Es[c][k]);
   printf("\n");
   CHECK(ising_destroy(h));
+  /* three independent lattices of the same shape in one batch (one CTA each) */
+  if (N * M <= 409600) {
+    ising_batch_t b = NULL;
+    const uint64_t seeds[3] = {seed, seed + 1, seed + 2};
+    const double betas[3] = {beta, beta / 2, 2 * beta};
+    int64_t bu[3], bE[3];
+    CHECK(ising_batch_create(&b, N, M, 3, seeds, 0));
+    CHECK(ising_batch_set_beta(b, betas, ISING_RULE_METROPOLIS));
+    CHECK(ising_batch_init_random(b));
+    CHECK(ising_batch_sweep(b, sweeps));
+    CHECK(ising_batch_observables(b, bu, bE));
+    for (int k = 0; k < 3; ++k) printf("%lld %lld ", (long long)bu[k], (long long)bE[k]);
+    printf("\n");
+    CHECK(ising_batch_destroy(b));
+  }
   return 0;
 }

@@ -21,7 +21,7 @@ def test_c_program_matches_oracle(N, M, seed, beta, sweeps, tmp_path):
     out = subprocess.run([EXE, str(N), str(M), str(seed), repr(beta), str(sweeps), str(lat_file)],
                          capture_output=True, text=True, timeout=120)
     assert out.returncode == 0, out.stderr
-    line1, line2 = out.stdout.strip().split("\n")
+    line1, line2, line3 = out.stdout.strip().split("\n")
     up, E, t, total = (int(x) for x in line1.split())
     o = oracle.Lattice(N, M, seed).init_random().set_beta(beta).sweep(sweeps)
     assert (up, E) == o.observables()
@@ -31,3 +31,8 @@ def test_c_program_matches_oracle(N, M, seed, beta, sweeps, tmp_path):
     ou, oE = o.chain(12)  # the async chain: 2 calls x 3 samples, one every 2 sweeps
     got = [int(x) for x in line2.split()]
     assert got[0::2] == [int(x) for x in ou[1::2]] and got[1::2] == [int(x) for x in oE[1::2]]
+    # the lattice batch: seeds seed, seed + 1, seed + 2 at beta, beta / 2, 2 beta
+    got_b = [int(x) for x in line3.split()]
+    for k, bk in enumerate([beta, beta / 2, 2 * beta]):
+        ok = oracle.Lattice(N, M, seed + k).init_random().set_beta(bk).sweep(sweeps)
+        assert tuple(got_b[2 * k:2 * k + 2]) == ok.observables(), f"batch lattice {k}"
