@@ -2525,7 +2525,11 @@ int ising_batch_create(ising_batch_t* out, int64_t L_rows, int64_t L_cols, int n
     batch_free(b);
     return s;
   };
-  b->lat.resize(n_lattices);
+  try {
+    b->lat.resize(n_lattices);
+  } catch (const std::bad_alloc&) {
+    return fail(ISING_ERR_OOM);
+  }
   for (int k = 0; k < n_lattices; ++k) {
     make_keys(seeds[k], &b->lat[k].keys);
     b->lat[k].acc = Accept{};
@@ -2604,11 +2608,21 @@ int ising_batch_sweep_measure(ising_batch_t b, int64_t n_samples, int64_t every,
   const size_t entries = (size_t)b->n * n_samples * 2;
   TRY(batch_ensure_obs(b, entries));
   TRY(batch_run(b, n_samples * every, every, n_samples));
-  std::vector<unsigned long long> host(entries);
-  CU(cudaMemcpy(host.data(), b->obs, entries * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
-  for (size_t q = 0; q < (size_t)b->n * n_samples; ++q) {
-    up_counts[q] = (int64_t)host[2 * q];
-    bond_energies[q] = 2 * (int64_t)host[2 * q + 1] - 2 * b->N * b->M;
+  // copy back in pieces through a bounded host buffer (no allocation of the whole series)
+  std::vector<unsigned long long> host;
+  try {
+    host.resize(std::min<size_t>(entries, size_t(1) << 22));
+  } catch (const std::bad_alloc&) {
+    return ISING_ERR_OOM;
+  }
+  for (size_t q0 = 0; q0 < entries; q0 += host.size()) {
+    const size_t m = std::min(host.size(), entries - q0);
+    CU(cudaMemcpy(host.data(), b->obs + q0, m * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    for (size_t e = 0; e < m; e += 2) {
+      const size_t q = (q0 + e) / 2;
+      up_counts[q] = (int64_t)host[e];
+      bond_energies[q] = 2 * (int64_t)host[e + 1] - 2 * b->N * b->M;
+    }
   }
   return ISING_OK;
 }
@@ -2623,7 +2637,12 @@ int ising_batch_observables(ising_batch_t b, int64_t* up_counts, int64_t* bond_e
   p.n_samples = 1;
   p.obs = b->obs;
   CU(launch_batch_sweeps(false, false, b->n, b->threads, b->smem, b->d.stream, p));
-  std::vector<unsigned long long> host((size_t)b->n * 2);
+  std::vector<unsigned long long> host;
+  try {
+    host.resize((size_t)b->n * 2);
+  } catch (const std::bad_alloc&) {
+    return ISING_ERR_OOM;
+  }
   CU(cudaMemcpyAsync(host.data(), b->obs, host.size() * sizeof(unsigned long long),
                      cudaMemcpyDeviceToHost, b->d.stream));
   CU(cudaStreamSynchronize(b->d.stream));
