@@ -279,10 +279,13 @@ int ising_probe_philox(int device, double* draws_per_ns);
  * n independent L_rows x L_cols lattices on one device, each with its own seed and beta
  * (temperature scans and the Binder-cumulant analysis, PAPER.md:414-421,
  * run many small lattices, which one-lattice handles leave launch-bound).  One CTA per lattice
- * keeps both colour planes in shared memory for up to 4096 sweeps per launch.  Every lattice
- * follows exactly the contract of a one-lattice handle with the same seed and beta (same
- * draws, thresholds and update order): bit-identical results.  Limits: L_rows even,
- * L_cols % 64 == 0, L_rows * L_cols <= 409600 (e.g. 640 x 640), 1 <= n <= 65535; else ARG.
+ * keeps both colour planes in shared memory for up to 4096 sweeps per launch (L_rows * L_cols
+ * <= 409600, e.g. 640 x 640); larger lattices span a thread-block cluster of 2 to 16 CTAs
+ * (the smallest that divides L_rows and fits (L_rows / C + 2) * L_cols / 2 bytes per CTA in
+ * 200 KB — up to 2048 x 2048), halo rows moving through distributed shared memory.  Every
+ * lattice follows exactly the contract of a one-lattice handle with the same seed and beta
+ * (same draws, thresholds and update order): bit-identical results.  Limits: L_rows even,
+ * L_cols % 64 == 0, a lattice that fits as above, 1 <= n <= 65535; else ARG.
  * The handle owns its device memory; calls synchronise before returning; not thread-safe. */
 typedef struct ising_batch* ising_batch_t;
 /* seeds: n values (lattice k draws with seeds[k]); device: CUDA device index. */

@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <type_traits>
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include "ising_kernels.cuh"
@@ -1662,6 +1663,174 @@ cudaError_t launch_batch_sweeps(bool heat_bath, bool fast, int n_lattices, int t
   if (heat_bath) return batch_launch<true, 2>(n_lattices, threads, smem, st, p);
   return fast ? batch_launch<false, 0>(n_lattices, threads, smem, st, p)
               : batch_launch<false, 2>(n_lattices, threads, smem, st, p);
+}
+
+// Lattices too large for one CTA's shared memory (up to 2048^2): a thread-block cluster of
+// P.cluster CTAs per lattice, CTA r holding rows [r R, (r + 1) R) of both planes plus one halo
+// row above and below (R = N / cluster).  Each phase starts by pulling the source plane's two
+// halo rows from the neighbouring CTAs' shared memory (distributed shared memory, the torus
+// wrap across the cluster), updates the band like k_batch_sweeps, and ends with a cluster
+// barrier — the neighbours' edge rows are final before anyone pulls them, and nobody
+// overwrites a row a neighbour is still pulling.  Observables reduce per CTA, then into CTA 0's
+// counters through DSMEM atomics.
+template <bool HB, int MR>
+__global__ void __launch_bounds__(kBatchMaxThreads) k_batch_cluster_sweeps(const BatchParams P) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ uint4 batch_smem[];
+  uint64_t* sm = reinterpret_cast<uint64_t*>(batch_smem);  // plane c: (R + 2) x W, padded
+  __shared__ BatchLattice L;
+  __shared__ unsigned long long red[2];
+  const int C = (int)cluster.num_blocks();
+  const int r = (int)cluster.block_rank();
+  const int k = blockIdx.x / C;
+  const int N = P.N, W = P.W;
+  const int R = N / C;
+  const int pw = (R + 2) * W;  // padded plane words
+  uint64_t* g = P.planes + (size_t)k * 2 * N * W;
+  for (int c = 0; c < 2; ++c)
+    for (int i = threadIdx.x; i < R * W / 2; i += blockDim.x)  // own rows, 128-bit
+      reinterpret_cast<uint4*>(sm + c * pw + W)[i] =
+          __ldcg(reinterpret_cast<const uint4*>(g + (size_t)c * N * W + (size_t)r * R * W) + i);
+  if (threadIdx.x == 0) {
+    L = P.lat[k];
+    red[0] = red[1] = 0;
+  }
+  HalfSweepParams p{};
+  const int up_rank = (r + C - 1) % C, dn_rank = (r + 1) % C;
+  uint64_t* up_sm = cluster.map_shared_rank(sm, up_rank);
+  uint64_t* dn_sm = cluster.map_shared_rank(sm, dn_rank);
+  unsigned long long* red0 = cluster.map_shared_rank(red, 0);
+  cluster.sync();  // every CTA loaded before anyone pulls halos
+  p.acc = L.acc;
+  if constexpr (HB) p.keys = L.keys;
+  const int half = W / 2;
+  const int bands = batch_bands(R, W);
+  const int H = (R + bands - 1) / bands;
+  const int band = (int)threadIdx.x / half;
+  const int w = 2 * ((int)threadIdx.x - band * half);
+  const int i0 = band < bands ? band * H : R, i1 = min(i0 + H, R);
+  const int wwest = w == 0 ? W - 1 : w - 1, weast = w + 2 == W ? 0 : w + 2;
+  const int grow0 = r * R;  // global row of local row 0
+  const uint32_t total = P.measure_only ? 1u : P.sweeps;
+  for (uint32_t s = 1; s <= total; ++s) {
+    const uint32_t t = P.t0 + s;
+    const bool measure = P.obs && (P.measure_only || (P.every && (P.s_base + s) % P.every == 0));
+    uint32_t up = 0, anti = 0;
+    for (int c = 0; c < 2; ++c) {
+      if (P.measure_only && c == 0) continue;
+      uint64_t* tgt = sm + c * pw + W;  // local row 0
+      uint64_t* src = sm + (1 - c) * pw + W;
+      // halo rows of the source plane: the upper neighbour's last row, the lower one's first
+      for (int q = threadIdx.x; q < 2 * W; q += blockDim.x) {
+        if (q < W)
+          src[-W + q] = up_sm[(1 - c) * pw + W + (R - 1) * W + q];
+        else
+          src[R * W + q - W] = dn_sm[(1 - c) * pw + W + q - W];
+      }
+      __syncthreads();
+      if (i0 < i1) {
+        const ulonglong2 nn = *reinterpret_cast<const ulonglong2*>(src + (i0 - 1) * W + w);
+        const ulonglong2 cc = *reinterpret_cast<const ulonglong2*>(src + i0 * W + w);
+        uint64_t n0 = nn.x, n1 = nn.y, c0 = cc.x, c1 = cc.y;
+        int ro = i0 * W;
+        for (int i = i0; i < i1; ++i, ro += W) {
+          const ulonglong2 ss = *reinterpret_cast<const ulonglong2*>(src + ro + W + w);
+          const uint64_t s0 = ss.x, s1 = ss.y;
+          const int gi = grow0 + i;
+          const bool west = ((gi & 1) == 0) == (c == 0);  // reading R2
+          uint64_t side0, side1;
+          if (west) {
+            side0 = splice_west(c0, src[ro + wwest]);
+            side1 = splice_west(c1, c0);
+          } else {
+            side0 = splice_east(c0, c1);
+            side1 = splice_east(c1, src[ro + weast]);
+          }
+          const ulonglong2 tv = *reinterpret_cast<const ulonglong2*>(tgt + ro + w);
+          uint64_t t0w = tv.x, t1w = tv.y;
+          if (!P.measure_only) {
+            if constexpr (HB) {
+              p.colour = (uint32_t)c;
+              t0w = update_word<1>(t0w, n0, c0, s0, side0, (uint32_t)(4 * w), (uint32_t)gi, t, p);
+              t1w = update_word<1>(t1w, n1, c1, s1, side1, (uint32_t)(4 * w + 4), (uint32_t)gi, t, p);
+            } else {
+              uint4 rb[8];
+              philox8(t, (uint32_t)(4 * w), (uint32_t)c, (uint32_t)gi, L.keys, rb);
+              t0w = word_from_draws<MR>(t0w, n0, c0, s0, side0, rb, p);
+              t1w = word_from_draws<MR>(t1w, n1, c1, s1, side1, rb + 4, p);
+            }
+            *reinterpret_cast<ulonglong2*>(tgt + ro + w) = make_ulonglong2(t0w, t1w);
+          }
+          if (c == 1 && measure) {
+            obs_word(t0w, n0, c0, s0, side0, up, anti);
+            obs_word(t1w, n1, c1, s1, side1, up, anti);
+          }
+          n0 = c0;
+          n1 = c1;
+          c0 = s0;
+          c1 = s1;
+        }
+      }
+      cluster.sync();  // this plane final everywhere before the next phase pulls its halos
+    }
+    if (measure) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        up += __shfl_xor_sync(0xffffffffu, up, off);
+        anti += __shfl_xor_sync(0xffffffffu, anti, off);
+      }
+      if ((threadIdx.x & 31) == 0 && (up | anti)) {
+        atomicAdd(&red0[0], (unsigned long long)up);
+        atomicAdd(&red0[1], (unsigned long long)anti);
+      }
+      cluster.sync();
+      if (r == 0 && threadIdx.x == 0) {
+        const uint32_t slot = P.measure_only ? 0u : (P.s_base + s) / P.every - 1;
+        unsigned long long* o = P.obs + 2 * ((size_t)k * P.n_samples + slot);
+        o[0] = red[0];
+        o[1] = red[1];
+        red[0] = red[1] = 0;  // before CTA 0 reaches the next cluster barrier
+      }
+    }
+  }
+  if (!P.measure_only)
+    for (int c = 0; c < 2; ++c)
+      for (int i = threadIdx.x; i < R * W / 2; i += blockDim.x)
+        __stcg(reinterpret_cast<uint4*>(g + (size_t)c * N * W + (size_t)r * R * W) + i,
+               reinterpret_cast<const uint4*>(sm + c * pw + W)[i]);
+  cluster.sync();  // no CTA exits while a neighbour may still read its shared memory
+}
+
+template <bool HB, int MR>
+static cudaError_t cluster_launch(int n_lattices, int cluster, int threads, size_t smem,
+                                  cudaStream_t st, const BatchParams& p) {
+  const void* f = (const void*)k_batch_cluster_sweeps<HB, MR>;
+  cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess && cluster > 8)
+    e = cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(n_lattices * cluster));
+  cfg.blockDim = dim3((unsigned)threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_batch_cluster_sweeps<HB, MR>, p);
+}
+
+cudaError_t launch_batch_cluster_sweeps(bool heat_bath, bool fast, int n_lattices, int cluster,
+                                        int threads, size_t smem, cudaStream_t st,
+                                        const BatchParams& p) {
+  if (heat_bath) return cluster_launch<true, 2>(n_lattices, cluster, threads, smem, st, p);
+  return fast ? cluster_launch<false, 0>(n_lattices, cluster, threads, smem, st, p)
+              : cluster_launch<false, 2>(n_lattices, cluster, threads, smem, st, p);
 }
 
 // Random / cold start of every lattice of a batch (row a3 with each lattice's seed): spin +1

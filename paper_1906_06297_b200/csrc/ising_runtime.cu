@@ -2423,6 +2423,7 @@ struct ising_batch {
   uint64_t t = 0;
   double last_ms = 0;
   int threads = 0;
+  int cluster = 1;  // CTAs per lattice (1: k_batch_sweeps; > 1: k_batch_cluster_sweeps)
   size_t smem = 0;
   unsigned long long* obs = nullptr;
   size_t obs_cap = 0;  // u64 entries
@@ -2468,6 +2469,11 @@ int batch_ensure_obs(ising_batch* b, size_t entries) {
   return ISING_OK;
 }
 
+cudaError_t batch_launch_sweeps(const ising_batch* b, bool heat, bool fast, const BatchParams& p) {
+  if (b->cluster == 1) return launch_batch_sweeps(heat, fast, b->n, b->threads, b->smem, b->d.stream, p);
+  return launch_batch_cluster_sweeps(heat, fast, b->n, b->cluster, b->threads, b->smem, b->d.stream, p);
+}
+
 // sweeps t + 1 .. t + n (every > 0: observables after every `every` sweeps into slots
 // sample0.., n_samples per lattice), in launches of at most kBatchSweepsPerLaunch sweeps
 int batch_run(ising_batch* b, int64_t n, int64_t every, int64_t n_samples) {
@@ -2487,7 +2493,7 @@ int batch_run(ising_batch* b, int64_t n, int64_t every, int64_t n_samples) {
       p.s_base = (uint32_t)done;
       p.obs = b->obs;
     }
-    CU(launch_batch_sweeps(heat, b->fast, b->n, b->threads, b->smem, b->d.stream, p));
+    CU(batch_launch_sweeps(b, heat, b->fast, p));
     done += chunk;
   }
   CU(cudaEventRecord(b->e1, b->d.stream));
@@ -2504,10 +2510,23 @@ int ising_batch_create(ising_batch_t* out, int64_t L_rows, int64_t L_cols, int n
                        const uint64_t* seeds, int device) {
   if (!out || !seeds) return ISING_ERR_ARG;
   *out = nullptr;
-  if (L_rows < 2 || (L_rows & 1) || L_cols < 64 || L_cols % 64 != 0 || n_lattices < 1 ||
-      n_lattices > 65535 || L_rows * L_cols / 2 > (int64_t)kBatchMaxSmem) {
-    g_last_error = "ising_batch_create: need L_rows even, L_cols % 64 == 0, L_rows * L_cols <= "
-                   "409600 (both planes in one CTA's shared memory), 1 <= n <= 65535";
+  // CTAs per lattice: one if both planes fit its shared memory, else the smallest cluster
+  // (2 .. 16 CTAs, dividing L_rows) whose row bands plus halo rows fit
+  int cluster = 0;
+  if (L_rows >= 2 && L_cols >= 64 && L_cols % 64 == 0 && L_rows <= 65536 && L_cols <= 65536) {
+    if (L_rows * L_cols / 2 <= (int64_t)kBatchMaxSmem) {
+      cluster = 1;
+    } else {
+      for (int C = 2; C <= 16 && !cluster; C *= 2)
+        if (L_rows % C == 0 && L_rows / C >= 2 &&
+            (L_rows / C + 2) * (L_cols / 32) * 16 <= (int64_t)kBatchMaxSmem)
+          cluster = C;
+    }
+  }
+  if (cluster == 0 || (L_rows & 1) || n_lattices < 1 || n_lattices > 65535) {
+    g_last_error = "ising_batch_create: need L_rows even, L_cols % 64 == 0, 1 <= n <= 65535, and "
+                   "a lattice that fits one CTA's shared memory (L_rows * L_cols <= 409600) or a "
+                   "cluster of up to 16 (L_rows / C + 2) * L_cols / 2 <= 204800 bytes, e.g. 2048^2";
     return ISING_ERR_ARG;
   }
   ising_batch* b = new (std::nothrow) ising_batch;
@@ -2541,8 +2560,15 @@ int ising_batch_create(ising_batch_t* out, int64_t L_rows, int64_t L_cols, int n
   if (e == cudaSuccess) e = cudaEventCreate(&b->e0);
   if (e == cudaSuccess) e = cudaEventCreate(&b->e1);
   if (e != cudaSuccess) return fail(fail_cuda(e, "ising_batch_create", __LINE__));
-  b->threads = batch_threads((int)b->N, (int)b->W);
-  b->smem = (size_t)(2 * b->N * b->W) * sizeof(uint64_t);
+  b->cluster = cluster;
+  if (cluster == 1) {
+    b->threads = batch_threads((int)b->N, (int)b->W);
+    b->smem = (size_t)(2 * b->N * b->W) * sizeof(uint64_t);
+  } else {
+    const int R = (int)(b->N / cluster);
+    b->threads = batch_threads(R, (int)b->W);
+    b->smem = (size_t)(2 * (R + 2) * b->W) * sizeof(uint64_t);
+  }
   *out = b;
   return ISING_OK;
 }
@@ -2636,7 +2662,7 @@ int ising_batch_observables(ising_batch_t b, int64_t* up_counts, int64_t* bond_e
   p.measure_only = 1;
   p.n_samples = 1;
   p.obs = b->obs;
-  CU(launch_batch_sweeps(false, false, b->n, b->threads, b->smem, b->d.stream, p));
+  CU(batch_launch_sweeps(b, false, false, p));
   std::vector<unsigned long long> host;
   try {
     host.resize((size_t)b->n * 2);

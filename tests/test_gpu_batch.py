@@ -102,6 +102,48 @@ def test_batch_many_lattices_spot_checks():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("N,M,n", [(1024, 512, 3), (1024, 1024, 2), (640, 1024, 2), (32, 16384, 2),
+                                   (2048, 2048, 1)])
+@pytest.mark.parametrize("rule", [ising.RULE_METROPOLIS, ising.RULE_HEATBATH])
+def test_cluster_batch_matches_oracle(N, M, n, rule):
+    # lattices beyond one CTA: a cluster of 2..16 CTAs per lattice, halos over DSMEM
+    seeds = [101 + 17 * k for k in range(n)]
+    betas = [[cases.BETA_TC, 0.0, 0.3][k % 3] for k in range(n)]
+    b = IsingBatch(N, M, seeds).set_beta(betas, rule).init_random()
+    try:
+        done = 0
+        for chunk in [1, 4]:
+            b.sweep(chunk)
+            done += chunk
+            up, E = b.observables()
+            for k in range(n):
+                o = oracle_for(N, M, seeds[k], betas[k], rule, "random").sweep(done)
+                assert np.array_equal(b.read_lattice(k), o.full()), f"lattice {k} t={done}"
+                assert (int(up[k]), int(E[k])) == o.observables()
+        u2, e2 = b.measure(3, 2)
+        for k in range(n):
+            o = oracle_for(N, M, seeds[k], betas[k], rule, "random").sweep(done)
+            ou, oE = o.chain(6)
+            assert u2[k].tolist() == [int(x) for x in ou[1::2]]
+            assert e2[k].tolist() == [int(x) for x in oE[1::2]]
+    finally:
+        b.close()
+
+
+@pytest.mark.gpu
+def test_cluster_batch_long_chain_equals_one_lattice_handle():
+    N = M = 2048
+    b = IsingBatch(N, M, [9, 10]).set_beta([cases.BETA_TC, 0.5]).init_random().sweep(5000)
+    try:
+        for k, (seed, beta) in enumerate([(9, cases.BETA_TC), (10, 0.5)]):
+            g = IsingLattice(N, M, seed).set_beta(beta).init_random().sweep(5000)
+            assert np.array_equal(b.read_lattice(k), g.read_lattice()), f"lattice {k}"
+            g.close()
+    finally:
+        b.close()
+
+
+@pytest.mark.gpu
 def test_batch_errors():
     with pytest.raises(ising.IsingError) as e:
         IsingBatch(63, 64, [1])                 # odd rows
@@ -110,7 +152,7 @@ def test_batch_errors():
         IsingBatch(64, 96, [1])                 # L_cols % 64
     assert e.value.status == ising.ISING_ERR_ARG
     with pytest.raises(ising.IsingError) as e:
-        IsingBatch(1024, 512, [1])              # both planes beyond one CTA's shared memory
+        IsingBatch(4096, 4096, [1])             # beyond a 16-CTA cluster's shared memory
     assert e.value.status == ising.ISING_ERR_ARG
     b = IsingBatch(64, 64, [1, 2])
     try:

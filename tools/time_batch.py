@@ -49,6 +49,12 @@ def main():
         row["batch_592_measured_every_8"] = batch(L, 592, sweeps, every=8)
         rows.append(row)
         print(json.dumps(row), flush=True)
+    # lattices beyond one CTA: thread-block clusters (1024^2: 4 CTAs, 2048^2: 16 CTAs each)
+    for L, sweeps, ns in [(1024, 128, [1, 8, 37, 74, 148]), (2048, 64, [1, 4, 9, 18, 36])]:
+        row = {"L": L, "sweeps": sweeps, "one_lattice_flips_per_ns": one_lattice(L, sweeps),
+               "cluster_batch": {n: batch(L, n, sweeps) for n in ns}}
+        rows.append(row)
+        print(json.dumps(row), flush=True)
     if args.out:
         with open(args.out, "w") as f:
             json.dump(rows, f, indent=1)
