@@ -133,3 +133,23 @@ def test_async_measure_errors():
     assert err.value.status == ising.ISING_ERR_ARG
     with pytest.raises(ValueError):
         g.measure_async(2, 1, np.zeros(1, dtype=np.int64), np.zeros(2, dtype=np.int64))
+
+
+def test_batch_equilibrium_matches_onsager_at_the_papers_sizes():
+    # lattice batches (one CTA / one thread-block cluster per chain): PAPER.md Fig. 5 check at
+    # 512^2 (one CTA) and 1024^2 (4-CTA clusters) below Tc, 8 replicas per temperature
+    from paper_1906_06297_b200.ising import IsingBatch
+
+    temps = [2.0, 2.15]
+    for L, sweeps in [(512, 20000), (1024, 12000)]:
+        chains = [(T, r) for T in temps for r in range(8)]
+        b = IsingBatch(L, L, [31 + 7 * q for q in range(len(chains))])
+        b.set_beta([1.0 / T for T, _ in chains]).init_cold().sweep(2000)
+        ups, Es = b.measure(sweeps // 20, 20)
+        b.close()
+        for i, T in enumerate(temps):
+            rows = slice(8 * i, 8 * i + 8)
+            m = np.abs(2 * ups[rows] - L * L) / (L * L)
+            e = Es[rows] / (L * L)
+            assert abs(m.mean() - exact.onsager_m(T)) <= 5e-4, (L, T, m.mean())
+            assert abs(e.mean() - exact.onsager_energy(T)) <= 5e-4, (L, T, e.mean())
