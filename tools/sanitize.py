@@ -2,7 +2,8 @@
 virtual slabs with R = 2, heat bath (0 / 1 / 2 "always" classes), draw-free, the TMA-staged
 kernel (shared memory + mbarrier, ragged band), both basic-layout kernels, measured chain,
 graph replay, the asynchronous measured chain, the rank transports in self-exchange form
-(p2p flags / fences, NCCL self send-recv), and (SANITIZE_BIG=1) the guided tail.  (Not the
+(p2p flags / fences, NCCL self send-recv), lattice batches (one CTA and thread-block-cluster
+forms), and (SANITIZE_BIG=1) the guided tail.  (Not the
 same-process rank groups: the sanitizer serialises kernels, and a rank's phase that waits on
 another rank's flags can then never see them.)"""
 import os
@@ -59,6 +60,17 @@ for name, mk in (("p2p-self", lambda: ising.ising_create_rank_p2p(96, 8192, 8, 0
     print(name, x.observables())
     x.close()
 os.environ.pop("ISING_SELF_EXCHANGE")
+from paper_1906_06297_b200.ising import IsingBatch  # noqa: E402
+
+# lattice batches: one CTA per lattice (shared-memory planes, row bands) and thread-block
+# clusters (halo rows over distributed shared memory, cluster barriers, DSMEM atomics)
+for (N, M, n), rule in (((64, 128, 3), 0), ((96, 192, 2), 1), ((1024, 512, 2), 0), ((1024, 512, 2), 1)):
+    bt = IsingBatch(N, M, list(range(n))).set_beta([0.3, 0.4406868, 0.0][:n], rule).init_random()
+    bt.sweep(3)
+    bt.measure(2, 2)
+    bt.write_lattice(0, bt.read_lattice(1), t=bt.t)
+    print("batch", N, M, rule, bt.observables()[1].tolist())
+    bt.close()
 if os.environ.get("SANITIZE_BIG"):  # >= 3 waves: the staged kernel's guided tail (memcheck)
     big = IsingLattice(7168, 32768, 9).set_beta(0.4406868).init_random()
     big.sweep(1)
