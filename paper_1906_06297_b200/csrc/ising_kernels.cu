@@ -1503,8 +1503,8 @@ namespace ising {
 #ifndef ISING_BATCH_BANDS
 #define ISING_BATCH_BANDS 1
 #endif
-// MR: Metropolis variant of the lockstep acceptance — 0 when every lattice of the batch has
-// both thresholds below 2^32 (the fast path of the big kernels), else 2 (generic).
+// MR: the lockstep acceptance variant all lattices share (0 / 2 Metropolis, 3 / 5 / 6 / 7 heat
+// bath); HB: the generic per-lane heat bath instead (lattices of different heat-bath classes).
 template <bool HB, int MR = 2>
 __global__ void __launch_bounds__(kBatchMaxThreads) k_batch_sweeps(const BatchParams P) {
   extern __shared__ uint4 batch_smem[];
@@ -1658,11 +1658,21 @@ static cudaError_t batch_launch(int n_lattices, int threads, size_t smem, cudaSt
   return cudaGetLastError();
 }
 
-cudaError_t launch_batch_sweeps(bool heat_bath, bool fast, int n_lattices, int threads, size_t smem,
+// variant: the kernel variant every lattice of the batch shares (kernel_variant's numbering:
+// 0 / 2 Metropolis, 3 / 5 / 6 / 7 heat bath, lockstep draws), 1 = generic heat bath (lattices
+// of different heat-bath classes)
+cudaError_t launch_batch_sweeps(int variant, int n_lattices, int threads, size_t smem,
                                 cudaStream_t st, const BatchParams& p) {
-  if (heat_bath) return batch_launch<true, 2>(n_lattices, threads, smem, st, p);
-  return fast ? batch_launch<false, 0>(n_lattices, threads, smem, st, p)
-              : batch_launch<false, 2>(n_lattices, threads, smem, st, p);
+  switch (variant) {
+    case 0: return batch_launch<false, 0>(n_lattices, threads, smem, st, p);
+    case 2: return batch_launch<false, 2>(n_lattices, threads, smem, st, p);
+    case 3: return batch_launch<false, 3>(n_lattices, threads, smem, st, p);
+    case 5: return batch_launch<false, 5>(n_lattices, threads, smem, st, p);
+    case 6: return batch_launch<false, 6>(n_lattices, threads, smem, st, p);
+    case 7: return batch_launch<false, 7>(n_lattices, threads, smem, st, p);
+    case 1: return batch_launch<true, 2>(n_lattices, threads, smem, st, p);
+  }
+  return cudaErrorInvalidValue;
 }
 
 // Lattices too large for one CTA's shared memory (up to 2048^2): a thread-block cluster of
@@ -1825,12 +1835,18 @@ static cudaError_t cluster_launch(int n_lattices, int cluster, int threads, size
   return cudaLaunchKernelEx(&cfg, k_batch_cluster_sweeps<HB, MR>, p);
 }
 
-cudaError_t launch_batch_cluster_sweeps(bool heat_bath, bool fast, int n_lattices, int cluster,
-                                        int threads, size_t smem, cudaStream_t st,
-                                        const BatchParams& p) {
-  if (heat_bath) return cluster_launch<true, 2>(n_lattices, cluster, threads, smem, st, p);
-  return fast ? cluster_launch<false, 0>(n_lattices, cluster, threads, smem, st, p)
-              : cluster_launch<false, 2>(n_lattices, cluster, threads, smem, st, p);
+cudaError_t launch_batch_cluster_sweeps(int variant, int n_lattices, int cluster, int threads,
+                                        size_t smem, cudaStream_t st, const BatchParams& p) {
+  switch (variant) {
+    case 0: return cluster_launch<false, 0>(n_lattices, cluster, threads, smem, st, p);
+    case 2: return cluster_launch<false, 2>(n_lattices, cluster, threads, smem, st, p);
+    case 3: return cluster_launch<false, 3>(n_lattices, cluster, threads, smem, st, p);
+    case 5: return cluster_launch<false, 5>(n_lattices, cluster, threads, smem, st, p);
+    case 6: return cluster_launch<false, 6>(n_lattices, cluster, threads, smem, st, p);
+    case 7: return cluster_launch<false, 7>(n_lattices, cluster, threads, smem, st, p);
+    case 1: return cluster_launch<true, 2>(n_lattices, cluster, threads, smem, st, p);
+  }
+  return cudaErrorInvalidValue;
 }
 
 // Random / cold start of every lattice of a batch (row a3 with each lattice's seed): spin +1

@@ -240,13 +240,12 @@ __host__ __device__ inline int batch_threads(int N, int W) {
   return (batch_bands(N, W) * (W / 2) + 31) / 32 * 32;
 }
 constexpr size_t kBatchMaxSmem = 200 * 1024;  // both planes, bytes
-// fast: every lattice has both Metropolis thresholds below 2^32 (kernel variant 0)
-cudaError_t launch_batch_sweeps(bool heat_bath, bool fast, int n_lattices, int threads, size_t smem,
+// variant: kernel variant shared by every lattice (0 / 2 / 3 / 5 / 6 / 7), 1 = generic heat bath
+cudaError_t launch_batch_sweeps(int variant, int n_lattices, int threads, size_t smem,
                                 cudaStream_t st, const BatchParams& p);
 // Lattices beyond one CTA: a thread-block cluster of `cluster` CTAs per lattice.
-cudaError_t launch_batch_cluster_sweeps(bool heat_bath, bool fast, int n_lattices, int cluster,
-                                        int threads, size_t smem, cudaStream_t st,
-                                        const BatchParams& p);
+cudaError_t launch_batch_cluster_sweeps(int variant, int n_lattices, int cluster, int threads,
+                                        size_t smem, cudaStream_t st, const BatchParams& p);
 cudaError_t launch_batch_init(int n_lattices, int cold, cudaStream_t st, const BatchParams& p);
 cudaError_t launch_batch_unpack(int lattice, cudaStream_t st, const BatchParams& p, int8_t* full);
 cudaError_t launch_batch_pack(int lattice, cudaStream_t st, const BatchParams& p, const int8_t* full,

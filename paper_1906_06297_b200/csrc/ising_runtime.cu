@@ -2418,7 +2418,7 @@ struct ising_batch {
   BatchLattice* lat_dev = nullptr;
   std::vector<BatchLattice> lat;
   int rule = ISING_RULE_METROPOLIS;
-  bool fast = false;  // Metropolis, every lattice's T3, T4 < 2^32: kernel variant 0
+  int variant = 2;  // kernel variant every lattice shares (kernel_variant's numbering), 1: mixed HB
   bool beta_set = false, state_set = false;
   uint64_t t = 0;
   double last_ms = 0;
@@ -2469,9 +2469,25 @@ int batch_ensure_obs(ising_batch* b, size_t entries) {
   return ISING_OK;
 }
 
-cudaError_t batch_launch_sweeps(const ising_batch* b, bool heat, bool fast, const BatchParams& p) {
-  if (b->cluster == 1) return launch_batch_sweeps(heat, fast, b->n, b->threads, b->smem, b->d.stream, p);
-  return launch_batch_cluster_sweeps(heat, fast, b->n, b->cluster, b->threads, b->smem, b->d.stream, p);
+// A lattice's kernel variant (kernel_variant's numbering, without the draw-free 4: batches
+// always draw): 0 / 2 Metropolis, 7 / 3 / 5 / 6 heat bath.
+int variant_of(int rule, const uint64_t T[5], const Accept& acc) {
+  if (rule == ISING_RULE_METROPOLIS) return (acc.keep3 & acc.keep4) == 0xffffffffu ? 0 : 2;
+  const uint64_t two32p1 = (uint64_t(1) << 32) + 1;
+  if (!env_is_zero("ISING_HB_SYMMETRIC") && T[2] == (uint64_t(1) << 31) && T[0] + T[4] == two32p1 &&
+      T[1] + T[3] == two32p1)
+    return 7;
+  switch (acc.always_mask) {
+    case 0: return 3;
+    case 1: return 5;
+    case 3: return 6;
+    default: return 1;
+  }
+}
+
+cudaError_t batch_launch_sweeps(const ising_batch* b, int variant, const BatchParams& p) {
+  if (b->cluster == 1) return launch_batch_sweeps(variant, b->n, b->threads, b->smem, b->d.stream, p);
+  return launch_batch_cluster_sweeps(variant, b->n, b->cluster, b->threads, b->smem, b->d.stream, p);
 }
 
 // sweeps t + 1 .. t + n (every > 0: observables after every `every` sweeps into slots
@@ -2481,7 +2497,6 @@ int batch_run(ising_batch* b, int64_t n, int64_t every, int64_t n_samples) {
   CU(cudaSetDevice(b->d.dev));
   CU(cudaEventRecord(b->e0, b->d.stream));
   int64_t done = 0;
-  const bool heat = b->rule == ISING_RULE_HEATBATH;
   while (done < n) {
     const int64_t chunk = std::min<int64_t>(n - done, kBatchSweepsPerLaunch);
     BatchParams p = batch_params(b);
@@ -2493,7 +2508,7 @@ int batch_run(ising_batch* b, int64_t n, int64_t every, int64_t n_samples) {
       p.s_base = (uint32_t)done;
       p.obs = b->obs;
     }
-    CU(batch_launch_sweeps(b, heat, b->fast, p));
+    CU(batch_launch_sweeps(b, b->variant, p));
     done += chunk;
   }
   CU(cudaEventRecord(b->e1, b->d.stream));
@@ -2583,14 +2598,15 @@ int ising_batch_set_beta(ising_batch_t b, const double* betas, int rule) {
     return ISING_ERR_ARG;
   for (int k = 0; k < b->n; ++k)
     if (std::isnan(betas[k]) || betas[k] < 0) return ISING_ERR_ARG;
-  bool fast = rule == ISING_RULE_METROPOLIS;
+  int variant = -1;  // the lattices' common kernel variant, if they share one
   for (int k = 0; k < b->n; ++k) {
     uint64_t T[5];
     compute_thresholds(betas[k], rule, T);
     b->lat[k].acc = make_accept(T);
-    fast = fast && (b->lat[k].acc.keep3 & b->lat[k].acc.keep4) == 0xffffffffu;
+    const int v = variant_of(rule, T, b->lat[k].acc);
+    variant = (k == 0 || v == variant) ? v : (rule == ISING_RULE_METROPOLIS ? 2 : 1);
   }
-  b->fast = fast;
+  b->variant = variant;
   CU(cudaSetDevice(b->d.dev));
   CU(cudaMemcpyAsync(b->lat_dev, b->lat.data(), sizeof(BatchLattice) * b->n,
                      cudaMemcpyHostToDevice, b->d.stream));
@@ -2662,7 +2678,7 @@ int ising_batch_observables(ising_batch_t b, int64_t* up_counts, int64_t* bond_e
   p.measure_only = 1;
   p.n_samples = 1;
   p.obs = b->obs;
-  CU(batch_launch_sweeps(b, false, false, p));
+  CU(batch_launch_sweeps(b, 2, p));  // observables only: no acceptance
   std::vector<unsigned long long> host;
   try {
     host.resize((size_t)b->n * 2);

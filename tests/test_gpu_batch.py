@@ -143,6 +143,29 @@ def test_cluster_batch_long_chain_equals_one_lattice_handle():
         b.close()
 
 
+HB_BETAS = [cases.BETA_TC, 0.2, 3.0, 6.0, math.inf, 0.0, 0.3377438395041983]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("beta", HB_BETAS)
+@pytest.mark.parametrize("sym", ["1", "0"])
+@pytest.mark.parametrize("N,M", [(64, 128), (1024, 512)])
+def test_batch_heatbath_variants_match_oracle(monkeypatch, beta, sym, N, M):
+    # all lattices at one beta: the batch runs that beta's lockstep heat-bath variant (7
+    # symmetric, else 3 / 5 / 6 by the number of "always" classes), one CTA or a cluster
+    monkeypatch.setenv("ISING_HB_SYMMETRIC", sym)
+    seeds = [3, 4]
+    b = IsingBatch(N, M, seeds).set_beta([beta, beta], ising.RULE_HEATBATH).init_random().sweep(5)
+    try:
+        up, E = b.observables()
+        for k in range(2):
+            o = oracle_for(N, M, seeds[k], beta, 1, "random").sweep(5)
+            assert np.array_equal(b.read_lattice(k), o.full()), f"beta {beta} lattice {k}"
+            assert (int(up[k]), int(E[k])) == o.observables()
+    finally:
+        b.close()
+
+
 @pytest.mark.gpu
 def test_batch_errors():
     with pytest.raises(ising.IsingError) as e:
