@@ -105,3 +105,22 @@ def test_connect_local_argument_errors():
     assert lib.ising_p2p_connect_local(arr, 2) == ising.ISING_ERR_ARG
     assert lib.ising_p2p_connect_local(arr, 0) == ising.ISING_ERR_ARG
     assert lib.ising_p2p_connect_local(arr, 9) == ising.ISING_ERR_ARG
+
+
+def test_batch_shape_rules_without_gpu():
+    # ising_batch_create validates the shape (one CTA, or a cluster of <= 16 CTAs whose row
+    # bands + halos fit 200 KB each) before any device call
+    for N, M in [(63, 64), (64, 96), (64, 32), (4096, 4096), (2048, 4096), (3, 8192), (0, 64)]:
+        with pytest.raises(ising.IsingError) as ei:
+            ising.IsingBatch(N, M, [1])
+        assert ei.value.status == ising.ISING_ERR_ARG, (N, M)
+    with pytest.raises(ising.IsingError) as ei:
+        ising.IsingBatch(64, 64, [])          # no lattices
+    assert ei.value.status == ising.ISING_ERR_ARG
+    import torch
+
+    if not torch.cuda.is_available():         # valid shapes reach the device: an error here
+        for N, M in [(64, 64), (640, 640), (1024, 1024), (2048, 2048)]:
+            with pytest.raises(ising.IsingError) as ei:
+                ising.IsingBatch(N, M, [1, 2])
+            assert ei.value.status in (ising.ISING_ERR_CUDA, ising.ISING_ERR_DEVICE), (N, M)
