@@ -393,6 +393,28 @@ def scaling_leg(name: str, kind: str, n: int, steps: int, warmup: int, R: Ranks)
     return out
 
 
+def batch_leg(L: int, n_lattices: int, sweeps: int) -> dict:
+    """Aggregate flips/ns of `n_lattices` independent L x L lattices (seeds 1.., beta_c) as one
+    lattice batch (ising_batch_*: one CTA, or one thread-block cluster, per lattice) against
+    one-lattice handles of the same size (launch-bound there), device-timed."""
+    import numpy as np
+
+    from paper_1906_06297_b200.ising import IsingBatch, IsingLattice
+
+    b = IsingBatch(L, L, list(range(1, n_lattices + 1))).set_beta(np.full(n_lattices, BETA))
+    b.init_random().sweep(4)
+    b.sweep(sweeps)
+    value = n_lattices * L * L * sweeps / (b.last_sweep_ms() * 1e6)
+    b.close()
+    one = IsingLattice(L, L, 1).set_beta(BETA).init_random().sweep(16)
+    one.sweep(sweeps)
+    one_value = L * L * sweeps / (one.last_sweep_ms() * 1e6)
+    one.close()
+    return {"lattices": n_lattices, "sweeps": sweeps, "value": value, "unit": "flips/ns",
+            "one_lattice_handle_value": one_value, "speedup": value / one_value,
+            "engine": "one CTA per lattice" if L * L <= 409600 else "thread-block cluster per lattice"}
+
+
 def single_process_leg(N: int, M: int, n: int, steps: int, R: Ranks) -> dict | None:
     """ising_create(N, M, seed, n) from rank 0 (all n devices in one process; same-device
     runs: n virtual slabs on cuda:0), device-timed; the other ranks wait at the barrier."""
@@ -692,6 +714,9 @@ def run_ours(args):
     if main_legs:
         legs["c4_strong"] = scaling_leg("c4_strong", "strong", n, max(4, min(args.steps, 32)), 2, R)
         legs["c5_weak"] = scaling_leg("c5_weak", "weak", n, max(2, min(args.steps, 8)), 1, R)
+    if main_legs and n == 1:
+        # temperature-scan workloads — many small lattices as one batch
+        legs["batch_scan"] = {"64x64": batch_leg(64, 2368, 2048), "1024x1024": batch_leg(1024, 148, 32)}
 
     cpu = None
     if rank == 0 and n == 1 and not args.no_cpu_baseline:
