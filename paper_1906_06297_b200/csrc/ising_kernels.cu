@@ -445,6 +445,48 @@ __device__ __forceinline__ void philox8(uint32_t t, uint32_t c1base, uint32_t co
   for (int b = 0; b < 8; ++b) out[b] = make_uint4(c0[b], c1[b], c2[b], c3[b]);
 }
 
+// philox8 with round 1's per-block product given: for colour <= 1, round 0 leaves block b's
+// counter word 0 at (c1base + b) ^ k0[0] (hi(colour * M1) = 0), so round 1's c0 * M0 depends on
+// the column only — a thread that keeps its column for many rows / sweeps computes
+// P1[b] = ((c1base + b) ^ k0[0]) * M0 once (philox8_round1) and saves 8 multiplies per call.
+__device__ __forceinline__ void philox8_round1(uint32_t c1base, const PhiloxKeys& K, uint64_t (&P1)[8]) {
+#pragma unroll
+  for (int b = 0; b < 8; ++b) P1[b] = (uint64_t)((c1base + b) ^ K.k0[0]) * kPhiloxM0;
+}
+__device__ __forceinline__ void philox8_pre(uint32_t t, uint32_t colour, uint32_t row,
+                                            const PhiloxKeys& K, const uint64_t (&P1)[8],
+                                            uint4 (&out)[8]) {
+  const uint64_t q0 = (uint64_t)t * kPhiloxM0;  // round 0, warp-uniform
+  const uint32_t c1r0 = colour * kPhiloxM1;      // lo(colour * M1); hi = 0
+  const uint32_t n2 = (uint32_t)(q0 >> 32) ^ row ^ K.k1[0];
+  const uint32_t c3r0 = (uint32_t)q0;
+  const uint64_t q1 = (uint64_t)n2 * kPhiloxM1;  // round 1, warp-uniform half
+  uint32_t c0[8], c1[8], c2[8], c3[8];
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    c0[b] = (uint32_t)(q1 >> 32) ^ c1r0 ^ K.k0[1];
+    c1[b] = (uint32_t)q1;
+    c2[b] = (uint32_t)(P1[b] >> 32) ^ c3r0 ^ K.k1[1];
+    c3[b] = (uint32_t)P1[b];
+  }
+#pragma unroll
+  for (int r = 2; r < 10; ++r) {
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      const uint64_t p0 = (uint64_t)c0[b] * kPhiloxM0;
+      const uint64_t p1 = (uint64_t)c2[b] * kPhiloxM1;
+      const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1[b] ^ K.k0[r];
+      const uint32_t n2b = (uint32_t)(p0 >> 32) ^ c3[b] ^ K.k1[r];
+      c1[b] = (uint32_t)p1;
+      c3[b] = (uint32_t)p0;
+      c0[b] = n0;
+      c2[b] = n2b;
+    }
+  }
+#pragma unroll
+  for (int b = 0; b < 8; ++b) out[b] = make_uint4(c0[b], c1[b], c2[b], c3[b]);
+}
+
 // Metropolis (RULE 0) acceptance of one word from its four precomputed blocks rb[0..3]
 // (block q serves lanes 4q .. 4q + 3), same Horner order as update_word_metropolis.
 template <int RULE>
@@ -1503,6 +1545,9 @@ namespace ising {
 #ifndef ISING_BATCH_BANDS
 #define ISING_BATCH_BANDS 1
 #endif
+#ifndef ISING_BATCH_PRE
+#define ISING_BATCH_PRE 1
+#endif
 // MR: the lockstep acceptance variant all lattices share (0 / 2 Metropolis, 3 / 5 / 6 / 7 heat
 // bath); HB: the generic per-lane heat bath instead (lattices of different heat-bath classes).
 template <bool HB, int MR = 2>
@@ -1536,6 +1581,10 @@ __global__ void __launch_bounds__(kBatchMaxThreads) k_batch_sweeps(const BatchPa
   const int i0 = band < bands ? band * H : N, i1 = min(i0 + H, N);
   const int wwest = w == 0 ? W - 1 : w - 1, weast = w + 2 == W ? 0 : w + 2;
   (void)items;
+#if ISING_BATCH_PRE
+  uint64_t P1[8];
+  philox8_round1((uint32_t)(4 * w), L.keys, P1);
+#endif
 #endif
   const uint32_t total = P.measure_only ? 1u : P.sweeps;
   for (uint32_t s = 1; s <= total; ++s) {
@@ -1597,7 +1646,11 @@ __global__ void __launch_bounds__(kBatchMaxThreads) k_batch_sweeps(const BatchPa
             t1w = update_word<1>(t1w, n1, c1, s1, side1, ctr0 + 4, (uint32_t)i, t, p);
           } else {
             uint4 rb[8];
+#if ISING_BATCH_BANDS && ISING_BATCH_PRE
+            philox8_pre(t, (uint32_t)c, (uint32_t)i, L.keys, P1, rb);
+#else
             philox8(t, ctr0, (uint32_t)c, (uint32_t)i, L.keys, rb);
+#endif
             t0w = word_from_draws<MR>(t0w, n0, c0, s0, side0, rb, p);
             t1w = word_from_draws<MR>(t1w, n1, c1, s1, side1, rb + 4, p);
           }
@@ -1722,6 +1775,10 @@ __global__ void __launch_bounds__(kBatchMaxThreads) k_batch_cluster_sweeps(const
   const int i0 = band < bands ? band * H : R, i1 = min(i0 + H, R);
   const int wwest = w == 0 ? W - 1 : w - 1, weast = w + 2 == W ? 0 : w + 2;
   const int grow0 = r * R;  // global row of local row 0
+#if ISING_BATCH_PRE
+  uint64_t P1[8];
+  philox8_round1((uint32_t)(4 * w), L.keys, P1);
+#endif
   const uint32_t total = P.measure_only ? 1u : P.sweeps;
   for (uint32_t s = 1; s <= total; ++s) {
     const uint32_t t = P.t0 + s;
@@ -1766,7 +1823,11 @@ __global__ void __launch_bounds__(kBatchMaxThreads) k_batch_cluster_sweeps(const
               t1w = update_word<1>(t1w, n1, c1, s1, side1, (uint32_t)(4 * w + 4), (uint32_t)gi, t, p);
             } else {
               uint4 rb[8];
+#if ISING_BATCH_PRE
+              philox8_pre(t, (uint32_t)c, (uint32_t)gi, L.keys, P1, rb);
+#else
               philox8(t, (uint32_t)(4 * w), (uint32_t)c, (uint32_t)gi, L.keys, rb);
+#endif
               t0w = word_from_draws<MR>(t0w, n0, c0, s0, side0, rb, p);
               t1w = word_from_draws<MR>(t1w, n1, c1, s1, side1, rb + 4, p);
             }
