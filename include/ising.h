@@ -285,7 +285,7 @@ int ising_probe_philox(int device, double* draws_per_ns);
  * 200 KB — up to 2048 x 2048), halo rows moving through distributed shared memory.  Every
  * lattice follows exactly the contract of a one-lattice handle with the same seed and beta
  * (same draws, thresholds and update order): bit-identical results.  Limits: L_rows even,
- * L_cols % 64 == 0, a lattice that fits as above, 1 <= n <= 65535; else ARG.
+ * L_cols % 64 == 0, L_cols <= 32768, a lattice that fits as above, 1 <= n <= 65535; else ARG.
  * The handle owns its device memory; calls synchronise before returning; not thread-safe. */
 typedef struct ising_batch* ising_batch_t;
 /* seeds: n values (lattice k draws with seeds[k]); device: CUDA device index. */

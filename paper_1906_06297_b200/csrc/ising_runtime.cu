@@ -2528,7 +2528,9 @@ int ising_batch_create(ising_batch_t* out, int64_t L_rows, int64_t L_cols, int n
   // CTAs per lattice: one if both planes fit its shared memory, else the smallest cluster
   // (2 .. 16 CTAs, dividing L_rows) whose row bands plus halo rows fit
   int cluster = 0;
-  if (L_rows >= 2 && L_cols >= 64 && L_cols % 64 == 0 && L_rows <= 65536 && L_cols <= 65536) {
+  // (a CTA has a thread per 128-bit column pair of a row: L_cols / 64 <= kBatchMaxThreads)
+  if (L_rows >= 2 && L_cols >= 64 && L_cols % 64 == 0 && L_rows <= 65536 &&
+      L_cols / 64 <= kBatchMaxThreads) {
     if (L_rows * L_cols / 2 <= (int64_t)kBatchMaxSmem) {
       cluster = 1;
     } else {

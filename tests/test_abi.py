@@ -110,7 +110,8 @@ def test_connect_local_argument_errors():
 def test_batch_shape_rules_without_gpu():
     # ising_batch_create validates the shape (one CTA, or a cluster of <= 16 CTAs whose row
     # bands + halos fit 200 KB each) before any device call
-    for N, M in [(63, 64), (64, 96), (64, 32), (4096, 4096), (2048, 4096), (3, 8192), (0, 64)]:
+    for N, M in [(63, 64), (64, 96), (64, 32), (4096, 4096), (2048, 4096), (3, 8192), (0, 64),
+                 (2, 65536)]:  # (2, 65536): more column pairs per row than a CTA has threads
         with pytest.raises(ising.IsingError) as ei:
             ising.IsingBatch(N, M, [1])
         assert ei.value.status == ising.ISING_ERR_ARG, (N, M)
