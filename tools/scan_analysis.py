@@ -50,12 +50,12 @@ def main(paths):
     by_l = {}
     for r in rows:
         by_l.setdefault(r["L"], []).append(r)
-    print("# Long GPU temperature scans (round 1)\n")
-    print(f"Tc = {TC:.6f}, U* = {U_STAR} (L -> inf). Chains: `tools/scan_long.sh` "
+    print("# GPU temperature scans\n")
+    print(f"Tc = {TC:.6f}, U* = {U_STAR} (L -> inf). Chains: `tools/scan.py` / `tools/scan_long.sh` "
           "(cold starts, device-side measured chains).\n")
     print("## Binder cumulant U_L(T)\n")
-    ts = sorted({r["T"] for r in rows if r["L"] <= 512})
-    ls = sorted(l for l in by_l if l <= 512)
+    ts = sorted({r["T"] for r in rows if "binder" in r})
+    ls = sorted(by_l)
     print("| T | " + " | ".join(f"U_{l}" for l in ls) + " |")
     print("|---|" + "---|" * len(ls))
     for t in ts:
