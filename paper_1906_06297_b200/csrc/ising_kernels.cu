@@ -1542,12 +1542,6 @@ namespace ising {
 // batch is bit-identical to a one-lattice handle and to the oracle.  Metropolis runs the
 // generic lockstep form (RULE 2: any beta, thresholds at 2^32 masked), heat bath the generic
 // per-lane form (RULE 1).
-#ifndef ISING_BATCH_BANDS
-#define ISING_BATCH_BANDS 1
-#endif
-#ifndef ISING_BATCH_PRE
-#define ISING_BATCH_PRE 1
-#endif
 // MR: the lockstep acceptance variant all lattices share (0 / 2 Metropolis, 3 / 5 / 6 / 7 heat
 // bath); HB: the generic per-lane heat bath instead (lattices of different heat-bath classes).
 template <bool HB, int MR = 2>
@@ -1571,21 +1565,15 @@ __global__ void __launch_bounds__(kBatchMaxThreads) k_batch_sweeps(const BatchPa
   HalfSweepParams p{};
   p.acc = L.acc;
   if constexpr (HB) p.keys = L.keys;
-  const int half = W / 2;  // a thread updates two words (one 128-bit chunk) per item
-  const int items = N * half;
-#if ISING_BATCH_BANDS
+  const int half = W / 2;  // a thread updates two words (one 128-bit chunk) per row
   const int bands = batch_bands(N, W);
   const int H = (N + bands - 1) / bands;
   const int band = (int)threadIdx.x / half;
   const int w = 2 * ((int)threadIdx.x - band * half);
   const int i0 = band < bands ? band * H : N, i1 = min(i0 + H, N);
   const int wwest = w == 0 ? W - 1 : w - 1, weast = w + 2 == W ? 0 : w + 2;
-  (void)items;
-#if ISING_BATCH_PRE
-  uint64_t P1[8];
+  uint64_t P1[8];  // round 1's column-only Philox products (philox8_pre)
   philox8_round1((uint32_t)(4 * w), L.keys, P1);
-#endif
-#endif
   const uint32_t total = P.measure_only ? 1u : P.sweeps;
   for (uint32_t s = 1; s <= total; ++s) {
     const uint32_t t = P.t0 + s;
@@ -1595,11 +1583,9 @@ __global__ void __launch_bounds__(kBatchMaxThreads) k_batch_sweeps(const BatchPa
       uint64_t* tgt = sm + c * plane_words;
       const uint64_t* src = sm + (1 - c) * plane_words;
       if (P.measure_only && c == 0) continue;
-#if ISING_BATCH_BANDS
       // a thread owns column pair `w` of a band of consecutive rows [i0, i1) and rolls the
       // north / centre source words down it (one 128-bit load of the south pair per row, as
-      // the staged kernel does); the round-2 Philox products, which depend on the column only,
-      // stay out of the row loop
+      // the staged kernel does)
       if (i0 < i1) {
         const ulonglong2 nn = *reinterpret_cast<const ulonglong2*>(src + (i0 == 0 ? N - 1 : i0 - 1) * W + w);
         const ulonglong2 cc = *reinterpret_cast<const ulonglong2*>(src + i0 * W + w);
@@ -1617,61 +1603,31 @@ __global__ void __launch_bounds__(kBatchMaxThreads) k_batch_sweeps(const BatchPa
             side0 = splice_east(c0, c1);
             side1 = splice_east(c1, src[ro + weast]);
           }
-          ulonglong2 tv = *reinterpret_cast<const ulonglong2*>(tgt + ro + w);
+          const ulonglong2 tv = *reinterpret_cast<const ulonglong2*>(tgt + ro + w);
           uint64_t t0w = tv.x, t1w = tv.y;
-#else
-      for (int it = threadIdx.x; it < items; it += blockDim.x) {
-        const int i = it / half;
-        const int w = 2 * (it - i * half);
-        const int im = i == 0 ? N - 1 : i - 1, ip = i == N - 1 ? 0 : i + 1;
-        const uint64_t n0 = src[im * W + w], n1 = src[im * W + w + 1];
-        const uint64_t c0 = src[i * W + w], c1 = src[i * W + w + 1];
-        const uint64_t s0 = src[ip * W + w], s1 = src[ip * W + w + 1];
-        const bool west = ((i & 1) == 0) == (c == 0);  // reading R2
-        uint64_t side0, side1;
-        if (west) {
-          side0 = splice_west(c0, src[i * W + (w == 0 ? W - 1 : w - 1)]);
-          side1 = splice_west(c1, c0);
-        } else {
-          side0 = splice_east(c0, c1);
-          side1 = splice_east(c1, src[i * W + (w + 2 == W ? 0 : w + 2)]);
-        }
-        uint64_t t0w = tgt[i * W + w], t1w = tgt[i * W + w + 1];
-#endif
-        if (!P.measure_only) {
-          const uint32_t ctr0 = (uint32_t)(4 * w);
-          if constexpr (HB) {
-            p.colour = (uint32_t)c;
-            t0w = update_word<1>(t0w, n0, c0, s0, side0, ctr0, (uint32_t)i, t, p);
-            t1w = update_word<1>(t1w, n1, c1, s1, side1, ctr0 + 4, (uint32_t)i, t, p);
-          } else {
-            uint4 rb[8];
-#if ISING_BATCH_BANDS && ISING_BATCH_PRE
-            philox8_pre(t, (uint32_t)c, (uint32_t)i, L.keys, P1, rb);
-#else
-            philox8(t, ctr0, (uint32_t)c, (uint32_t)i, L.keys, rb);
-#endif
-            t0w = word_from_draws<MR>(t0w, n0, c0, s0, side0, rb, p);
-            t1w = word_from_draws<MR>(t1w, n1, c1, s1, side1, rb + 4, p);
+          if (!P.measure_only) {
+            if constexpr (HB) {
+              const uint32_t ctr0 = (uint32_t)(4 * w);
+              p.colour = (uint32_t)c;
+              t0w = update_word<1>(t0w, n0, c0, s0, side0, ctr0, (uint32_t)i, t, p);
+              t1w = update_word<1>(t1w, n1, c1, s1, side1, ctr0 + 4, (uint32_t)i, t, p);
+            } else {
+              uint4 rb[8];
+              philox8_pre(t, (uint32_t)c, (uint32_t)i, L.keys, P1, rb);
+              t0w = word_from_draws<MR>(t0w, n0, c0, s0, side0, rb, p);
+              t1w = word_from_draws<MR>(t1w, n1, c1, s1, side1, rb + 4, p);
+            }
+            *reinterpret_cast<ulonglong2*>(tgt + ro + w) = make_ulonglong2(t0w, t1w);
           }
-#if ISING_BATCH_BANDS
-          *reinterpret_cast<ulonglong2*>(tgt + ro + w) = make_ulonglong2(t0w, t1w);
-#else
-          tgt[i * W + w] = t0w;
-          tgt[i * W + w + 1] = t1w;
-#endif
-        }
-        if (c == 1 && measure) {  // every bond has exactly one white end (row a8)
-          obs_word(t0w, n0, c0, s0, side0, up, anti);
-          obs_word(t1w, n1, c1, s1, side1, up, anti);
-        }
-#if ISING_BATCH_BANDS
+          if (c == 1 && measure) {  // every bond has exactly one white end (row a8)
+            obs_word(t0w, n0, c0, s0, side0, up, anti);
+            obs_word(t1w, n1, c1, s1, side1, up, anti);
+          }
           n0 = c0;
           n1 = c1;
           c0 = s0;
           c1 = s1;
         }
-#endif
       }
       __syncthreads();
     }
@@ -1775,10 +1731,8 @@ __global__ void __launch_bounds__(kBatchMaxThreads) k_batch_cluster_sweeps(const
   const int i0 = band < bands ? band * H : R, i1 = min(i0 + H, R);
   const int wwest = w == 0 ? W - 1 : w - 1, weast = w + 2 == W ? 0 : w + 2;
   const int grow0 = r * R;  // global row of local row 0
-#if ISING_BATCH_PRE
-  uint64_t P1[8];
+  uint64_t P1[8];  // round 1's column-only Philox products (philox8_pre)
   philox8_round1((uint32_t)(4 * w), L.keys, P1);
-#endif
   const uint32_t total = P.measure_only ? 1u : P.sweeps;
   for (uint32_t s = 1; s <= total; ++s) {
     const uint32_t t = P.t0 + s;
@@ -1823,11 +1777,7 @@ __global__ void __launch_bounds__(kBatchMaxThreads) k_batch_cluster_sweeps(const
               t1w = update_word<1>(t1w, n1, c1, s1, side1, (uint32_t)(4 * w + 4), (uint32_t)gi, t, p);
             } else {
               uint4 rb[8];
-#if ISING_BATCH_PRE
               philox8_pre(t, (uint32_t)c, (uint32_t)gi, L.keys, P1, rb);
-#else
-              philox8(t, (uint32_t)(4 * w), (uint32_t)c, (uint32_t)gi, L.keys, rb);
-#endif
               t0w = word_from_draws<MR>(t0w, n0, c0, s0, side0, rb, p);
               t1w = word_from_draws<MR>(t1w, n1, c1, s1, side1, rb + 4, p);
             }
