@@ -38,10 +38,12 @@ def main():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--replicas", type=int, default=1, help="independent chains per (L, T)")
     ap.add_argument("--no-batch", action="store_true", help="one handle per chain")
+    ap.add_argument("--rule", choices=["metropolis", "heatbath"], default="metropolis")
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     rows = []
     ns = a.sweeps // a.every
+    rule = 1 if a.rule == "heatbath" else 0
     for L in a.sizes:
         series = {}  # k -> (ups, Es) concatenated over the replicas
         t0 = time.perf_counter()
@@ -54,7 +56,7 @@ def main():
             except IsingError:
                 b = None
         if b is not None:
-            b.set_beta([1.0 / a.temps[k] for k, _ in chains]).init_cold()
+            b.set_beta([1.0 / a.temps[k] for k, _ in chains], rule).init_cold()
             b.sweep(a.discard)
             ups, Es = b.measure(ns, a.every)
             b.close()
@@ -66,7 +68,7 @@ def main():
             for k, T in enumerate(a.temps):
                 us, es = [], []
                 for r in range(a.replicas):
-                    g = IsingLattice(L, L, a.seed + 1000 * k + L + 7919 * r).set_beta(1.0 / T).init_cold()
+                    g = IsingLattice(L, L, a.seed + 1000 * k + L + 7919 * r).set_beta(1.0 / T, rule).init_cold()
                     g.sweep(a.discard)
                     u, e = g.measure(ns, a.every)
                     g.close()
@@ -94,7 +96,7 @@ def main():
                    "E_site_se": float(np.std(eb, ddof=1) / math.sqrt(nb)), "m2": m2, "m4": m4,
                    "binder": 1 - m4 / (3 * m2 * m2), "binder_paper_literal": 1 - m4 / (m2 * m2),
                    "binder_se": float(math.sqrt((nb - 1) / nb * np.sum((jk - np.mean(jk)) ** 2))),
-                   "samples": len(m), "replicas": a.replicas, "engine": engine,
+                   "samples": len(m), "replicas": a.replicas, "engine": engine, "rule": a.rule,
                    "seconds_for_all_T_at_this_L": seconds}
             rows.append(row)
             print(json.dumps(row), flush=True)
