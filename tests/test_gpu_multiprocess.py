@@ -167,3 +167,64 @@ def test_rank_p2p_matches_oracle(world, N, M):
     ou2, oE2 = o.chain(2)
     assert ups == [int(x) for x in ou[1::2]] + [int(x) for x in ou2], "measured chain (up)"
     assert Es == [int(x) for x in oE[1::2]] + [int(x) for x in oE2], "measured chain (E)"
+
+
+def _large_worker(rank, world, port, N, M, seed, beta, sweeps, q):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    from paper_1906_06297_b200.ising import IsingLattice
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        lat = IsingLattice.distributed(N, M, seed, device=0, transport="p2p")
+        row0, rows = lat.slab_info()
+        lat.set_beta(beta).init_random()
+        for chunk in (1, sweeps - 1):  # a short call, then one long one
+            lat.sweep(chunk)
+        mine = np.empty((rows, M), dtype=np.int8)
+        lat.read_lattice(mine)
+        digest = np.frombuffer(mine.tobytes(), dtype=np.uint64).sum(dtype=np.uint64)
+        parts = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(parts, torch.tensor([int(digest) & (2**62 - 1)], dtype=torch.int64))
+        obs = lat.observables()
+        lat.close()
+        if rank == 0:
+            q.put(("ok", ([int(p.item()) for p in parts], obs)))
+    except Exception as e:  # pragma: no cover - reported to the parent
+        q.put(("error", f"rank {rank}: {e!r}"))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_rank_p2p_large_lattice_equals_one_handle():
+    """4 processes x 1024-row slabs of a 4096 x 8192 lattice (TMA-staged kernel: edge bands wait
+    on the flags, 50 interior bands do not), 200 sweeps, against one handle of the whole lattice
+    on the same GPU — slab digests and the all-reduced observables."""
+    from paper_1906_06297_b200.ising import IsingLattice
+
+    world, N, M, seed, beta, sweeps = 4, 4096, 8192, 21, 0.4406868, 200
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_large_worker, args=(r, world, port, N, M, seed, beta, sweeps, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    status, payload = q.get(timeout=900)
+    for p in procs:
+        p.join(timeout=120)
+    assert status == "ok", payload
+    digests, obs = payload
+    g = IsingLattice(N, M, seed).set_beta(beta).init_random().sweep(sweeps)
+    full = g.read_lattice()
+    R = N // world
+    want = [int(np.frombuffer(full[r * R:(r + 1) * R].tobytes(), dtype=np.uint64).sum(dtype=np.uint64))
+            & (2**62 - 1) for r in range(world)]
+    assert digests == want
+    assert obs == g.observables()
+    g.close()
