@@ -1661,7 +1661,9 @@ template <bool HB, int MR>
 static cudaError_t batch_launch(int n_lattices, int threads, size_t smem, cudaStream_t st,
                                 const BatchParams& p) {
   cudaError_t e = cudaFuncSetAttribute((const void*)k_batch_sweeps<HB, MR>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)kBatchMaxSmem);  // one value for every handle:
+                                                              // no race between threads
   if (e != cudaSuccess) return e;
   k_batch_sweeps<HB, MR><<<n_lattices, threads, smem, st>>>(p);
   return cudaGetLastError();
@@ -1827,7 +1829,8 @@ template <bool HB, int MR>
 static cudaError_t cluster_launch(int n_lattices, int cluster, int threads, size_t smem,
                                   cudaStream_t st, const BatchParams& p) {
   const void* f = (const void*)k_batch_cluster_sweeps<HB, MR>;
-  cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e =
+      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBatchMaxSmem);
   if (e == cudaSuccess && cluster > 8)
     e = cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (e != cudaSuccess) return e;
