@@ -2439,7 +2439,7 @@ void batch_free(ising_batch* b) {
   if (!b) return;
   if (b->d.dev >= 0) {
     cudaSetDevice(b->d.dev);
-    cudaDeviceSynchronize();
+    if (b->d.stream) cudaStreamSynchronize(b->d.stream);  // this handle's work only
     for (void* p : {(void*)b->planes, (void*)b->lat_dev, (void*)b->obs, (void*)b->full, (void*)b->bad})
       if (p) cudaFree(p);
     if (b->e0) cudaEventDestroy(b->e0);
@@ -2490,8 +2490,8 @@ cudaError_t batch_launch_sweeps(const ising_batch* b, int variant, const BatchPa
   return launch_batch_cluster_sweeps(variant, b->n, b->cluster, b->threads, b->smem, b->d.stream, p);
 }
 
-// sweeps t + 1 .. t + n (every > 0: observables after every `every` sweeps into slots
-// sample0.., n_samples per lattice), in launches of at most kBatchSweepsPerLaunch sweeps
+// sweeps t + 1 .. t + n (every > 0: observables after every `every` sweeps into slot
+// s / every - 1 of each lattice's n_samples), in launches of at most kBatchSweepsPerLaunch
 int batch_run(ising_batch* b, int64_t n, int64_t every, int64_t n_samples) {
   NvtxRange r("ising_batch_sweeps %lld x %lld lattices", (long long)n, (long long)b->n);
   CU(cudaSetDevice(b->d.dev));
