@@ -771,7 +771,7 @@ int trace_mark(ising_ctx* h, const char* name, cudaStream_t st, const char* stre
 
 void trace_dump(ising_ctx* h) {
   if (h->trace.empty()) return;
-  cudaDeviceSynchronize();
+  for (auto& t : h->trace) cudaEventSynchronize(t.ev);  // this handle's events only
   FILE* f = fopen(h->trace_path.c_str(), "w");
   if (f) {
     fprintf(f, "phase,name,stream,ms\n");
