@@ -304,9 +304,11 @@ int ising_batch_sweep(ising_batch_t b, int64_t n);
  * (n * n_samples entries each, caller-owned). */
 int ising_batch_sweep_measure(ising_batch_t b, int64_t n_samples, int64_t every,
                               int64_t* up_counts, int64_t* bond_energies);
-/* Current (up count, bond energy) of every lattice (n entries each). */
+/* Current (up count, bond energy) of every lattice (n entries each); STATE before an init /
+ * write. */
 int ising_batch_observables(ising_batch_t b, int64_t* up_counts, int64_t* bond_energies);
-/* Lattice `lattice` as +-1 bytes, row-major; out_len >= L_rows * L_cols (else RANGE). */
+/* Lattice `lattice` as +-1 bytes, row-major; out_len >= L_rows * L_cols (else RANGE); lattice
+ * outside 0 .. n-1 -> ARG; STATE before an init / write. */
 int ising_batch_read_lattice(ising_batch_t b, int lattice, int8_t* out, int64_t out_len);
 /* Load lattice `lattice` from +-1 bytes (in_len >= L_rows * L_cols, else RANGE; other values
  * -> ARG) and set the batch's sweep counter to t (shared by all lattices: the next sweep is
