@@ -1174,172 +1174,6 @@ cudaError_t launch_halfsweep_staged(int rule, int64_t slots, cudaStream_t st, Ha
   });
 }
 
-// Persistent, double-buffered form of the staged half-sweep (single slab, no peer flags, no
-// fused observables): one wave of CTAs, CTA j walking a contiguous range of (band, span) items
-// of kPRows rows, the next item's source tile loaded by TMA into the other buffer while this
-// one is computed — no block start-up per band and no partial last wave.  A tile row holds
-// words [w0 - 2, w0 + 258) of the span (the side words of the first and last thread included),
-// so no separate edge loads; mirror phases walk each CTA's range backwards (its first items
-// read what it wrote last in the previous phase).
-constexpr int kPRows = 10;
-constexpr int kPTileW = kStageWords + 4;
-constexpr size_t kPSmem = 2 * (size_t)(kPRows + 2) * kPTileW * sizeof(uint64_t);
-
-__device__ __forceinline__ void pstaged_issue(const uint64_t* src, int64_t W, int64_t w0, int ra,
-                                              int nrows, uint64_t* tile, uint32_t bar) {
-  const uint32_t bytes = (uint32_t)(nrows + 2) * kPTileW * 8;
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-  for (int rr = 0; rr < nrows + 2; ++rr) {
-    const uint64_t* g = src + (int64_t)(ra - 1 + rr) * W;
-    uint64_t* t = tile + rr * kPTileW;
-    // [w0 - 2, w0) | [w0, w0 + 256) | [w0 + 256, w0 + 258), each wrapping mod W
-    const int64_t lw = w0 == 0 ? W - 2 : w0 - 2;
-    const int64_t rw = w0 + kStageWords == W ? 0 : w0 + kStageWords;
-    if (lw + 2 == w0 && rw == w0 + kStageWords) {
-      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                   ::"r"(smem_u32(t)), "l"(g + lw), "r"((uint32_t)(kPTileW * 8)), "r"(bar) : "memory");
-    } else {
-      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                   ::"r"(smem_u32(t)), "l"(g + lw), "r"(16u), "r"(bar) : "memory");
-      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                   ::"r"(smem_u32(t + 2)), "l"(g + w0), "r"((uint32_t)(kStageWords * 8)), "r"(bar) : "memory");
-      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                   ::"r"(smem_u32(t + 2 + kStageWords)), "l"(g + rw), "r"(16u), "r"(bar) : "memory");
-    }
-  }
-}
-
-template <int RULE>
-__global__ void __launch_bounds__(kStageThreads, staged_minb(RULE)) k_halfsweep_pstaged(const HalfSweepParams p) {
-  if (p.pdl) {
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-  }
-  extern __shared__ __align__(128) uint64_t psm[];
-  __shared__ alignas(8) uint64_t mbar[2];
-  const int64_t W = p.W;
-  const int64_t spans = W / kStageWords;
-  const int rows = p.r_end - p.r_begin;
-  const int64_t bands = (rows + kPRows - 1) / kPRows;
-  const int64_t items = bands * spans;
-  const int64_t ib = items * blockIdx.x / gridDim.x, ie = items * (blockIdx.x + 1) / gridDim.x;
-  const int64_t n_it = ie - ib;
-  const uint64_t* src = p.src + W;  // local row r at src + r * W
-  uint64_t* tgt = p.tgt + W;
-  const uint32_t bar0 = smem_u32(&mbar[0]), bar1 = smem_u32(&mbar[1]);
-  const int tid = threadIdx.x;
-  const uint32_t t = p.t_dev ? *p.t_dev + p.t : p.t;
-  // item k of this CTA (mirror phases backwards) -> band, span, rows [ra, rb)
-  auto item_geom = [&](int64_t k, int& ra, int& rb, int64_t& w0) {
-    const int64_t it = p.mirror ? ie - 1 - k : ib + k;
-    const int64_t band = it / spans;
-    w0 = (it - band * spans) * kStageWords;
-    ra = p.r_begin + (int)band * kPRows;
-    rb = min(ra + kPRows, p.r_end);
-  };
-  if (tid == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0));
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar1));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    if (n_it > 0) {
-      int ra, rb;
-      int64_t w0;
-      item_geom(0, ra, rb, w0);
-      pstaged_issue(src, W, w0, ra, rb - ra, psm, bar0);
-    }
-  }
-  __syncthreads();
-  for (int64_t k = 0; k < n_it; ++k) {
-    const int b = (int)(k & 1);
-    uint64_t* tile = psm + (size_t)b * (kPRows + 2) * kPTileW;
-    if (tid == 0 && k + 1 < n_it) {  // prefetch the next item into the other buffer
-      int ra2, rb2;
-      int64_t w02;
-      item_geom(k + 1, ra2, rb2, w02);
-      pstaged_issue(src, W, w02, ra2, rb2 - ra2, psm + (size_t)(b ^ 1) * (kPRows + 2) * kPTileW,
-                    b ? bar0 : bar1);
-    }
-    int ra, rb;
-    int64_t w0;
-    item_geom(k, ra, rb, w0);
-    {
-      const uint32_t bar = b ? bar1 : bar0;
-      const uint32_t parity = (uint32_t)((k >> 1) & 1);  // k-th use of buffer b: phase k / 2
-      uint32_t done = 0;
-      while (!done)
-        asm volatile(
-            "{\n\t.reg .pred q;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, q;\n\t}"
-            : "=r"(done)
-            : "r"(bar), "r"(parity)
-            : "memory");
-    }
-    const int64_t wc = w0 + 2 * tid;
-    uint64_t* tp = tgt + (int64_t)ra * W + wc;
-    const int nrows = rb - ra;
-    for (int rr = 0; rr < nrows; ++rr, tp += W) {
-      const int r = ra + rr;
-      const int64_t gi = p.row0 + r;
-      const bool west = ((gi & 1) == 0) == (p.colour == 0);
-      const uint64_t* tn = tile + rr * kPTileW + 2 + 2 * tid;
-      const uint64_t n0 = tn[0], n1 = tn[1];
-      const uint64_t c0 = tn[kPTileW], c1 = tn[kPTileW + 1];
-      const uint64_t s0 = tn[2 * kPTileW], s1 = tn[2 * kPTileW + 1];
-      uint64_t side0, side1;
-      if (west) {
-        side0 = splice_west(c0, tn[kPTileW - 1]);
-        side1 = splice_west(c1, c0);
-      } else {
-        side0 = splice_east(c0, c1);
-        side1 = splice_east(c1, tn[kPTileW + 2]);
-      }
-      ulonglong2 tv = __ldcg(reinterpret_cast<const ulonglong2*>(tp));
-      const uint32_t ctr0 = (uint32_t)(4 * wc);
-      if constexpr (lockstep_rule(RULE)) {
-        uint4 rbk[8];
-        philox8(t, ctr0, p.colour, (uint32_t)gi, p.keys, rbk);
-        tv.x = word_from_draws<RULE>(tv.x, n0, c0, s0, side0, rbk, p);
-        tv.y = word_from_draws<RULE>(tv.y, n1, c1, s1, side1, rbk + 4, p);
-      } else {
-        tv.x = update_word<RULE>(tv.x, n0, c0, s0, side0, ctr0, (uint32_t)gi, t, p);
-        tv.y = update_word<RULE>(tv.y, n1, c1, s1, side1, ctr0 + 4, (uint32_t)gi, t, p);
-      }
-      *reinterpret_cast<ulonglong2*>(tp) = tv;
-      if (r == 0 && p.halo_up) *reinterpret_cast<ulonglong2*>(p.halo_up + wc) = tv;
-      if (r == p.R - 1 && p.halo_dn) *reinterpret_cast<ulonglong2*>(p.halo_dn + wc) = tv;
-    }
-    __syncthreads();  // buffer b free: item k + 2 is prefetched into it next iteration
-  }
-}
-
-cudaError_t launch_halfsweep_pstaged(int rule, int grid, cudaStream_t st, const HalfSweepParams& p) {
-  return dispatch_rule(rule, false, [&](auto R, auto) -> cudaError_t {
-    const void* f = (const void*)k_halfsweep_pstaged<decltype(R)::value>;
-    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPSmem);
-    if (e != cudaSuccess) return e;
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3((unsigned)grid);
-    cfg.blockDim = dim3(kStageThreads);
-    cfg.dynamicSmemBytes = kPSmem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = p.pdl ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, k_halfsweep_pstaged<decltype(R)::value>, p);
-  });
-}
-
-cudaError_t pstaged_occupancy(int* blocks_per_sm) {
-  cudaError_t e = cudaFuncSetAttribute((const void*)k_halfsweep_pstaged<0>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPSmem);
-  if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_halfsweep_pstaged<0>,
-                                                       kStageThreads, kPSmem);
-}
-
 cudaError_t staged_occupancy(int* blocks_per_sm) {
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_halfsweep_staged<0>,
                                                        kStageThreads, 0);

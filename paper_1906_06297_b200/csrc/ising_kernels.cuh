@@ -255,9 +255,6 @@ cudaError_t launch_batch_pack(int lattice, cudaStream_t st, const BatchParams& p
 cudaError_t launch_sync(cudaStream_t st, const SyncParams& p);
 cudaError_t launch_halfsweep_staged(int rule, int64_t slots, cudaStream_t st, HalfSweepParams p);
 cudaError_t staged_occupancy(int* blocks_per_sm);
-// Persistent double-buffered staged half-sweep (single slab, no peer flags / fused observables)
-cudaError_t launch_halfsweep_pstaged(int rule, int grid, cudaStream_t st, const HalfSweepParams& p);
-cudaError_t pstaged_occupancy(int* blocks_per_sm);
 cudaError_t launch_persistent(int rule, int grid, cudaStream_t st, const PersistentParams& P);
 cudaError_t persistent_occupancy(int* blocks_per_sm);
 cudaError_t launch_set_u32(cudaStream_t st, uint32_t* dst, uint32_t v, int add);

@@ -137,7 +137,6 @@ struct Device {
   int sms = 0;
   int hs_blocks_per_sm = 0;  // occupancy of k_halfsweep<0>
   int staged_blocks_per_sm = 0;  // occupancy of k_halfsweep_staged<0>
-  int pstaged_blocks_per_sm = 0;  // occupancy of k_halfsweep_pstaged<0>
   cudaStream_t stream = nullptr;
   cudaStream_t comm = nullptr;
   cudaEvent_t ev_phase = nullptr;  // end of the latest phase on this device
@@ -235,8 +234,6 @@ struct ising_ctx {
   bool persistent_enabled = false;         // opt-in (ISING_PERSISTENT=1): measured slower
                                            // than graph replay on B200 (grid barrier ~3 us)
   bool staged = true;                      // TMA-staged half-sweep (ISING_STAGED=0: off)
-  // persistent double-buffered form of it for single-slab, flag-free, unmeasured phases
-  bool pstaged = env_is_one("ISING_PSTAGED");
   bool guided_tail = !env_is_zero("ISING_TAIL");  // staged kernel: 8- / 4-row last waves
   bool pdl = !env_is_zero("ISING_PDL");  // staged kernel: programmatic dependent launch
   // staged kernel: white phases walk the bands bottom-up (ISING_MIRROR=0: off); C3 1552 ->
@@ -384,7 +381,6 @@ int setup_device(Device& d, int dev) {
   CU(halfsweep_occupancy(&d.hs_blocks_per_sm));
   if (d.hs_blocks_per_sm < 1) d.hs_blocks_per_sm = 1;
   CU(staged_occupancy(&d.staged_blocks_per_sm));
-  CU(pstaged_occupancy(&d.pstaged_blocks_per_sm));
   if (d.staged_blocks_per_sm < 1) d.staged_blocks_per_sm = 1;
   {  // once per device and process (see preload_kernels)
     static std::mutex mu;
@@ -668,10 +664,7 @@ int run_halfsweep(ising_ctx* h, Slab& s, int c, int r_begin, int r_end, uint64_t
   // previous phase wrote last (still in L2).  (Rank-p2p: the edge bands stay first in the grid;
   // mirroring swaps which rows the first and last logical band hold, both still edge rows.)
   p.mirror = (h->mirror && c == 1) ? 1 : 0;
-  if (h->pstaged && h->staged && h->W % kStageWords == 0 && !p.wait_flags && !p.obs_out &&
-      !p.obs_clear && !p.slot_dev) {
-    CU(launch_halfsweep_pstaged(kernel_variant(h), d.sms * d.pstaged_blocks_per_sm, d.stream, p));
-  } else if (h->staged && h->W % kStageWords == 0) {
+  if (h->staged && h->W % kStageWords == 0) {
     CU(launch_halfsweep_staged(kernel_variant(h),
                                h->guided_tail ? (int64_t)d.sms * d.staged_blocks_per_sm : 0, d.stream, p));
   } else {
