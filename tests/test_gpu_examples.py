@@ -39,3 +39,25 @@ def test_distributed_example_checkpoint_matches_oracle(tmp_path):
     up, E = o.observables()
     m = (2 * up - N * M) / (N * M)
     assert f"m={m:+.5f}" in lines[-1] and f"E/site={E / (N * M):+.5f}" in lines[-1]
+
+
+def test_scan_tool_batch_and_one_handle_paths_agree(tmp_path):
+    # tools/scan.py: the lattice-batch engine and one handle per chain give identical series
+    # (every batch lattice is bit-identical to a one-lattice handle with its seed)
+    import json
+
+    outs = []
+    for extra, name in (([], "batch"), (["--no-batch"], "single")):
+        path = tmp_path / f"{name}.json"
+        out = subprocess.run(
+            [sys.executable, os.path.join(ROOT, "tools", "scan.py"), "--sizes", "64", "128",
+             "--temps", "2.2", "2.4", "--sweeps", "2000", "--discard", "100", "--every", "10",
+             "--replicas", "2", "--out", str(path)] + extra,
+            capture_output=True, text=True, timeout=600, cwd=ROOT)
+        assert out.returncode == 0, out.stderr[-2000:]
+        outs.append(json.load(open(path)))
+    a, b = outs
+    assert [r["engine"] for r in a] == ["batch"] * 4 and [r["engine"] for r in b] == ["one handle per chain"] * 4
+    for ra, rb in zip(a, b):
+        for key in ("L", "T", "abs_m", "E_site", "m2", "m4", "binder", "samples"):
+            assert ra[key] == rb[key], (key, ra, rb)
