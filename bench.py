@@ -415,6 +415,25 @@ def batch_leg(L: int, n_lattices: int, sweeps: int) -> dict:
             "engine": "one CTA per lattice" if L * L <= 409600 else "thread-block cluster per lattice"}
 
 
+def batch_ranks_leg(L: int, n_lattices: int, sweeps: int, n: int, R: Ranks) -> dict:
+    """Each of the n ranks sweeps its own batch of n_lattices independent lattices (seeds
+    offset per rank) on its GPU; device time max over ranks."""
+    import numpy as np
+
+    from paper_1906_06297_b200.ising import IsingBatch
+
+    seeds = list(range(1 + R.rank * n_lattices, 1 + (R.rank + 1) * n_lattices))
+    b = IsingBatch(L, L, seeds, device=R.dev).set_beta(np.full(n_lattices, BETA))
+    b.init_random().sweep(4)
+    R.barrier()
+    b.sweep(sweeps)
+    ms = R.allmax(b.last_sweep_ms())
+    b.close()
+    return {"lattices_per_gpu": n_lattices, "sweeps": sweeps, "n_gpus": n,
+            "value": n * n_lattices * L * L * sweeps / (ms * 1e6), "unit": "flips/ns",
+            "scaling": "weak", "collective": "none (independent problems)"}
+
+
 def single_process_leg(N: int, M: int, n: int, steps: int, R: Ranks) -> dict | None:
     """ising_create(N, M, seed, n) from rank 0 (all n devices in one process; same-device
     runs: n virtual slabs on cuda:0), device-timed; the other ranks wait at the barrier."""
@@ -717,6 +736,10 @@ def run_ours(args):
     if main_legs and n == 1:
         # temperature-scan workloads — many small lattices as one batch
         legs["batch_scan"] = {"64x64": batch_leg(64, 2368, 2048), "1024x1024": batch_leg(1024, 148, 32)}
+    elif main_legs:
+        # independent lattices shard across ranks with no collective (weak scaling): every
+        # rank runs its own 64^2 x 2368 batch; aggregate = all ranks' flips / the slowest rank
+        legs["batch_scan"] = {"64x64": batch_ranks_leg(64, 2368, 2048, n, R)}
 
     cpu = None
     if rank == 0 and n == 1 and not args.no_cpu_baseline:
