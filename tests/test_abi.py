@@ -125,3 +125,19 @@ def test_batch_shape_rules_without_gpu():
             with pytest.raises(ising.IsingError) as ei:
                 ising.IsingBatch(N, M, [1, 2])
             assert ei.value.status in (ising.ISING_ERR_CUDA, ising.ISING_ERR_DEVICE), (N, M)
+
+
+def test_batch_calls_reject_null_handles_without_gpu():
+    lib = ising.load()
+    assert lib.ising_batch_destroy(None) == ising.ISING_OK
+    assert lib.ising_batch_create(None, 64, 64, 1, None, 0) == ising.ISING_ERR_ARG
+    assert lib.ising_batch_set_beta(None, None, 0) == ising.ISING_ERR_ARG
+    assert lib.ising_batch_init_random(None) == ising.ISING_ERR_ARG
+    assert lib.ising_batch_init_cold(None) == ising.ISING_ERR_ARG
+    assert lib.ising_batch_sweep(None, 1) == ising.ISING_ERR_ARG
+    assert lib.ising_batch_sweep_measure(None, 1, 1, None, None) == ising.ISING_ERR_ARG
+    assert lib.ising_batch_observables(None, None, None) == ising.ISING_ERR_ARG
+    assert lib.ising_batch_read_lattice(None, 0, None, 0) == ising.ISING_ERR_ARG
+    assert lib.ising_batch_write_lattice(None, 0, None, 0, 0) == ising.ISING_ERR_ARG
+    assert lib.ising_batch_last_sweep_ms(None, None) == ising.ISING_ERR_ARG
+    assert lib.ising_batch_get_sweep(None, None) == ising.ISING_ERR_ARG
