@@ -141,3 +141,22 @@ def test_batch_calls_reject_null_handles_without_gpu():
     assert lib.ising_batch_write_lattice(None, 0, None, 0, 0) == ising.ISING_ERR_ARG
     assert lib.ising_batch_last_sweep_ms(None, None) == ising.ISING_ERR_ARG
     assert lib.ising_batch_get_sweep(None, None) == ising.ISING_ERR_ARG
+
+
+def test_every_handle_call_rejects_a_null_handle():
+    # every exported call that takes a handle returns ISING_ERR_ARG for NULL (destroy: a no-op),
+    # with NULL / zero for the remaining arguments — no crash, no device access
+    import ctypes
+
+    lib = ising.load()
+    no_handle = {"ising_create", "ising_create_slabs", "ising_create_rank", "ising_nccl_unique_id",
+                 "ising_create_rank_p2p", "ising_create_rank_lsa", "ising_create_basic",
+                 "ising_probe_philox", "ising_strerror", "ising_last_error", "ising_batch_create",
+                 "ising_p2p_connect_local"}
+    for name, (_, args) in ising.SIGNATURES.items():
+        if name in no_handle:
+            continue
+        vals = [None if (a is ctypes.c_void_p or (isinstance(a, type) and issubclass(a, ctypes._Pointer)))
+                else 0 for a in args]
+        want = ising.ISING_OK if name.endswith("destroy") else ising.ISING_ERR_ARG
+        assert getattr(lib, name)(*vals) == want, name
